@@ -1,0 +1,179 @@
+"""ctypes handles on the test-only checkers. TEST INFRASTRUCTURE ONLY.
+
+`load_oracle()` -> oracle/_build/liboracle.so (the CPU restatement, lattice_oracle.c)
+`load_ref()`    -> oracle/_ref/libref.so (the reference headers compiled in place, ref_shim.cpp)
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg may import this
+package. The product (paper_2512_09200_b200) never does.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_U64 = ctypes.c_uint64
+_I32 = ctypes.c_int32
+_SZ = ctypes.c_size_t
+_D = ctypes.c_double
+
+
+def ptr(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+class LoNetCfg(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("d", ctypes.c_int), ("blocks", ctypes.c_int),
+                ("nF", ctypes.c_int), ("nL", ctypes.c_int), ("k", ctypes.c_int),
+                ("n_mlp", ctypes.c_int), ("mlp", ctypes.c_int * 6), ("G", ctypes.c_int),
+                ("heads", ctypes.c_int), ("tower_hidden", ctypes.c_int), ("hard", ctypes.c_int),
+                ("bf16", ctypes.c_int)]
+
+
+class LoNetWeights(ctypes.Structure):
+    _fields_ = [("YT", _P), ("WL", _P), ("mlp", _P), ("T1", _P), ("T2", _P)]
+
+
+_oracle = None
+_ref = None
+
+
+def load_oracle():
+    global _oracle
+    if _oracle is None:
+        lib = ctypes.CDLL(os.path.join(_HERE, "_build", "liboracle.so"))
+        lib.lo_xxh64.restype = _U64
+        lib.lo_xxh64.argtypes = [_P, _SZ, _U64]
+        lib.lo_gen.restype = _U64
+        lib.lo_gen.argtypes = [_U64, _U64, _U64]
+        lib.lo_signature.restype = _SZ
+        lib.lo_signature.argtypes = [ctypes.c_char_p, ctypes.c_uint32, ctypes.c_char_p,
+                                     ctypes.c_uint32, _I64, _P]
+        lib.lo_assign_window.restype = ctypes.c_int
+        lib.lo_assign_window.argtypes = [ctypes.c_char_p, ctypes.c_uint32, ctypes.c_char_p,
+                                         ctypes.c_uint32, _I64, _U64, _P, ctypes.c_int]
+        lib.lo_zip_columns.restype = _I64
+        lib.lo_zip_columns.argtypes = [_I64, _P, _P, _P, _P, _P, ctypes.c_int, _P, _P,
+                                       ctypes.c_int, _P, _P, _U64, _P, _P, _P]
+        for name in ("lo_rms_norm", "lo_swish_rn", "lo_swish_rn_hard"):
+            f = getattr(lib, name)
+            f.restype = ctypes.c_int
+            f.argtypes = [_P, _SZ, _D, _P]
+        lib.lo_table_value.restype = ctypes.c_float
+        lib.lo_table_value.argtypes = [_U64, _I64, _I64, ctypes.c_int, _I64, _I64]
+        lib.lo_weight_value.restype = ctypes.c_float
+        lib.lo_weight_value.argtypes = [_U64, _U64, _I64, _I64, _I64]
+        lib.lo_weight_tag.restype = _U64
+        lib.lo_weight_tag.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        lib.lo_weight_shift.restype = ctypes.c_int
+        lib.lo_weight_shift.argtypes = [_I64]
+        lib.lo_embedding_bag_synth.restype = _I64
+        lib.lo_embedding_bag_synth.argtypes = [_U64, ctypes.c_int, _I64, ctypes.c_int, _I64,
+                                               _P, _P, _I64, _I64, _P, ctypes.c_int]
+        lib.lo_embedding_bag.restype = _I64
+        lib.lo_embedding_bag.argtypes = [ctypes.c_int, _P, ctypes.c_int, _I64, _P, _P, _P, _P]
+        lib.lo_net_forward.restype = None
+        lib.lo_net_forward.argtypes = [ctypes.POINTER(LoNetCfg), ctypes.POINTER(LoNetWeights),
+                                       _I64, _P, _P, _P, ctypes.c_int]
+        lib.lo_bf16_round.restype = ctypes.c_float
+        lib.lo_bf16_round.argtypes = [ctypes.c_float]
+        _oracle = lib
+    return _oracle
+
+
+def ref_available():
+    return os.path.exists(os.path.join(_HERE, "_ref", "libref.so"))
+
+
+def load_ref():
+    global _ref
+    if _ref is None:
+        lib = ctypes.CDLL(os.path.join(_HERE, "_ref", "libref.so"))
+        lib.ref_last_error.restype = ctypes.c_char_p
+        lib.ref_stable_hash.restype = _U64
+        lib.ref_stable_hash.argtypes = [_P, _SZ, _U64]
+        lib.ref_signature.restype = _SZ
+        lib.ref_signature.argtypes = [ctypes.c_char_p, ctypes.c_uint32, ctypes.c_char_p,
+                                      ctypes.c_uint32, _I64, _P]
+        lib.ref_zipper_config_check.restype = ctypes.c_int
+        lib.ref_zipper_config_check.argtypes = [ctypes.c_int, _P, _P, _U64]
+        lib.ref_assign_window.restype = ctypes.c_int
+        lib.ref_assign_window.argtypes = [ctypes.c_char_p, ctypes.c_uint32, ctypes.c_char_p,
+                                          ctypes.c_uint32, _I64, ctypes.c_int, _P, _P, _U64,
+                                          ctypes.POINTER(_I64)]
+        lib.ref_zip_dataset.restype = ctypes.c_int
+        lib.ref_zip_dataset.argtypes = [_I64, _P, _P, _P, _P, _P, ctypes.c_int, _P, _P,
+                                        ctypes.c_int, _P, _P, _U64, _P, _P]
+        for name in ("ref_rms_norm", "ref_swish_rn", "ref_swish_rn_hard"):
+            f = getattr(lib, name)
+            f.restype = ctypes.c_int
+            f.argtypes = [_P, _SZ, _D, _P]
+        _ref = lib
+    return _ref
+
+
+# ---- thin numpy conveniences ---------------------------------------------------------
+
+def xxh64(data: bytes, seed: int) -> int:
+    buf = np.frombuffer(data, dtype=np.uint8) if data else np.zeros(1, np.uint8)
+    return load_oracle().lo_xxh64(ptr(buf), len(data), seed)
+
+
+def pack_strings(strs):
+    """list[bytes] -> (uint8 bytes, int64 offsets[n+1])"""
+    offs = np.zeros(len(strs) + 1, dtype=np.int64)
+    offs[1:] = np.cumsum([len(s) for s in strs])
+    data = np.frombuffer(b"".join(strs), dtype=np.uint8).copy() if offs[-1] else np.zeros(1, np.uint8)
+    return data, offs
+
+
+def zip_columns(users, ads, ts, conv, conv_present, durations, probs, seed, lib=None):
+    """Oracle columnar zip. Returns (window u8[n], labels u8[n,T,W], err_record, err_task)."""
+    lib = lib or load_oracle()
+    n = len(users)
+    T = conv.shape[1] if conv.ndim == 2 else 0
+    W = len(durations)
+    ub, uo = pack_strings(users)
+    ab, ao = pack_strings(ads)
+    ts = np.ascontiguousarray(ts, dtype=np.int64)
+    conv = np.ascontiguousarray(conv, dtype=np.int64).reshape(n, T)
+    pres = np.ascontiguousarray(conv_present, dtype=np.uint8).reshape(n, T)
+    dur = np.ascontiguousarray(durations, dtype=np.int64)
+    pr = np.ascontiguousarray(probs, dtype=np.float64)
+    win = np.zeros(max(n, 1), np.uint8)
+    lab = np.zeros(max(n * T * W, 1), np.uint8)
+    et = ctypes.c_int32(-1)
+    err = lib.lo_zip_columns(n, ptr(ub), ptr(uo), ptr(ab), ptr(ao), ptr(ts), T, ptr(conv),
+                             ptr(pres), W, ptr(dur), ptr(pr), seed, ptr(win), ptr(lab),
+                             ctypes.byref(et))
+    return win[:n], lab[: n * T * W].reshape(n, T, W), int(err), int(et.value)
+
+
+def ref_zip_dataset(users, ads, ts, conv, conv_present, durations, probs, seed):
+    """Reference zip_dataset over columns: (rc, window, labels, message)."""
+    lib = load_ref()
+    n = len(users)
+    T = conv.shape[1]
+    W = len(durations)
+    ub, uo = pack_strings(users)
+    ab, ao = pack_strings(ads)
+    ts = np.ascontiguousarray(ts, dtype=np.int64)
+    conv = np.ascontiguousarray(conv, dtype=np.int64)
+    pres = np.ascontiguousarray(conv_present, dtype=np.uint8)
+    dur = np.ascontiguousarray(durations, dtype=np.int64)
+    pr = np.ascontiguousarray(probs, dtype=np.float64)
+    win = np.zeros(max(n, 1), np.uint8)
+    lab = np.zeros(max(n * T * W, 1), np.uint8)
+    rc = lib.ref_zip_dataset(n, ptr(ub), ptr(uo), ptr(ab), ptr(ao), ptr(ts), T, ptr(conv),
+                             ptr(pres), W, ptr(dur), ptr(pr), seed, ptr(win), ptr(lab))
+    msg = lib.ref_last_error().decode() if rc else ""
+    return rc, win[:n], lab[: n * T * W].reshape(n, T, W), msg
+
+
+def vec_op(lib, name, x, eps=1e-6):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.zeros(max(len(x), 1), np.float64)
+    rc = getattr(lib, name)(ptr(x) if len(x) else None, len(x), eps, ptr(out))
+    return rc, out[: len(x)]

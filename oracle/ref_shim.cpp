@@ -1,0 +1,132 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY. Exposes the reference's own header-only
+// functions (compiled from /root/reference/proj/include, never copied) behind a C ABI so
+// the tests can pin the oracle restatement and the CUDA path against the reference itself.
+// Built by oracle/Makefile into oracle/_ref/libref.so (git-ignored; travels to the GPU box).
+//
+// The reference headers are included under `#define lattice lattice_ref` so they cannot
+// collide with anything named lattice:: elsewhere ("verified by probe").
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#define lattice lattice_ref
+#include "lattice/core.hpp"
+#include "lattice/datasets.hpp"
+#include "lattice/numerics.hpp"
+#undef lattice
+
+namespace {
+thread_local std::string g_err;
+
+int copy_out(const std::vector<double>& v, double* out) {
+    std::memcpy(out, v.data(), v.size() * sizeof(double));
+    return 0;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const lattice_ref::UsageError& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const lattice_ref::DataError& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// core.hpp:84
+uint64_t ref_stable_hash(const uint8_t* data, size_t len, uint64_t seed) {
+    return lattice_ref::stable_hash(std::span<const std::uint8_t>(data, len), lattice_ref::Seed{seed});
+}
+
+// core.hpp:149-175, as used by datasets.hpp:181-184
+size_t ref_signature(const char* user, uint32_t ulen, const char* ad, uint32_t alen, int64_t ts,
+                     uint8_t* out) {
+    lattice_ref::ByteWriter w;
+    w.length_prefixed(std::string_view(user, ulen));
+    w.length_prefixed(std::string_view(ad, alen));
+    w.u64_be(static_cast<std::uint64_t>(ts));
+    std::memcpy(out, w.view().data(), w.view().size());
+    return w.view().size();
+}
+
+static lattice_ref::ZipperConfig make_config(int W, const int64_t* durations, const double* probs,
+                                             uint64_t seed) {
+    std::vector<lattice_ref::AttributionWindow> windows;
+    for (int i = 0; i < W; ++i) windows.push_back({"w" + std::to_string(i), durations[i]});
+    return lattice_ref::ZipperConfig::create(std::move(windows),
+                                             std::vector<double>(probs, probs + W),
+                                             lattice_ref::Seed{seed});
+}
+
+// datasets.hpp:60-84 validation only
+int ref_zipper_config_check(int W, const int64_t* durations, const double* probs, uint64_t seed) {
+    return guarded([&] {
+        make_config(W, durations, probs, seed);
+        return 0;
+    });
+}
+
+// datasets.hpp:179
+int ref_assign_window(const char* user, uint32_t ulen, const char* ad, uint32_t alen, int64_t ts,
+                      int W, const int64_t* durations, const double* probs, uint64_t seed,
+                      int64_t* out_window) {
+    return guarded([&] {
+        const auto cfg = make_config(W, durations, probs, seed);
+        *out_window = static_cast<int64_t>(lattice_ref::assign_window(
+            std::string_view(user, ulen), std::string_view(ad, alen), ts, cfg));
+        return 0;
+    });
+}
+
+// datasets.hpp:199 over columns. Tasks are named "t0".."t{T-1}". Returns 0 / 1 / 2 and
+// fills window[n], labels[n*T*W]. On DataError the message is in ref_last_error().
+int ref_zip_dataset(int64_t n, const char* user_bytes, const int64_t* user_off, const char* ad_bytes,
+                    const int64_t* ad_off, const int64_t* ts, int T, const int64_t* conv,
+                    const uint8_t* conv_present, int W, const int64_t* durations,
+                    const double* probs, uint64_t seed, uint8_t* window, uint8_t* labels) {
+    return guarded([&] {
+        const auto cfg = make_config(W, durations, probs, seed);
+        std::vector<std::string> tasks;
+        for (int t = 0; t < T; ++t) tasks.push_back("t" + std::to_string(t));
+        std::vector<lattice_ref::DomainRecord> recs(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) {
+            auto& r = recs[static_cast<size_t>(i)];
+            r.domain = "d";
+            r.user_id.assign(user_bytes + user_off[i], static_cast<size_t>(user_off[i + 1] - user_off[i]));
+            r.ad_id.assign(ad_bytes + ad_off[i], static_cast<size_t>(ad_off[i + 1] - ad_off[i]));
+            r.impression_time_ms = ts[i];
+            for (int t = 0; t < T; ++t)
+                if (conv_present[i * T + t]) r.conversions[tasks[static_cast<size_t>(t)]] = conv[i * T + t];
+        }
+        const auto z = lattice_ref::zip_dataset(recs, tasks, cfg);
+        for (int64_t i = 0; i < n; ++i) {
+            const auto& zr = z.records[static_cast<size_t>(i)];
+            window[i] = static_cast<uint8_t>(zr.assigned_window);
+            std::memcpy(labels + i * T * W, zr.window_labels.data(), static_cast<size_t>(T * W));
+        }
+        return 0;
+    });
+}
+
+// numerics.hpp:81-107
+int ref_rms_norm(const double* x, size_t n, double eps, double* out) {
+    return guarded([&] { return copy_out(lattice_ref::rms_norm(std::span<const double>(x, n), eps), out); });
+}
+int ref_swish_rn(const double* x, size_t n, double eps, double* out) {
+    return guarded([&] { return copy_out(lattice_ref::swish_rn(std::span<const double>(x, n), eps), out); });
+}
+int ref_swish_rn_hard(const double* x, size_t n, double eps, double* out) {
+    return guarded(
+        [&] { return copy_out(lattice_ref::swish_rn_hard(std::span<const double>(x, n), eps), out); });
+}
+
+}  // extern "C"
