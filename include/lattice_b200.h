@@ -1,0 +1,218 @@
+/*
+ * lattice_b200.h -- C ABI of the B200-native Lattice hot path (liblattice_b200.so).
+ *
+ * Plain pointers and sizes only; all array arguments are DEVICE pointers on the current
+ * CUDA device unless stated otherwise, caller-owned, and every call is ordered on the
+ * stream it is given. No call falls back to the CPU: without a usable sm_100a device the
+ * library returns LATTICE_CUDA.
+ *
+ * Status codes follow the reference's error model (proj/include/lattice/core.hpp:20-27,
+ * CLI exit codes proj/tools/lattice_cli.cpp:342-351): USAGE = UsageError (contract
+ * violation), DATA = DataError (bad input data). lattice_last_error() returns the message
+ * of the last failing call on this thread; lattice_last_error_index() the offending
+ * record / id index when the failure is a DATA error.
+ *
+ * Which reference interface each entry replaces is cited per declaration; INTEGRATION.md
+ * shows the C++ drop-in (include/lattice/ headers) and a ctypes binding.
+ */
+#ifndef LATTICE_B200_H
+#define LATTICE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LATTICE_OK = 0,
+    LATTICE_USAGE = 1, /* UsageError  (core.hpp:20-22) */
+    LATTICE_DATA = 2,  /* DataError   (core.hpp:25-27) */
+    LATTICE_CUDA = 3,
+    LATTICE_NCCL = 4
+} lattice_status;
+
+typedef enum { LATTICE_F32 = 0, LATTICE_BF16 = 1 } lattice_dtype;
+
+typedef struct CUstream_st* lattice_stream; /* == cudaStream_t; NULL = legacy default stream */
+
+const char* lattice_last_error(void);
+int64_t lattice_last_error_index(void);
+int lattice_abi_version(void); /* bumps on any signature change */
+
+/* ======================================================================================
+ * Hashing -- replaces lattice::stable_hash (core.hpp:84-145) for batches.
+ * Strings packed back to back in `bytes`, string i = bytes[off[i] .. off[i+1]).
+ * ==================================================================================== */
+lattice_status lattice_stable_hash(int64_t n, const uint8_t* bytes, const int64_t* off,
+                                   uint64_t seed, uint64_t* out, lattice_stream stream);
+
+/* ======================================================================================
+ * Zipper -- replaces lattice::ZipperConfig::create (datasets.hpp:60-84, validation),
+ * lattice::assign_window (datasets.hpp:179-194) and the label loop of
+ * lattice::zip_dataset (datasets.hpp:199-249), bit-exact.
+ * ==================================================================================== */
+/* Host-side validation of the numeric part of ZipperConfig::create: >= 1 window,
+ * durations > 0 and strictly increasing, probabilities >= 0 finite, |sum - 1| <= 1e-9.
+ * (Window names are checked by the C++ shim, include/lattice/datasets.hpp.) HOST pointers. */
+lattice_status lattice_zipper_validate(int32_t windows, const int64_t* durations_host,
+                                       const double* probabilities_host);
+
+typedef struct {
+    int64_t n;                  /* impressions */
+    const uint8_t* user_bytes;  /* packed user ids */
+    const int64_t* user_off;    /* [n+1] */
+    const uint8_t* ad_bytes;    /* packed ad ids */
+    const int64_t* ad_off;      /* [n+1] */
+    const int64_t* ts;          /* impression_time_ms [n] */
+    int32_t tasks;              /* T */
+    const int64_t* conv;        /* conversion time [n][T] */
+    const uint8_t* conv_present;/* [n][T]: 0 = no conversion for that task */
+    int32_t windows;            /* W (<= 255) */
+    const int64_t* durations_host;      /* [W] HOST */
+    const double* probabilities_host;   /* [W] HOST */
+    uint64_t seed;              /* ZipperConfig.seed */
+    uint8_t* window;            /* out [n] assigned window */
+    uint8_t* labels;            /* out [n][T][W] task-major per record (datasets.hpp:92) */
+    uint8_t* routed;            /* optional out [n][T]: label of the assigned window */
+    int32_t check;              /* 1: synchronise and return DATA on a negative delay */
+} lattice_zip_args;
+
+lattice_status lattice_zipper_assign_labels(const lattice_zip_args* args, lattice_stream stream);
+
+/* ======================================================================================
+ * Embedding bag ("embedding tables producing (B, |F_c|, d)"; no reference
+ * code -- semantics in DESIGN.md 3.1). Sum pooling, fp32 accumulation, empty bag -> 0.
+ * Bags in feature-major CSR: bag (f, b) = ids[offsets[f*batch + b] .. offsets[f*batch+b+1]).
+ * ==================================================================================== */
+typedef struct {
+    int32_t features;            /* F (tables in this call) */
+    int64_t batch;               /* B */
+    int32_t dim;                 /* D (multiple of 8) */
+    int32_t table_dtype;         /* lattice_dtype */
+    const void* const* tables;   /* DEVICE array [F] of device pointers to [rows_f][D] */
+    const int64_t* rows;         /* DEVICE [F] */
+    const int64_t* offsets;      /* DEVICE [F*B + 1] */
+    const int32_t* ids;          /* DEVICE */
+    int32_t out_dtype;           /* lattice_dtype */
+    void* out;                   /* out[pos(b)*out_row_stride + (out_feature_offset+f)*D + c] */
+    int64_t out_row_stride;      /* elements between samples (>= features*D) */
+    int32_t out_feature_offset;
+    const int32_t* sample_pos;   /* optional DEVICE [B]: output row of sample b (NULL = b) */
+    int32_t normalize;           /* 1: rms_norm over D of each pooled row (numerics.hpp:81) */
+    int32_t check;               /* 1: synchronise and return DATA on an id outside [0, rows) */
+} lattice_bag_args;
+
+lattice_status lattice_embedding_bag(const lattice_bag_args* args, lattice_stream stream);
+
+/* ======================================================================================
+ * Fused activations, row-wise -- replaces lattice::rms_norm / swish_rn / swish_rn_hard
+ * (numerics.hpp:81-107) for a [rows][width] fp32 matrix. Returns DATA on non-finite input
+ * (numerics.hpp:24) when check = 1. mode: 0 rms_norm, 1 swish_rn, 2 swish_rn_hard.
+ * ==================================================================================== */
+lattice_status lattice_rownorm(int32_t mode, int64_t rows, int64_t width, double eps,
+                               const float* x, float* out, int32_t check, lattice_stream stream);
+
+/* ======================================================================================
+ * Synthetic inputs: counter-based, identical to oracle/ so inputs
+ * never cross PCIe.
+ * ==================================================================================== */
+lattice_status lattice_fill_tables(void* tables, int32_t dtype, int32_t features, int64_t rows,
+                                   int32_t dim, uint64_t seed, int32_t feature_base,
+                                   int64_t rows_total, lattice_stream stream);
+lattice_status lattice_fill_weights(void* w, int32_t dtype, int64_t out_features,
+                                    int64_t fan_in, uint64_t seed, uint64_t tag,
+                                    lattice_stream stream);
+/* lengths L = H(seed,LEN,f*B+b) mod (max_len+1); ids = H(seed,ID,(f*B+b)*max_len+j) mod rows.
+ * offsets [F*B+1] are written; ids must hold F*B*max_len entries (upper bound). */
+lattice_status lattice_synth_bags(int32_t features, int64_t batch, int32_t max_len, int64_t rows,
+                                  uint64_t seed, int64_t* offsets, int32_t* ids,
+                                  lattice_stream stream);
+lattice_status lattice_synth_domains(int64_t batch, int32_t domains, uint64_t seed,
+                                     int32_t* domain, lattice_stream stream);
+
+/* ======================================================================================
+ * Domain bucketing (K6): stable counting sort of samples by domain. pos[b] = row of
+ * sample b in domain-sorted order; order[p] = b; seg[g] = first row of domain g (G+1).
+ * ==================================================================================== */
+lattice_status lattice_domain_bucket(int64_t batch, int32_t domains, const int32_t* domain,
+                                     int32_t* pos, int32_t* order, int32_t* seg,
+                                     lattice_stream stream);
+
+/* ======================================================================================
+ * Dense GEMM on tcgen05 (K3): C[M][N] = A[M][K] . B[N][K]^T, bf16 in, fp32 accumulate in
+ * TMEM, fused epilogue. Exposed for tests and for callers composing their own blocks.
+ * epilogue: 0 store (out_dtype), 1 swish_rn over each full row, 2 swish_rn_hard,
+ *           3 residual + rms_norm over groups of `group` columns.
+ * ==================================================================================== */
+typedef struct {
+    int64_t M, N, K;
+    const void* A;      /* bf16 [M][lda] */
+    int64_t lda;
+    const void* B;      /* bf16 [N][ldb] */
+    int64_t ldb;
+    void* C;            /* out_dtype [M][ldc] */
+    int64_t ldc;
+    int32_t out_dtype;
+    int32_t epilogue;
+    const void* resid;  /* bf16 [M][ldr] for epilogue 3 */
+    int64_t ldr;
+    int32_t group;      /* epilogue 3 group width (128 or 64) */
+} lattice_gemm_args;
+
+lattice_status lattice_gemm(const lattice_gemm_args* args, lattice_stream stream);
+
+/* ======================================================================================
+ * Network (K1 -> K2/K3 blocks -> K4 towers). No reference code; the
+ * arithmetic is DESIGN.md section 3 and oracle/lattice_oracle.c lo_net_forward.
+ * ==================================================================================== */
+typedef struct {
+    int32_t n;             /* embeddings per sample (= sparse features) */
+    int32_t d;             /* embedding dim */
+    int32_t blocks;
+    int32_t nF, nL, k;     /* nF + nL == n */
+    int32_t n_mlp;         /* FMB MLP weight matrices */
+    int32_t mlp[6];        /* widths: mlp[0] = n*k ... mlp[n_mlp] = nF*d */
+    int32_t domains;       /* G */
+    int32_t heads;         /* objectives * windows */
+    int32_t tower_hidden;
+    int32_t hard;          /* 1: swish_rn_hard */
+    int64_t max_batch;
+    uint64_t weight_seed;
+} lattice_net_config;
+
+typedef struct lattice_net lattice_net;
+
+lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** out);
+void lattice_net_destroy(lattice_net* net);
+/* Device pointer of a weight tensor (bf16): kind 1 Y^T [k][n], 2 W_L [nL][n],
+ * 3 MLP layer `index` [out][in], 4 tower W1 [G][tower_hidden][n*d], 5 tower W2 fp32
+ * [G][heads][tower_hidden]. block ignored for 4/5. */
+const void* lattice_net_weight(lattice_net* net, int32_t block, int32_t kind, int32_t index);
+
+typedef struct {
+    int64_t batch;
+    const int32_t* domain;       /* DEVICE [B] */
+    /* sparse input, as lattice_bag_args (features = cfg.n) */
+    int32_t table_dtype;
+    const void* const* tables;
+    const int64_t* rows;
+    const int64_t* offsets;
+    const int32_t* ids;
+    /* or, when tables == NULL: already pooled sums [B][n][d] in table_dtype */
+    const void* pooled;
+} lattice_batch;
+
+/* logits: DEVICE fp32 [B][heads] in the caller's sample order. */
+lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch, float* logits,
+                                   lattice_stream stream);
+/* Per-stage CUDA-event times (ms) of the last forward when timing was enabled. */
+lattice_status lattice_net_set_timing(lattice_net* net, int32_t enable);
+lattice_status lattice_net_stage_times(lattice_net* net, float* ms, int32_t max_stages,
+                                       int32_t* n_stages);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

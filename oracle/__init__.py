@@ -77,6 +77,10 @@ def load_oracle():
         lib.lo_net_forward.restype = None
         lib.lo_net_forward.argtypes = [ctypes.POINTER(LoNetCfg), ctypes.POINTER(LoNetWeights),
                                        _I64, _P, _P, _P, ctypes.c_int]
+        lib.lo_synth_bags.restype = None
+        lib.lo_synth_bags.argtypes = [ctypes.c_int, _I64, ctypes.c_int, _I64, _U64, _P, _P]
+        lib.lo_synth_domains.restype = None
+        lib.lo_synth_domains.argtypes = [_I64, ctypes.c_int, _U64, _P]
         lib.lo_bf16_round.restype = ctypes.c_float
         lib.lo_bf16_round.argtypes = [ctypes.c_float]
         _oracle = lib
@@ -177,3 +181,34 @@ def vec_op(lib, name, x, eps=1e-6):
     out = np.zeros(max(len(x), 1), np.float64)
     rc = getattr(lib, name)(ptr(x) if len(x) else None, len(x), eps, ptr(out))
     return rc, out[: len(x)]
+
+
+def synth_bags(F, B, max_len, rows, seed):
+    lib = load_oracle()
+    offsets = np.zeros(F * B + 1, np.int64)
+    ids = np.zeros(max(F * B * max_len, 1), np.int32)
+    lib.lo_synth_bags(F, B, max_len, rows, seed, ptr(offsets), ptr(ids))
+    return offsets, ids[: offsets[-1]]
+
+
+def synth_domains(B, G, seed):
+    dom = np.zeros(B, np.int32)
+    load_oracle().lo_synth_domains(B, G, seed, ptr(dom))
+    return dom
+
+
+def embedding_bag_synth(seed, F, rows, D, B, offsets, ids, b_lo=0, b_hi=None, threads=0):
+    """Exact fp32 pooled sums of samples [b_lo, b_hi) over the synthetic tables."""
+    b_hi = B if b_hi is None else b_hi
+    out = np.zeros((b_hi - b_lo, F, D), np.float32)
+    bad = load_oracle().lo_embedding_bag_synth(seed, F, rows, D, B, ptr(offsets), ptr(ids), b_lo,
+                                               b_hi, ptr(out), threads)
+    return out, int(bad)
+
+
+def bf16_round(x):
+    """Round-to-nearest-even fp32 -> bf16, returned as fp32 (vectorised)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32)

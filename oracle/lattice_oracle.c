@@ -414,3 +414,23 @@ void lo_net_forward(const lo_net_cfg* cfg, const lo_net_weights* w, int64_t coun
         free(scratch);
     }
 }
+
+/* ---------------------------------------------------------------------------------------
+ * Synthetic bags / domains, same formulas as lattice_synth_bags.
+ * ------------------------------------------------------------------------------------- */
+void lo_synth_bags(int F, int64_t B, int max_len, int64_t rows, uint64_t seed, int64_t* offsets,
+                   int32_t* ids) {
+    const int64_t bags = (int64_t)F * B;
+    offsets[0] = 0;
+    for (int64_t i = 0; i < bags; ++i)
+        offsets[i + 1] = offsets[i] + (int64_t)(lo_gen(seed, LO_TAG_LEN, (uint64_t)i) %
+                                                (uint64_t)(max_len + 1));
+    for (int64_t i = 0; i < bags; ++i)
+        for (int64_t j = offsets[i]; j < offsets[i + 1]; ++j)
+            ids[j] = (int32_t)(lo_gen(seed, LO_TAG_ID, (uint64_t)i * max_len + (uint64_t)(j - offsets[i])) %
+                               (uint64_t)rows);
+}
+
+void lo_synth_domains(int64_t B, int G, uint64_t seed, int32_t* dom) {
+    for (int64_t i = 0; i < B; ++i) dom[i] = (int32_t)(lo_gen(seed, LO_TAG_DOM, (uint64_t)i) % (uint64_t)G);
+}

@@ -89,6 +89,12 @@ int64_t lo_embedding_bag(int F, const int64_t* rows, int D, int64_t B,
                          const float* const* tables, const int64_t* offsets,
                          const int32_t* ids, float* out);
 
+/* lengths/ids/domains exactly as lattice_synth_bags / lattice_synth_domains. ids must hold
+ * F*B*max_len entries. */
+void lo_synth_bags(int F, int64_t B, int max_len, int64_t rows, uint64_t seed, int64_t* offsets,
+                   int32_t* ids);
+void lo_synth_domains(int64_t B, int G, uint64_t seed, int32_t* dom);
+
 /* ---- network forward -------------------------------------------- */
 typedef struct {
     int n;          /* embeddings per sample (= sparse features F) */

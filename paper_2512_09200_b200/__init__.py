@@ -1,0 +1,281 @@
+"""Host-side (Python) mirror of the Lattice hot-path interface over liblattice_b200.so.
+
+The product is the C ABI in include/lattice_b200.h (sm_100a CUDA kernels); this module is a
+thin ctypes binding used by the tests and bench.py. torch is used only as the device-memory
+and stream plumbing: every array argument is a CUDA tensor whose data_ptr() is handed to the
+library. There is no CPU fallback -- if the shared library is missing, importing this module
+raises.
+
+Errors map to the reference's exception types (proj/include/lattice/core.hpp:20-27):
+LATTICE_USAGE -> UsageError(ValueError), LATTICE_DATA -> DataError(RuntimeError).
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblattice_b200.so")
+
+OK, USAGE, DATA, CUDA, NCCL = 0, 1, 2, 3, 4
+F32, BF16 = 0, 1
+
+
+class LatticeError(Exception):
+    pass
+
+
+class UsageError(LatticeError, ValueError):
+    """core.hpp:20 -- caller broke an API contract."""
+
+
+class DataError(LatticeError, RuntimeError):
+    """core.hpp:25 -- input data is malformed."""
+
+    def __init__(self, msg, index=-1):
+        super().__init__(msg)
+        self.index = index
+
+
+class CudaError(LatticeError, RuntimeError):
+    pass
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+_U64 = ctypes.c_uint64
+
+
+class ZipArgs(ctypes.Structure):
+    _fields_ = [("n", _I64), ("user_bytes", _P), ("user_off", _P), ("ad_bytes", _P),
+                ("ad_off", _P), ("ts", _P), ("tasks", _I32), ("conv", _P),
+                ("conv_present", _P), ("windows", _I32), ("durations_host", _P),
+                ("probabilities_host", _P), ("seed", _U64), ("window", _P), ("labels", _P),
+                ("routed", _P), ("check", _I32)]
+
+
+class BagArgs(ctypes.Structure):
+    _fields_ = [("features", _I32), ("batch", _I64), ("dim", _I32), ("table_dtype", _I32),
+                ("tables", _P), ("rows", _P), ("offsets", _P), ("ids", _P), ("out_dtype", _I32),
+                ("out", _P), ("out_row_stride", _I64), ("out_feature_offset", _I32),
+                ("sample_pos", _P), ("normalize", _I32), ("check", _I32)]
+
+
+class GemmArgs(ctypes.Structure):
+    _fields_ = [("M", _I64), ("N", _I64), ("K", _I64), ("A", _P), ("lda", _I64), ("B", _P),
+                ("ldb", _I64), ("C", _P), ("ldc", _I64), ("out_dtype", _I32), ("epilogue", _I32),
+                ("resid", _P), ("ldr", _I64), ("group", _I32)]
+
+
+class NetConfig(ctypes.Structure):
+    _fields_ = [("n", _I32), ("d", _I32), ("blocks", _I32), ("nF", _I32), ("nL", _I32),
+                ("k", _I32), ("n_mlp", _I32), ("mlp", _I32 * 6), ("domains", _I32),
+                ("heads", _I32), ("tower_hidden", _I32), ("hard", _I32), ("max_batch", _I64),
+                ("weight_seed", _U64)]
+
+
+class Batch(ctypes.Structure):
+    _fields_ = [("batch", _I64), ("domain", _P), ("table_dtype", _I32), ("tables", _P),
+                ("rows", _P), ("offsets", _P), ("ids", _P), ("pooled", _P)]
+
+
+def _sig(name, res, args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = args
+    return f
+
+
+_sig("lattice_last_error", ctypes.c_char_p, [])
+_sig("lattice_last_error_index", _I64, [])
+_sig("lattice_abi_version", ctypes.c_int, [])
+_sig("lattice_stable_hash", ctypes.c_int, [_I64, _P, _P, _U64, _P, _P])
+_sig("lattice_zipper_validate", ctypes.c_int, [_I32, _P, _P])
+_sig("lattice_zipper_assign_labels", ctypes.c_int, [ctypes.POINTER(ZipArgs), _P])
+_sig("lattice_embedding_bag", ctypes.c_int, [ctypes.POINTER(BagArgs), _P])
+_sig("lattice_rownorm", ctypes.c_int, [_I32, _I64, _I64, ctypes.c_double, _P, _P, _I32, _P])
+_sig("lattice_fill_tables", ctypes.c_int, [_P, _I32, _I32, _I64, _I32, _U64, _I32, _I64, _P])
+_sig("lattice_fill_weights", ctypes.c_int, [_P, _I32, _I64, _I64, _U64, _U64, _P])
+_sig("lattice_synth_bags", ctypes.c_int, [_I32, _I64, _I32, _I64, _U64, _P, _P, _P])
+_sig("lattice_synth_domains", ctypes.c_int, [_I64, _I32, _U64, _P, _P])
+_sig("lattice_domain_bucket", ctypes.c_int, [_I64, _I32, _P, _P, _P, _P, _P])
+_sig("lattice_gemm", ctypes.c_int, [ctypes.POINTER(GemmArgs), _P])
+_sig("lattice_net_create", ctypes.c_int, [ctypes.POINTER(NetConfig), ctypes.POINTER(_P)])
+_sig("lattice_net_destroy", None, [_P])
+_sig("lattice_net_weight", _P, [_P, _I32, _I32, _I32])
+_sig("lattice_net_forward", ctypes.c_int, [_P, ctypes.POINTER(Batch), _P, _P])
+_sig("lattice_net_set_timing", ctypes.c_int, [_P, _I32])
+_sig("lattice_net_stage_times", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_float), _I32,
+                                               ctypes.POINTER(_I32)])
+
+EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_version",
+           "lattice_stable_hash", "lattice_zipper_validate", "lattice_zipper_assign_labels",
+           "lattice_embedding_bag", "lattice_rownorm", "lattice_fill_tables",
+           "lattice_fill_weights", "lattice_synth_bags", "lattice_synth_domains",
+           "lattice_domain_bucket", "lattice_gemm", "lattice_net_create", "lattice_net_destroy",
+           "lattice_net_weight", "lattice_net_forward", "lattice_net_set_timing",
+           "lattice_net_stage_times"]
+
+lib = _lib
+
+
+def check(rc):
+    if rc == OK:
+        return
+    msg = _lib.lattice_last_error().decode()
+    if rc == USAGE:
+        raise UsageError(msg)
+    if rc == DATA:
+        raise DataError(msg, int(_lib.lattice_last_error_index()))
+    raise CudaError(msg)
+
+
+def _stream(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+# ---- Zipper ---------------------------------------------------------------------------------
+
+def zipper_assign_labels(user_bytes, user_off, ad_bytes, ad_off, ts, conv, conv_present,
+                         durations, probabilities, seed, routed=False, check_errors=True,
+                         stream=None):
+    """Columnar lattice::zip_dataset core (datasets.hpp:199-249) on the GPU.
+
+    Device tensors: user_bytes/ad_bytes uint8, *_off int64 [n+1], ts int64 [n],
+    conv int64 [n,T], conv_present uint8 [n,T]. durations/probabilities are host sequences.
+    Returns (window uint8 [n], labels uint8 [n,T,W], routed uint8 [n,T] or None)."""
+    import numpy as np
+    import torch
+    n = ts.shape[0]
+    T = conv.shape[1] if conv.dim() == 2 else 0
+    W = len(durations)
+    dur = np.ascontiguousarray(durations, dtype=np.int64)
+    pr = np.ascontiguousarray(probabilities, dtype=np.float64)
+    dev = ts.device
+    win = torch.empty(n, dtype=torch.uint8, device=dev)
+    lab = torch.empty((n, T, W), dtype=torch.uint8, device=dev)
+    rt = torch.empty((n, T), dtype=torch.uint8, device=dev) if routed else None
+    a = ZipArgs(n, _p(user_bytes), _p(user_off), _p(ad_bytes), _p(ad_off), _p(ts), T, _p(conv),
+                _p(conv_present), W, ctypes.c_void_p(dur.ctypes.data),
+                ctypes.c_void_p(pr.ctypes.data), seed, _p(win), _p(lab), _p(rt),
+                1 if check_errors else 0)
+    check(_lib.lattice_zipper_assign_labels(ctypes.byref(a), _stream(stream)))
+    return win, lab, rt
+
+
+def stable_hash(bytes_, off, seed, stream=None):
+    import torch
+    n = off.shape[0] - 1
+    out = torch.empty(n, dtype=torch.int64, device=off.device)
+    check(_lib.lattice_stable_hash(n, _p(bytes_), _p(off), seed, _p(out), _stream(stream)))
+    return out
+
+
+# ---- embedding bag ----------------------------------------------------------------------------
+
+def embedding_bag(tables, offsets, ids, batch, out=None, out_dtype=None, sample_pos=None,
+                  normalize=False, out_row_stride=None, out_feature_offset=0, check_errors=True,
+                  stream=None, table_ptrs=None, rows=None):
+    """Sum-pooled embedding bags. tables: list of [rows_f, D] CUDA tensors (f32 or bf16).
+    offsets int64 [F*B+1] feature-major CSR, ids int32. Returns out [B, F, D]."""
+    import torch
+    F = len(tables)
+    D = tables[0].shape[1]
+    tdt = tables[0].dtype
+    odt = out_dtype or tdt
+    dev = tables[0].device
+    if table_ptrs is None:
+        table_ptrs = torch.tensor([t.data_ptr() for t in tables], dtype=torch.int64, device=dev)
+    if rows is None:
+        rows = torch.tensor([t.shape[0] for t in tables], dtype=torch.int64, device=dev)
+    if out is None:
+        out = torch.empty((batch, F, D), dtype=odt, device=dev)
+    stride = out_row_stride if out_row_stride is not None else F * D
+    a = BagArgs(F, batch, D, F32 if tdt == torch.float32 else BF16, _p(table_ptrs), _p(rows),
+                _p(offsets), _p(ids), F32 if odt == torch.float32 else BF16, _p(out), stride,
+                out_feature_offset, _p(sample_pos), 1 if normalize else 0, 1 if check_errors else 0)
+    check(_lib.lattice_embedding_bag(ctypes.byref(a), _stream(stream)))
+    return out
+
+
+def rownorm(x, mode=1, eps=1e-6, check_errors=True, stream=None):
+    """mode 0 rms_norm, 1 swish_rn, 2 swish_rn_hard over the last dim of an fp32 matrix."""
+    import torch
+    x = x.contiguous()
+    out = torch.empty_like(x)
+    rows = x.numel() // x.shape[-1] if x.numel() else 0
+    check(_lib.lattice_rownorm(mode, rows, x.shape[-1], eps, _p(x), _p(out),
+                               1 if check_errors else 0, _stream(stream)))
+    return out
+
+
+def fill_tables(tables, seed, feature_base=0, rows_total=None, stream=None):
+    """tables: contiguous [F, rows, D] tensor (f32 or bf16)."""
+    import torch
+    F, R, D = tables.shape
+    check(_lib.lattice_fill_tables(_p(tables), F32 if tables.dtype == torch.float32 else BF16, F,
+                                   R, D, seed, feature_base, rows_total or R, _stream(stream)))
+    return tables
+
+
+def fill_weights(w, seed, tag, stream=None):
+    import torch
+    out_f, fan_in = w.shape[-2], w.shape[-1]
+    rows = w.numel() // fan_in
+    check(_lib.lattice_fill_weights(_p(w), F32 if w.dtype == torch.float32 else BF16, rows,
+                                    fan_in, seed, tag, _stream(stream)))
+    return w
+
+
+def synth_bags(F, B, max_len, rows, seed, device="cuda", stream=None):
+    import torch
+    offsets = torch.empty(F * B + 1, dtype=torch.int64, device=device)
+    ids = torch.empty(max(F * B * max_len, 1), dtype=torch.int32, device=device)
+    check(_lib.lattice_synth_bags(F, B, max_len, rows, seed, _p(offsets), _p(ids), _stream(stream)))
+    return offsets, ids
+
+
+def synth_domains(B, G, seed, device="cuda", stream=None):
+    import torch
+    dom = torch.empty(B, dtype=torch.int32, device=device)
+    check(_lib.lattice_synth_domains(B, G, seed, _p(dom), _stream(stream)))
+    return dom
+
+
+def domain_bucket(domain, G, stream=None):
+    import torch
+    B = domain.shape[0]
+    pos = torch.empty(B, dtype=torch.int32, device=domain.device)
+    order = torch.empty(B, dtype=torch.int32, device=domain.device)
+    seg = torch.empty(G + 1, dtype=torch.int32, device=domain.device)
+    check(_lib.lattice_domain_bucket(B, G, _p(domain), _p(pos), _p(order), _p(seg), _stream(stream)))
+    return pos, order, seg
+
+
+# ---- GEMM ---------------------------------------------------------------------------------------
+
+EPI_STORE, EPI_SWISH, EPI_SWISH_HARD, EPI_RESID_NORM = 0, 1, 2, 3
+
+
+def gemm(A, B, epilogue=EPI_STORE, out_dtype=None, resid=None, group=128, out=None, stream=None):
+    """C = A @ B^T with A [M,K] bf16, B [N,K] bf16 on tcgen05; fused epilogue."""
+    import torch
+    M, K = A.shape
+    N = B.shape[0]
+    odt = out_dtype or torch.bfloat16
+    if out is None:
+        out = torch.empty((M, N), dtype=odt, device=A.device)
+    a = GemmArgs(M, N, K, _p(A), A.stride(0), _p(B), B.stride(0), _p(out), out.stride(0),
+                 F32 if odt == torch.float32 else BF16, epilogue, _p(resid),
+                 resid.stride(0) if resid is not None else 0, group)
+    check(_lib.lattice_gemm(ctypes.byref(a), _stream(stream)))
+    return out

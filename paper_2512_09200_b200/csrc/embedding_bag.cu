@@ -1,0 +1,499 @@
+// embedding_bag.cu -- K1 jagged embedding-bag sum pooling, the synthetic
+// input generators, K6 domain bucketing and the row-wise
+// norm/activation kernel (numerics.hpp:81-107).
+//
+// K1 layout: one warp per bag (f, b); a row of D elements is LPR lanes x 16 B, so a warp
+// gathers 32/LPR rows per pass and keeps U passes (U x 16 B per lane) in flight. Ids are
+// read once per 32 with one coalesced load and broadcast with shuffles. Table rows are
+// streamed with ld.global.nc.L1::no_allocate (no reuse under uniform ids). The pooled row
+// is reduced across the row groups with xor-shuffles, optionally rms-normalised over D and
+// written once (HBM-bound: bytes = ids*D*s_tab + ids*4 + (F*B+1)*8 + F*B*D*s_out).
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <string>
+
+#include "common.cuh"
+
+namespace lat {
+namespace {
+
+struct BagParams {
+    int32_t F;
+    int64_t B;
+    int32_t D;
+    const void* const* tables;
+    const int64_t* rows;
+    const int64_t* offsets;
+    const int32_t* ids;
+    void* out;
+    int64_t out_stride;
+    int32_t out_foff;
+    const int32_t* pos;
+    int32_t normalize;
+    unsigned long long* err;
+};
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+template <typename T>
+struct Elem;
+template <>
+struct Elem<float> {
+    static constexpr int kPerChunk = 4;
+    __device__ static void add(float* acc, uint4 v) {
+        acc[0] += __uint_as_float(v.x);
+        acc[1] += __uint_as_float(v.y);
+        acc[2] += __uint_as_float(v.z);
+        acc[3] += __uint_as_float(v.w);
+    }
+    __device__ static void store(float* dst, const float* v) {
+        *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+template <>
+struct Elem<__nv_bfloat16> {
+    static constexpr int kPerChunk = 8;
+    __device__ static void add(float* acc, uint4 v) {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            acc[2 * i] += bf16_lo(w[i]);
+            acc[2 * i + 1] += bf16_hi(w[i]);
+        }
+    }
+};
+
+template <typename OT, int N>
+__device__ __forceinline__ void store_out(OT* dst, const float* v);
+template <>
+__device__ __forceinline__ void store_out<float, 4>(float* dst, const float* v) {
+    *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+}
+template <>
+__device__ __forceinline__ void store_out<float, 8>(float* dst, const float* v) {
+    reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+template <>
+__device__ __forceinline__ void store_out<__nv_bfloat16, 4>(__nv_bfloat16* dst, const float* v) {
+    *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]));
+}
+template <>
+__device__ __forceinline__ void store_out<__nv_bfloat16, 8>(__nv_bfloat16* dst, const float* v) {
+    *reinterpret_cast<uint4*>(dst) = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
+                                                pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+}
+
+constexpr int kBagWarps = 8;
+
+template <typename TT, typename OT, int LPR, int CPL>
+__global__ void __launch_bounds__(kBagWarps * 32) bag_kernel(const BagParams p) {
+    constexpr int EPC = Elem<TT>::kPerChunk;
+    constexpr int RPP = 32 / LPR;  // rows per pass
+    constexpr int U = 4;           // passes in flight
+    const int lane = threadIdx.x & 31;
+    const int64_t bag = (int64_t)blockIdx.x * kBagWarps + (threadIdx.x >> 5);
+    if (bag >= (int64_t)p.F * p.B) return;
+    const int f = (int)(bag / p.B);
+    const int64_t b = bag - (int64_t)f * p.B;
+    const TT* __restrict__ table = static_cast<const TT*>(p.tables[f]);
+    const int64_t rows = p.rows[f];
+    const int64_t s = p.offsets[bag], e = p.offsets[bag + 1];
+    const int sub = lane / LPR, cl = lane % LPR;
+
+    float acc[CPL * EPC];
+#pragma unroll
+    for (int i = 0; i < CPL * EPC; ++i) acc[i] = 0.0f;
+
+    for (int64_t base = s; base < e; base += 32) {
+        const int cnt = (int)((e - base) < 32 ? (e - base) : 32);
+        const int my_id = lane < cnt ? __ldg(p.ids + base + lane) : 0;
+        for (int j = 0; j < cnt; j += RPP * U) {
+            uint4 v[U][CPL];
+            bool ok[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int jj = j + u * RPP + sub;
+                const int id = __shfl_sync(0xffffffffu, my_id, jj & 31);
+                const bool live = jj < cnt;
+                ok[u] = live && id >= 0 && (int64_t)id < rows;
+                if (live && !ok[u]) atomicMin(p.err, (unsigned long long)(base + jj));
+                const TT* row = table + (int64_t)(ok[u] ? id : 0) * p.D;
+#pragma unroll
+                for (int c = 0; c < CPL; ++c)
+                    v[u][c] = ok[u] ? ld_stream(row + (c * LPR + cl) * EPC) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) Elem<TT>::add(acc + c * EPC, v[u][c]);
+        }
+    }
+    // fold the RPP row groups: lanes with equal cl end up with the full sum
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+        for (int i = 0; i < CPL * EPC; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+
+    if (p.normalize) {  // rms_norm over D (numerics.hpp:81-90), eps 1e-6
+        float ss = 0.0f;
+#pragma unroll
+        for (int i = 0; i < CPL * EPC; ++i) ss += acc[i] * acc[i];
+#pragma unroll
+        for (int o = 1; o < LPR; o <<= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        const float denom = sqrtf(ss / (float)p.D + 1e-6f);
+#pragma unroll
+        for (int i = 0; i < CPL * EPC; ++i) acc[i] = acc[i] / denom;
+    }
+    if (sub == 0) {
+        const int64_t row = p.pos ? (int64_t)p.pos[b] : b;
+        OT* dst = static_cast<OT*>(p.out) + row * p.out_stride + (int64_t)(p.out_foff + f) * p.D;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) store_out<OT, EPC>(dst + (c * LPR + cl) * EPC, acc + c * EPC);
+    }
+}
+
+template <typename TT, typename OT>
+lattice_status launch_bag(const BagParams& p, int row_bytes, cudaStream_t st) {
+    const int64_t bags = (int64_t)p.F * p.B;
+    const unsigned grid = (unsigned)((bags + kBagWarps - 1) / kBagWarps);
+    const int threads = kBagWarps * 32;
+    switch (row_bytes) {
+        case 128: bag_kernel<TT, OT, 8, 1><<<grid, threads, 0, st>>>(p); break;
+        case 256: bag_kernel<TT, OT, 16, 1><<<grid, threads, 0, st>>>(p); break;
+        case 512: bag_kernel<TT, OT, 32, 1><<<grid, threads, 0, st>>>(p); break;
+        case 1024: bag_kernel<TT, OT, 32, 2><<<grid, threads, 0, st>>>(p); break;
+        default:
+            return set_error(LATTICE_USAGE,
+                             "embedding_bag: D * sizeof(table dtype) must be 128, 256, 512 or 1024 bytes");
+    }
+    return LATTICE_OK;
+}
+
+// ---- synthetic generators ---------------------------------------------------------------
+__global__ void fill_tables_kernel(void* out, int dtype, int64_t n, int D, int64_t rows,
+                                   int64_t rows_total, int feature_base, uint64_t seed) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i % D;
+        const int64_t r = (i / D) % rows;
+        const int64_t f = i / ((int64_t)D * rows) + feature_base;
+        const uint64_t idx = ((uint64_t)f * (uint64_t)rows_total + (uint64_t)r) * (uint64_t)D + c;
+        const float v = (float)(int8_t)(gen_u64(seed, kTagTable, idx) >> 56) * 0x1.0p-10f;
+        if (dtype == LATTICE_F32)
+            static_cast<float*>(out)[i] = v;
+        else
+            static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+    }
+}
+
+__global__ void fill_weights_kernel(void* out, int dtype, int64_t n, int64_t fan_in, int shift,
+                                    uint64_t seed, uint64_t tag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = ldexpf((float)(int8_t)(gen_u64(seed, tag, (uint64_t)i) >> 56), -shift);
+        if (dtype == LATTICE_F32)
+            static_cast<float*>(out)[i] = v;
+        else
+            static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+    }
+}
+
+__global__ void synth_len_kernel(int64_t bags, int max_len, uint64_t seed, int64_t* len) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < bags;
+         i += (int64_t)gridDim.x * blockDim.x)
+        len[i] = (int64_t)(gen_u64(seed, kTagLen, (uint64_t)i) % (uint64_t)(max_len + 1));
+}
+
+__global__ void synth_ids_kernel(int64_t bags, int max_len, int64_t rows, uint64_t seed,
+                                 const int64_t* __restrict__ off, int32_t* __restrict__ ids) {
+    // one warp per bag
+    const int lane = threadIdx.x & 31;
+    for (int64_t bag = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; bag < bags;
+         bag += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t s = off[bag], e = off[bag + 1];
+        for (int64_t j = s + lane; j < e; j += 32)
+            ids[j] = (int32_t)(gen_u64(seed, kTagId, (uint64_t)bag * max_len + (j - s)) %
+                               (uint64_t)rows);
+    }
+}
+
+__global__ void synth_dom_kernel(int64_t n, int G, uint64_t seed, int32_t* dom) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dom[i] = (int32_t)(gen_u64(seed, kTagDom, (uint64_t)i) % (uint64_t)G);
+}
+
+// ---- K6: stable counting sort by domain, one CTA of 1024 threads -----------------------
+constexpr int kBucketThreads = 1024;
+constexpr int kMaxDomains = 32;
+
+__global__ void __launch_bounds__(kBucketThreads) bucket_kernel(int64_t B, int G,
+                                                                const int32_t* __restrict__ dom,
+                                                                int32_t* __restrict__ pos,
+                                                                int32_t* __restrict__ order,
+                                                                int32_t* __restrict__ seg) {
+    extern __shared__ int32_t cnt[];  // [G][1024]
+    __shared__ int32_t tot[kMaxDomains + 1];
+    __shared__ int32_t warp_tot[32];
+    const int t = threadIdx.x;
+    const int64_t per = (B + kBucketThreads - 1) / kBucketThreads;
+    const int64_t lo = (int64_t)t * per < B ? (int64_t)t * per : B;
+    const int64_t hi = lo + per < B ? lo + per : B;
+    for (int g = 0; g < G; ++g) cnt[g * kBucketThreads + t] = 0;
+    for (int64_t b = lo; b < hi; ++b) {
+        const int g = dom[b];
+        cnt[(g >= 0 && g < G ? g : 0) * kBucketThreads + t]++;
+    }
+    __syncthreads();
+    // exclusive scan of cnt[g][*] for every g
+    for (int g = 0; g < G; ++g) {
+        int v = cnt[g * kBucketThreads + t];
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int n = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((t & 31) >= o) incl += n;
+        }
+        if ((t & 31) == 31) warp_tot[t >> 5] = incl;
+        __syncthreads();
+        if (t < 32) {
+            int w = warp_tot[t], wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int n = __shfl_up_sync(0xffffffffu, wi, o);
+                if (t >= o) wi += n;
+            }
+            warp_tot[t] = wi - w;
+            if (t == 31) tot[g] = wi;
+        }
+        __syncthreads();
+        cnt[g * kBucketThreads + t] = incl - v + warp_tot[t >> 5];
+        __syncthreads();
+    }
+    if (t == 0) {
+        int run = 0;
+        for (int g = 0; g < G; ++g) {
+            const int c = tot[g];
+            tot[g] = run;
+            seg[g] = run;
+            run += c;
+        }
+        seg[G] = run;
+    }
+    __syncthreads();
+    for (int64_t b = lo; b < hi; ++b) {
+        int g = dom[b];
+        g = (g >= 0 && g < G) ? g : 0;
+        const int p = tot[g] + cnt[g * kBucketThreads + t]++;
+        pos[b] = p;
+        order[p] = (int32_t)b;
+    }
+}
+
+// ---- row-wise rms_norm / swish_rn / swish_rn_hard, one warp per row ---------------------
+__global__ void rownorm_kernel(int mode, int64_t rows, int64_t width, float eps,
+                               const float* __restrict__ x, float* __restrict__ out,
+                               unsigned long long* err) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const float* xr = x + r * width;
+        float ss = 0.0f;
+        bool bad = false;
+        for (int64_t c = lane; c < width; c += 32) {
+            const float v = xr[c];
+            bad |= !isfinite(v);
+            ss += v * v;
+        }
+        ss = warp_sum(ss);
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(err, (unsigned long long)r);
+        const float denom = sqrtf(ss / (float)width + eps);
+        for (int64_t c = lane; c < width; c += 32) {
+            const float v = xr[c] / denom;
+            out[r * width + c] = mode == 0 ? v : act_swish(v, mode == 2);
+        }
+    }
+}
+
+unsigned grid_for(int64_t n, int threads) {
+    int64_t b = (n + threads - 1) / threads;
+    const int64_t cap = (int64_t)num_sms() * 16;
+    return (unsigned)std::max<int64_t>(1, std::min(b, cap));
+}
+
+lattice_status sync_err(unsigned long long* err, cudaStream_t st, unsigned long long* host) {
+    *host = ~0ull;
+    cudaError_t e = cudaMemcpyAsync(host, err, sizeof(*host), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    return e == cudaSuccess ? LATTICE_OK : check_cuda(e, "error readback");
+}
+
+}  // namespace
+}  // namespace lat
+
+extern "C" {
+
+lattice_status lattice_embedding_bag(const lattice_bag_args* a, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(a != nullptr, "lattice_embedding_bag: null args");
+    LAT_REQUIRE(a->features >= 0 && a->batch >= 0 && a->dim > 0, "embedding_bag: bad sizes");
+    LAT_REQUIRE(a->table_dtype == LATTICE_F32 || a->table_dtype == LATTICE_BF16,
+                "embedding_bag: table dtype must be f32 or bf16");
+    LAT_REQUIRE(a->out_dtype == LATTICE_F32 || a->out_dtype == LATTICE_BF16,
+                "embedding_bag: out dtype must be f32 or bf16");
+    LAT_REQUIRE(a->out_row_stride >= (int64_t)(a->out_feature_offset + a->features) * a->dim,
+                "embedding_bag: out_row_stride too small");
+    if ((int64_t)a->features * a->batch == 0) return LATTICE_OK;
+    LAT_REQUIRE(a->tables && a->rows && a->offsets && a->out, "embedding_bag: null pointer");
+    const int esize = a->table_dtype == LATTICE_F32 ? 4 : 2;
+    const int row_bytes = a->dim * esize;
+    const int out_chunk = (a->out_dtype == LATTICE_F32 ? 4 : 2) * (16 / esize);
+    LAT_REQUIRE(out_chunk == 8 || out_chunk == 16 || out_chunk == 32,
+                "embedding_bag: unsupported dtype combination");
+
+    unsigned long long* err = nullptr;
+    LAT_CUDA(cudaMallocAsync(&err, sizeof(*err), stream));
+    LAT_CUDA(cudaMemsetAsync(err, 0xff, sizeof(*err), stream));
+    BagParams p{a->features, a->batch, a->dim, a->tables, a->rows, a->offsets, a->ids, a->out,
+                a->out_row_stride, a->out_feature_offset, a->sample_pos, a->normalize, err};
+    lattice_status st;
+    if (a->table_dtype == LATTICE_F32)
+        st = a->out_dtype == LATTICE_F32 ? launch_bag<float, float>(p, row_bytes, stream)
+                                         : launch_bag<float, __nv_bfloat16>(p, row_bytes, stream);
+    else
+        st = a->out_dtype == LATTICE_F32
+                 ? launch_bag<__nv_bfloat16, float>(p, row_bytes, stream)
+                 : launch_bag<__nv_bfloat16, __nv_bfloat16>(p, row_bytes, stream);
+    if (st != LATTICE_OK) {
+        cudaFreeAsync(err, stream);
+        return st;
+    }
+    cudaError_t le = cudaGetLastError();
+    unsigned long long host = ~0ull;
+    if (le == cudaSuccess && a->check) {
+        lattice_status s2 = sync_err(err, stream, &host);
+        if (s2 != LATTICE_OK) {
+            cudaFreeAsync(err, stream);
+            return s2;
+        }
+    }
+    cudaFreeAsync(err, stream);
+    if (le != cudaSuccess) return check_cuda(le, "bag_kernel");
+    if (host != ~0ull)
+        return set_error(LATTICE_DATA,
+                         "embedding_bag: id at position " + std::to_string(host) + " is outside its table",
+                         (int64_t)host);
+    return LATTICE_OK;
+}
+
+lattice_status lattice_fill_tables(void* tables, int32_t dtype, int32_t F, int64_t rows, int32_t D,
+                                   uint64_t seed, int32_t feature_base, int64_t rows_total,
+                                   lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(tables && F >= 0 && rows > 0 && D > 0, "fill_tables: bad args");
+    if (rows_total <= 0) rows_total = rows;
+    const int64_t n = (int64_t)F * rows * D;
+    fill_tables_kernel<<<grid_for(n, 256), 256, 0, stream>>>(tables, dtype, n, D, rows, rows_total,
+                                                             feature_base, seed);
+    LAT_CUDA(cudaGetLastError());
+    return LATTICE_OK;
+}
+
+lattice_status lattice_fill_weights(void* w, int32_t dtype, int64_t out_features, int64_t fan_in,
+                                    uint64_t seed, uint64_t tag, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(w && out_features > 0 && fan_in > 0, "fill_weights: bad args");
+    const int64_t n = out_features * fan_in;
+    fill_weights_kernel<<<grid_for(n, 256), 256, 0, stream>>>(w, dtype, n, fan_in,
+                                                              weight_shift(fan_in), seed, tag);
+    LAT_CUDA(cudaGetLastError());
+    return LATTICE_OK;
+}
+
+lattice_status lattice_synth_bags(int32_t F, int64_t B, int32_t max_len, int64_t rows, uint64_t seed,
+                                  int64_t* offsets, int32_t* ids, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(F > 0 && B > 0 && max_len >= 0 && rows > 0 && offsets && ids, "synth_bags: bad args");
+    const int64_t bags = (int64_t)F * B;
+    int64_t* len = nullptr;
+    LAT_CUDA(cudaMallocAsync(&len, sizeof(int64_t) * (bags + 1), stream));
+    synth_len_kernel<<<grid_for(bags, 256), 256, 0, stream>>>(bags, max_len, seed, len);
+    LAT_CUDA(cudaMemsetAsync(len + bags, 0, sizeof(int64_t), stream));
+    size_t tmp_bytes = 0;
+    LAT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, len, offsets, bags + 1, stream));
+    void* tmp = nullptr;
+    LAT_CUDA(cudaMallocAsync(&tmp, tmp_bytes, stream));
+    LAT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, len, offsets, bags + 1, stream));
+    synth_ids_kernel<<<grid_for(bags * 32, 256), 256, 0, stream>>>(bags, max_len, rows, seed,
+                                                                   offsets, ids);
+    LAT_CUDA(cudaGetLastError());
+    cudaFreeAsync(tmp, stream);
+    cudaFreeAsync(len, stream);
+    return LATTICE_OK;
+}
+
+lattice_status lattice_synth_domains(int64_t B, int32_t G, uint64_t seed, int32_t* dom,
+                                     lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(B >= 0 && G > 0 && dom, "synth_domains: bad args");
+    if (!B) return LATTICE_OK;
+    synth_dom_kernel<<<grid_for(B, 256), 256, 0, stream>>>(B, G, seed, dom);
+    LAT_CUDA(cudaGetLastError());
+    return LATTICE_OK;
+}
+
+lattice_status lattice_domain_bucket(int64_t B, int32_t G, const int32_t* dom, int32_t* pos,
+                                     int32_t* order, int32_t* seg, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(B >= 0 && B < (1ll << 31) && G > 0 && G <= kMaxDomains, "domain_bucket: bad sizes");
+    LAT_REQUIRE(dom && pos && order && seg, "domain_bucket: null pointer");
+    const size_t smem = sizeof(int32_t) * G * kBucketThreads;
+    static bool attr = false;
+    if (!attr) {
+        LAT_CUDA(cudaFuncSetAttribute(bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(int32_t) * kMaxDomains * kBucketThreads)));
+        attr = true;
+    }
+    LAT_REQUIRE(smem <= 227 * 1024, "domain_bucket: too many domains");
+    bucket_kernel<<<1, kBucketThreads, smem, stream>>>(B, G, dom, pos, order, seg);
+    LAT_CUDA(cudaGetLastError());
+    return LATTICE_OK;
+}
+
+lattice_status lattice_rownorm(int32_t mode, int64_t rows, int64_t width, double eps, const float* x,
+                               float* out, int32_t check, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(mode >= 0 && mode <= 2, "rownorm: mode must be 0, 1 or 2");
+    LAT_REQUIRE(eps > 0.0, "eps must be > 0");  // numerics.hpp:20
+    LAT_REQUIRE(width > 0, "rms_norm: empty input");  // numerics.hpp:83
+    if (rows <= 0) return LATTICE_OK;
+    unsigned long long* err = nullptr;
+    LAT_CUDA(cudaMallocAsync(&err, sizeof(*err), stream));
+    LAT_CUDA(cudaMemsetAsync(err, 0xff, sizeof(*err), stream));
+    rownorm_kernel<<<grid_for(rows * 32, 256), 256, 0, stream>>>(mode, rows, width, (float)eps, x,
+                                                                 out, err);
+    cudaError_t le = cudaGetLastError();
+    unsigned long long host = ~0ull;
+    if (le == cudaSuccess && check) {
+        lattice_status s2 = sync_err(err, stream, &host);
+        if (s2 != LATTICE_OK) {
+            cudaFreeAsync(err, stream);
+            return s2;
+        }
+    }
+    cudaFreeAsync(err, stream);
+    if (le != cudaSuccess) return check_cuda(le, "rownorm_kernel");
+    if (host != ~0ull)
+        return set_error(LATTICE_DATA, "rms_norm: non-finite input", (int64_t)host);
+    return LATTICE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,331 @@
+// fm_lcb.cu -- K2: the per-sample interaction half of a DWFB block, fused.
+//
+// For every sample b with embeddings X_b [n][d] (bf16):
+//   P   = bf16( X_b^T . Y )                    d x k     (FMB compression, Wukong-style)
+//   F   = X_b . P                               n x k     (factorisation-machine interaction)
+//   Fin = bf16( rms_norm(flatten(F)) )          n*k       -> the FMB MLP input (K3)
+//   L   = W_L . X_b                             nL x d    (LCB)
+//   X'_b[nF+i] = bf16( rms_norm_d(L_i + X_b[nF+i]) ), i < nL   (block combine, LCB half)
+//
+// X_b is read from HBM exactly once: TMA lands it in shared memory as 64-column panels with
+// the 128-byte swizzle, and that one image serves three tcgen05 MMAs through different
+// descriptors -- MN-major A (X^T for P), MN-major B (X for L) and K-major A (X for F).
+// W_L and Y stay resident in shared memory for the whole persistent CTA. P goes TMEM ->
+// registers -> bf16 -> swizzled shared memory to become F's B operand. Accumulators live in
+// TMEM (P | L | F columns). Warp roles: 0 TMA producer, 1 MMA issuer, 2-5 epilogue
+// (thread = TMEM lane = accumulator row). X stages are double-buffered so the next
+// sample's load overlaps this sample's MMAs and epilogue.
+#include <cudaTypedefs.h>
+
+#include <string>
+
+#include "common.cuh"
+#include "fm_lcb.h"
+#include "gemm_host.h"
+#include "tc.cuh"
+
+namespace lat {
+namespace fm {
+
+constexpr int kThreads = 192;
+
+__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t col_elem) {
+    // byte offset of bf16 element (row, col) inside a [rows][64] SW128 panel
+    return row * 128u + ((((col_elem >> 3) ^ (row & 7u)) << 4) | ((col_elem & 7u) << 1));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    fm_lcb_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWL,
+                  const __grid_constant__ CUtensorMap tmYT, const Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int npad = p.n_pad, kpad = p.k_pad, d = p.d;
+    const int panels_d = d / 64, panels_n = npad / 64 > 0 ? (npad + 63) / 64 : 1;
+    const uint32_t xpanel = (uint32_t)npad * 128u;           // bytes of one X panel
+    const uint32_t xstage = xpanel * panels_d;                // bytes of one X stage
+    const uint32_t wlpanel = 128u * 128u;                     // [128 rows][64] bf16
+    const uint32_t ytpanel = (uint32_t)kpad * 128u;
+    const uint32_t ppanel = (uint32_t)kpad * 128u;
+    uint8_t* sWL = smem;
+    uint8_t* sYT = sWL + wlpanel * panels_n;
+    uint8_t* sP = sYT + ytpanel * panels_n;
+    uint8_t* sX = sP + ((ppanel * panels_d + 1023) & ~1023u);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sX + 2 * xstage);
+    uint64_t* x_full = bars;        // [2]
+    uint64_t* x_empty = bars + 2;   // [2]
+    uint64_t* w_full = bars + 4;
+    uint64_t* pl_full = bars + 5;
+    uint64_t* pbuf_full = bars + 6;
+    uint64_t* f_full = bars + 7;
+    uint64_t* tmem_empty = bars + 8;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+    float* red = reinterpret_cast<float*>(bars + 10);  // [4] warp partials
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        tc::tma_prefetch(&tmX);
+        tc::tma_prefetch(&tmWL);
+        tc::tma_prefetch(&tmYT);
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&x_full[i], 1);
+            tc::mbar_init(&x_empty[i], 128);
+        }
+        tc::mbar_init(w_full, 1);
+        tc::mbar_init(pl_full, 1);
+        tc::mbar_init(pbuf_full, 128);
+        tc::mbar_init(f_full, 1);
+        tc::mbar_init(tmem_empty, 128);
+        tc::fence_mbar_init();
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, p.tmem_cols);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t t_P = tmem + 0, t_L = tmem + 64, t_F = tmem + 64 + (uint32_t)d;
+    const int m_tiles = (npad + 127) / 128;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            tc::mbar_expect_tx(w_full, wlpanel * panels_n + ytpanel * panels_n);
+            for (int pn = 0; pn < panels_n; ++pn) {
+                tc::tma_load_2d(sWL + pn * wlpanel, &tmWL, w_full, pn * 64, 0);
+                tc::tma_load_2d(sYT + pn * ytpanel, &tmYT, w_full, pn * 64, 0);
+            }
+            int it = 0;
+            for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
+                const int st = it & 1;
+                tc::mbar_wait(&x_empty[st], ((it >> 1) & 1) ^ 1);
+                tc::mbar_expect_tx(&x_full[st], xstage);
+                for (int pd = 0; pd < panels_d; ++pd)
+                    tc::tma_load_3d(sX + st * xstage + pd * xpanel, &tmX, &x_full[st], pd * 64, 0, (int)b);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            const uint32_t id_P = tc::idesc_bf16(128, kpad, 1, 0);  // A = X^T (MN-major)
+            const uint32_t id_L = tc::idesc_bf16(128, d, 0, 1);     // B = X (MN-major)
+            const uint32_t id_F = tc::idesc_bf16(128, kpad, 0, 0);
+            tc::mbar_wait(w_full, 0);
+            int it = 0;
+            for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
+                const int st = it & 1;
+                tc::mbar_wait(&x_full[st], (it >> 1) & 1);
+                tc::mbar_wait(tmem_empty, (it & 1) ^ 1);
+                tc::fence_after();
+                const uint32_t xs = tc::smem_u32(sX + st * xstage);
+                const uint32_t wl = tc::smem_u32(sWL), yt = tc::smem_u32(sYT);
+                for (int kk = 0; kk < npad / 16; ++kk) {
+                    const int k16 = kk * 16;
+                    const uint32_t kb_off = (uint32_t)(k16 / 64) , kin = (uint32_t)(k16 % 64) * 2;
+                    // P += X^T[:, k16:k16+16] . Y[k16:k16+16, :]
+                    const uint64_t a_xt = tc::sdesc(xs + k16 * 128, xpanel, 1024, 2);
+                    const uint64_t b_y = tc::sdesc(yt + kb_off * ytpanel + kin, 16, 1024, 2);
+                    tc::mma_f16(t_P, a_xt, b_y, id_P, kk != 0);
+                    // L += W_L[:, k16:k16+16] . X[k16:k16+16, :]
+                    const uint64_t a_wl = tc::sdesc(wl + kb_off * wlpanel + kin, 16, 1024, 2);
+                    const uint64_t b_x = tc::sdesc(xs + k16 * 128, xpanel, 1024, 2);
+                    tc::mma_f16(t_L, a_wl, b_x, id_L, kk != 0);
+                }
+                tc::mma_commit(pl_full);
+                tc::mbar_wait(pbuf_full, it & 1);
+                tc::fence_after();
+                const uint32_t pb = tc::smem_u32(sP);
+                for (int mt = 0; mt < m_tiles; ++mt) {
+                    for (int kk = 0; kk < d / 16; ++kk) {
+                        const int k16 = kk * 16;
+                        const uint32_t pan = (uint32_t)(k16 / 64), kin = (uint32_t)(k16 % 64) * 2;
+                        const uint64_t a_x = tc::sdesc(xs + pan * xpanel + mt * 16384 + kin, 16, 1024, 2);
+                        const uint64_t b_p = tc::sdesc(pb + pan * ppanel + kin, 16, 1024, 2);
+                        tc::mma_f16(t_F + mt * kpad, a_x, b_p, id_F, kk != 0);
+                    }
+                }
+                tc::mma_commit(f_full);
+            }
+        }
+    } else {  // ---- epilogue warps 2..5
+        const int q = warp & 3;
+        const int row = q * 32 + lane;  // TMEM lane
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        int it = 0;
+        for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
+            const int st = it & 1;
+            const uint32_t ph = it & 1;
+            uint8_t* xs = sX + st * xstage;
+            tc::mbar_wait(pl_full, ph);
+            tc::fence_after();
+            // P row `row` (= d index) -> bf16 -> Pbuf[j][row] (K-major B operand of F)
+            for (int c0 = 0; c0 < kpad; c0 += 16) {
+                float v[16];
+                tc::tmem_ld16(t_P + lane_off + c0, v);
+                if (row < d) {
+                    uint8_t* pan = sP + (row / 64) * ppanel;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        *reinterpret_cast<__nv_bfloat16*>(pan + swz(c0 + j, row & 63)) = __float2bfloat16_rn(v[j]);
+                }
+            }
+            tc::fence_async_shared();
+            tc::mbar_arrive(pbuf_full);
+            // LCB half: X'[nF+row] = rms_norm_d(L[row] + X[nF+row])
+            {
+                float ss = 0.0f;
+                const bool live = row < p.nL;
+                const int xr = p.nF + row;
+                for (int c0 = 0; c0 < d; c0 += 32) {
+                    float v[32];
+                    tc::tmem_ld32(t_L + lane_off + c0, v);
+                    if (live) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 8) {
+                            const int c = c0 + j;
+                            const uint4 r = *reinterpret_cast<const uint4*>(xs + (c / 64) * xpanel + swz(xr, c & 63));
+                            const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                v[j + 2 * i] += bf16_lo(w[i]);
+                                v[j + 2 * i + 1] += bf16_hi(w[i]);
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) ss += v[j] * v[j];
+                    }
+                }
+                const float denom = sqrtf(ss / (float)d + 1e-6f);
+                for (int c0 = 0; c0 < d; c0 += 32) {
+                    float v[32];
+                    tc::tmem_ld32(t_L + lane_off + c0, v);
+                    if (live) {
+                        __nv_bfloat16* dst = p.Xout + (b * p.n + xr) * (int64_t)d + c0;
+#pragma unroll
+                        for (int j = 0; j < 32; j += 8) {
+                            const int c = c0 + j;
+                            const uint4 r = *reinterpret_cast<const uint4*>(xs + (c / 64) * xpanel + swz(xr, c & 63));
+                            const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+                            float o[8];
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                o[2 * i] = (v[j + 2 * i] + bf16_lo(w[i])) / denom;
+                                o[2 * i + 1] = (v[j + 2 * i + 1] + bf16_hi(w[i])) / denom;
+                            }
+                            *reinterpret_cast<uint4*>(dst + j) =
+                                make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]),
+                                           pack_bf16x2(o[4], o[5]), pack_bf16x2(o[6], o[7]));
+                        }
+                    }
+                }
+            }
+            // FM: Fin = rms_norm(flatten(X P)) over the n*k real entries
+            tc::mbar_wait(f_full, ph);
+            tc::fence_after();
+            float ss = 0.0f;
+            for (int mt = 0; mt < m_tiles; ++mt) {
+                const int r = mt * 128 + row;
+                for (int c0 = 0; c0 < kpad; c0 += 16) {
+                    float v[16];
+                    tc::tmem_ld16(t_F + lane_off + mt * kpad + c0, v);
+                    if (r < p.n) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (c0 + j < p.k) ss += v[j] * v[j];
+                    }
+                }
+            }
+            ss = warp_sum(ss);
+            if (lane == 0) red[q] = ss;
+            tc::named_bar(1, 128);
+            const float total = red[0] + red[1] + red[2] + red[3];
+            const float denom = sqrtf(total / (float)(p.n * p.k) + 1e-6f);
+            for (int mt = 0; mt < m_tiles; ++mt) {
+                const int r = mt * 128 + row;
+                for (int c0 = 0; c0 < kpad; c0 += 16) {
+                    float v[16];
+                    tc::tmem_ld16(t_F + lane_off + mt * kpad + c0, v);
+                    if (r < p.n) {
+                        __nv_bfloat16* dst = p.Fout + b * (int64_t)p.n * p.k + (int64_t)r * p.k + c0;
+                        if ((p.k & 15) == 0) {
+#pragma unroll
+                            for (int j = 0; j < 16; j += 8)
+                                *reinterpret_cast<uint4*>(dst + j) = make_uint4(
+                                    pack_bf16x2(v[j] / denom, v[j + 1] / denom), pack_bf16x2(v[j + 2] / denom, v[j + 3] / denom),
+                                    pack_bf16x2(v[j + 4] / denom, v[j + 5] / denom), pack_bf16x2(v[j + 6] / denom, v[j + 7] / denom));
+                        } else {
+                            for (int j = 0; j < 16 && c0 + j < p.k; ++j) dst[j] = __float2bfloat16_rn(v[j] / denom);
+                        }
+                    }
+                }
+            }
+            tc::named_bar(1, 128);  // red[] reuse guard
+            tc::fence_before();
+            tc::mbar_arrive(tmem_empty);
+            tc::mbar_arrive(&x_empty[st]);
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc(tmem, p.tmem_cols);
+}
+
+size_t smem_bytes(const Params& p) {
+    const int panels_d = p.d / 64, panels_n = (p.n_pad + 63) / 64;
+    size_t s = 1024;
+    s += (size_t)128 * 128 * panels_n;            // W_L
+    s += (size_t)p.k_pad * 128 * panels_n;        // Y^T
+    s += ((size_t)p.k_pad * 128 * panels_d + 1023) & ~size_t(1023);  // P
+    s += 2 * (size_t)p.n_pad * 128 * panels_d;    // X stages
+    s += 256;
+    return s;
+}
+
+lattice_status check(const Params& p) {
+    if (!(p.d == 64 || p.d == 128)) return set_error(LATTICE_USAGE, "fm_lcb: d must be 64 or 128");
+    if (p.n < 1 || p.n_pad > 256 || p.n_pad % 16 || p.n_pad < p.n)
+        return set_error(LATTICE_USAGE, "fm_lcb: n must be <= 256");
+    if (p.k < 1 || p.k_pad > 64 || p.k_pad % 16 || p.k_pad < p.k)
+        return set_error(LATTICE_USAGE, "fm_lcb: k must be <= 64");
+    if (p.nL < 0 || p.nL > 128 || p.nF + p.nL != p.n)
+        return set_error(LATTICE_USAGE, "fm_lcb: nL must be <= 128 and nF + nL == n");
+    if (smem_bytes(p) > 227 * 1024) return set_error(LATTICE_USAGE, "fm_lcb: shared memory budget exceeded");
+    return LATTICE_OK;
+}
+
+lattice_status make_maps(Plan* pl, const void* X, const void* WLpad, const void* YTpad) {
+    const Params& p = pl->p;
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return set_error(LATTICE_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    cuuint64_t dims[3] = {(cuuint64_t)p.d, (cuuint64_t)p.n, (cuuint64_t)p.B};
+    cuuint64_t strides[2] = {(cuuint64_t)p.d * 2, (cuuint64_t)p.n * p.d * 2};
+    cuuint32_t box[3] = {64, (cuuint32_t)p.n_pad, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(&pl->tmX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(X), dims, strides,
+                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(LATTICE_CUDA, "fm_lcb: X tensor map (" + std::to_string((int)r) + ")");
+    lattice_status s = gemm::make_map_2d(&pl->tmWL, WLpad, (uint64_t)p.n_pad, 128, (uint64_t)p.n_pad * 2, 64, 128);
+    if (s != LATTICE_OK) return s;
+    return gemm::make_map_2d(&pl->tmYT, YTpad, (uint64_t)p.n_pad, (uint64_t)p.k_pad, (uint64_t)p.n_pad * 2, 64,
+                             (uint32_t)p.k_pad);
+}
+
+lattice_status launch(const Plan& pl, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        LAT_CUDA(cudaFuncSetAttribute(fm_lcb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    const int grid = (int)(pl.p.B < num_sms() ? pl.p.B : num_sms());
+    if (grid <= 0) return LATTICE_OK;
+    fm_lcb_kernel<<<grid, kThreads, smem_bytes(pl.p), st>>>(pl.tmX, pl.tmWL, pl.tmYT, pl.p);
+    LAT_CUDA(cudaGetLastError());
+    return LATTICE_OK;
+}
+
+}  // namespace fm
+}  // namespace lat

@@ -1,0 +1,135 @@
+"""K1 embedding-bag parity on the GPU through the C ABI.
+
+With the synthetic value scheme (k * 2^-10, |k| <= 128) every fp32 bag sum is exact, so the
+GPU output must equal the oracle bit for bit (fp32 out) or equal the one RNE rounding of the
+exact sum (bf16 out). Edge cases: empty bags, bad ids (first offender), permuted output rows,
+strided/offset output (sharding), D in {64, 128, 256}, fp32 and bf16 tables."""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+SEED_T, SEED_D = 0x1A77, 0x1A78
+
+
+def make(F, rows, D, B, max_len, dtype):
+    import torch
+    import paper_2512_09200_b200 as L
+    tab = torch.empty((F, rows, D), dtype=dtype, device="cuda")
+    L.fill_tables(tab, SEED_T)
+    offsets, ids = L.synth_bags(F, B, max_len, rows, SEED_D)
+    return tab, offsets, ids
+
+
+@pytest.mark.parametrize("D,tdt,odt", [(128, "f32", "f32"), (128, "bf16", "bf16"),
+                                       (128, "bf16", "f32"), (64, "f32", "f32"),
+                                       (64, "bf16", "bf16"), (256, "f32", "bf16")])
+def test_bit_exact_vs_oracle(D, tdt, odt):
+    import torch
+    import paper_2512_09200_b200 as L
+    dt = {"f32": torch.float32, "bf16": torch.bfloat16}
+    F, rows, B, max_len = 6, 5000, 700, 40
+    tab, offsets, ids = make(F, rows, D, B, max_len, dt[tdt])
+    out = L.embedding_bag(list(tab.unbind(0)), offsets, ids, B, out_dtype=dt[odt])
+    torch.cuda.synchronize()
+    o_cpu, i_cpu = oracle.synth_bags(F, B, max_len, rows, SEED_D)
+    assert (offsets.cpu().numpy() == o_cpu).all()
+    assert (ids[: o_cpu[-1]].cpu().numpy() == i_cpu).all()
+    ref, bad = oracle.embedding_bag_synth(SEED_T, F, rows, D, B, o_cpu, i_cpu)
+    assert bad == -1
+    got = out.float().cpu().numpy()
+    want = ref if odt == "f32" else oracle.bf16_round(ref)
+    assert np.array_equal(got, want)
+    lens = np.diff(o_cpu).reshape(F, B)
+    assert (lens == 0).any() and (got.transpose(1, 0, 2)[lens == 0] == 0).all()
+
+
+def test_normalize_permute_and_sharded_output():
+    import torch
+    import paper_2512_09200_b200 as L
+    F, rows, D, B = 4, 3000, 128, 513
+    tab, offsets, ids = make(F, rows, D, B, 20, torch.bfloat16)
+    perm = torch.randperm(B, device="cuda").to(torch.int32)
+    # write into features [3, 7) of an 11-feature row, rows permuted, rms-normalised
+    out = torch.zeros((B, 11, D), dtype=torch.bfloat16, device="cuda")
+    L.embedding_bag(list(tab.unbind(0)), offsets, ids, B, out=out, sample_pos=perm, normalize=True,
+                    out_row_stride=11 * D, out_feature_offset=3)
+    o_cpu, i_cpu = offsets.cpu().numpy(), ids.cpu().numpy()
+    ref, _ = oracle.embedding_bag_synth(SEED_T, F, rows, D, B, o_cpu, i_cpu)
+    ref64 = ref.astype(np.float64)
+    norm = ref64 / np.sqrt((ref64 ** 2).mean(-1, keepdims=True) + 1e-6)
+    got = out.float().cpu().numpy()[perm.cpu().numpy().astype(np.int64)]
+    np.testing.assert_allclose(got[:, 3:7], norm, rtol=8e-3, atol=1e-6)  # one bf16 rounding
+    assert (got[:, :3] == 0).all() and (got[:, 7:] == 0).all()
+
+
+def test_bad_id_reports_first_offender():
+    import torch
+    import paper_2512_09200_b200 as L
+    F, rows, D, B = 3, 100, 128, 64
+    tab, offsets, ids = make(F, rows, D, B, 10, torch.float32)
+    n = int(offsets[-1])
+    bad = [n - 3, n // 2, n // 3]
+    ids[bad[0]] = rows
+    ids[bad[1]] = -1
+    ids[bad[2]] = 1 << 30
+    with pytest.raises(L.DataError) as ei:
+        L.embedding_bag(list(tab.unbind(0)), offsets, ids, B)
+    assert ei.value.index == min(bad)
+    o_cpu, i_cpu = offsets.cpu().numpy(), ids.cpu().numpy()[:n]
+    assert oracle.embedding_bag_synth(SEED_T, F, rows, D, B, o_cpu, i_cpu)[1] == min(bad)
+
+
+def test_long_bags_and_empty_batch():
+    import torch
+    import paper_2512_09200_b200 as L
+    F, rows, D, B = 2, 1000, 128, 9
+    tab, _, _ = make(F, rows, D, B, 1, torch.float32)
+    lens = np.array([0, 1, 31, 32, 33, 64, 65, 200, 7] * F, np.int64)
+    offsets = np.zeros(F * B + 1, np.int64)
+    offsets[1:] = np.cumsum(lens)
+    ids = np.random.default_rng(0).integers(0, rows, offsets[-1]).astype(np.int32)
+    out = L.embedding_bag(list(tab.unbind(0)), torch.from_numpy(offsets).cuda(),
+                          torch.from_numpy(ids).cuda(), B)
+    ref, _ = oracle.embedding_bag_synth(SEED_T, F, rows, D, B, offsets, ids)
+    assert np.array_equal(out.cpu().numpy(), ref)
+    empty = L.embedding_bag(list(tab.unbind(0)), torch.zeros(1, dtype=torch.int64, device="cuda"),
+                            torch.zeros(1, dtype=torch.int32, device="cuda"), 0)
+    assert empty.shape == (0, F, D)
+
+
+def test_domain_bucket_is_stable_sort():
+    import paper_2512_09200_b200 as L
+    for B, G in [(1, 1), (1000, 4), (65536, 16), (32768, 3)]:
+        dom = L.synth_domains(B, G, 99)
+        pos, order, seg = L.domain_bucket(dom, G)
+        d = dom.cpu().numpy()
+        assert (d == oracle.synth_domains(B, G, 99)).all()
+        want_order = np.argsort(d, kind="stable")
+        assert (order.cpu().numpy() == want_order).all()
+        assert (pos.cpu().numpy()[want_order] == np.arange(B)).all()
+        assert (seg.cpu().numpy() == np.concatenate([[0], np.cumsum(np.bincount(d, minlength=G))])).all()
+
+
+def test_rownorm_matches_reference_numerics():
+    import json
+    import os
+    import torch
+    import paper_2512_09200_b200 as L
+    with open(os.path.join(os.path.dirname(__file__), "golden", "numerics_ref.json")) as f:
+        g = json.load(f)
+    names = ["rms_norm", "swish_rn", "swish_rn_hard"]
+    for c in g["cases"]:
+        if max(abs(v) for v in c["x"]) > 1e5:
+            continue  # fp32 GPU path; the 1e6 probe is checked for finiteness below
+        x = torch.tensor([c["x"]], dtype=torch.float32, device="cuda")
+        for mode, name in enumerate(names):
+            got = L.rownorm(x, mode).cpu().numpy()[0]
+            np.testing.assert_allclose(got, c[name], rtol=2e-5, atol=2e-6)
+    huge = torch.tensor([[1e6] * 7 + [-1e6]], device="cuda")
+    assert torch.isfinite(L.rownorm(huge, 1)).all()
+    with pytest.raises(L.DataError):
+        L.rownorm(torch.tensor([[1.0, float("nan")]], device="cuda"), 1)
+    with pytest.raises(L.UsageError):
+        L.rownorm(torch.zeros((1, 0), device="cuda"), 1)

@@ -1,0 +1,75 @@
+"""K3 tcgen05 GEMM + fused epilogues vs a plain PyTorch fp32 reference of the same op
+(bf16 operands, fp32 accumulation). Tolerances: fp32 output rtol 1e-4 (accumulation order
+only); bf16 outputs one bf16 rounding (rel 2^-8) plus fp32 epilogue math."""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def ref_swish(z, hard=False):
+    import torch
+    r = z / torch.sqrt((z * z).mean(-1, keepdim=True) + 1e-6)
+    return r * (torch.clamp((r + 3) / 6, 0, 1) if hard else torch.sigmoid(r))
+
+
+def operands(M, N, K, seed=0):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    A = (torch.randn((M, K), generator=g, device="cuda") * 0.5).to(torch.bfloat16)
+    B = (torch.randn((N, K), generator=g, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    return A, B
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 512, 1024), (1000, 768, 2048),
+                                   (129, 100, 72), (4096, 2048, 8192)])
+def test_store_fp32(M, N, K):
+    import torch
+    import paper_2512_09200_b200 as L
+    A, B = operands(M, N, K)
+    C = L.gemm(A, B, out_dtype=torch.float32)
+    ref = A.float() @ B.float().t()
+    torch.testing.assert_close(C, ref, rtol=1e-4, atol=1e-4)
+
+
+def test_store_bf16():
+    import torch
+    import paper_2512_09200_b200 as L
+    A, B = operands(512, 1024, 512)
+    C = L.gemm(A, B)
+    ref = (A.float() @ B.float().t()).to(torch.bfloat16)
+    torch.testing.assert_close(C.float(), ref.float(), rtol=8e-3, atol=1e-3)
+
+
+@pytest.mark.parametrize("N", [256, 384, 512, 2048])
+@pytest.mark.parametrize("hard", [False, True])
+def test_swish_rn_full_row(N, hard):
+    import torch
+    import paper_2512_09200_b200 as L
+    A, B = operands(700, N, 512, seed=N)
+    C = L.gemm(A, B, epilogue=L.EPI_SWISH_HARD if hard else L.EPI_SWISH)
+    ref = ref_swish(A.float() @ B.float().t(), hard)
+    torch.testing.assert_close(C.float(), ref, rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("group", [128, 64])
+def test_residual_group_norm(group):
+    import torch
+    import paper_2512_09200_b200 as L
+    M, N, K = 513, 1024, 768
+    A, B = operands(M, N, K, seed=3)
+    R = torch.randn((M, N), device="cuda").to(torch.bfloat16)
+    C = L.gemm(A, B, epilogue=L.EPI_RESID_NORM, resid=R, group=group)
+    z = (A.float() @ B.float().t() + R.float()).view(M, N // group, group)
+    ref = (z / torch.sqrt((z * z).mean(-1, keepdim=True) + 1e-6)).view(M, N)
+    torch.testing.assert_close(C.float(), ref, rtol=1e-2, atol=1e-2)
+
+
+def test_contract_errors():
+    import torch
+    import paper_2512_09200_b200 as L
+    A, B = operands(64, 256, 60)
+    with pytest.raises(L.UsageError):
+        L.gemm(A, B)  # K % 8 != 0 -> TMA stride alignment
+    A, B = operands(64, 4096, 64)
+    with pytest.raises(L.UsageError):
+        L.gemm(A, B, epilogue=L.EPI_SWISH)  # row wider than one 8-CTA cluster
