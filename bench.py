@@ -245,13 +245,258 @@ def cpu_baseline_micro(seconds=15.0):
             "sample": f"{n} of {B} samples of the micro batch ({dt:.1f} s, tables regenerated lazily)"}
 
 
+# ------------------------------------------------------------------------------------------------
+# mid: the Lattice Network step (configs[2]); builder widths from SURVEY.md 8d
+# ------------------------------------------------------------------------------------------------
+MID = dict(n=256, d=128, blocks=4, nF=128, nL=128, k=32, mlp=[8192, 2048, 2048, 16384],
+           domains=4, heads=6, tower_hidden=512)
+MID_ROWS, MID_B, MID_MAXLEN = 100_000, 32768, 40
+SEED_W = 0x1A79
+
+
+def dense_flops_per_sample(c):
+    n, d, k, nL = c["n"], c["d"], c["k"], c["nL"]
+    mlp = c["mlp"]
+    per_block = 4 * n * d * k + 2 * nL * n * d + 2 * sum(mlp[i] * mlp[i + 1] for i in range(len(mlp) - 1))
+    return c["blocks"] * per_block + 2 * (n * d * c["tower_hidden"] + c["tower_hidden"] * c["heads"])
+
+
+def mlp_flops_per_sample(c):
+    mlp = c["mlp"]
+    return 2 * sum(mlp[i] * mlp[i + 1] for i in range(len(mlp) - 1))
+
+
+def run_mid(args, rank, world, local):
+    import torch
+    import paper_2512_09200_b200 as L
+    c = MID
+    n, d, B = c["n"], c["d"], MID_B
+    net = L.Network(**c, max_batch=B, weight_seed=SEED_W)
+    tab = torch.empty((n, MID_ROWS, d), dtype=torch.bfloat16, device="cuda")
+    L.fill_tables(tab, SEED_T)
+    ptrs = torch.tensor([t.data_ptr() for t in tab.unbind(0)], dtype=torch.int64, device="cuda")
+    rows = torch.full((n,), MID_ROWS, dtype=torch.int64, device="cuda")
+    offsets, ids = L.synth_bags(n, B, MID_MAXLEN, MID_ROWS, SEED_D + rank)
+    dom = L.synth_domains(B, c["domains"], SEED_D + rank)
+    n_ids = int(offsets[-1].item())
+    logits = torch.empty((B, c["heads"]), dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        net.forward(dom, offsets, ids, ptrs, rows, torch.bfloat16, logits=logits)
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        barrier(world)
+        torch.cuda.synchronize()
+        clk.mark()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
+    value = world * B / (ms / 1e3)
+
+    # per-stage device times (separate pass, events between stages)
+    net.set_timing(True)
+    stages = []
+    for _ in range(3):
+        step()
+        stages.append(net.stage_times())
+    net.set_timing(False)
+    st = [statistics.median(s[i] for s in stages) for i in range(len(stages[0]))]
+    # stages: [bucket, bag, (fm_lcb, mlp) x blocks, tower]
+    t_bag = st[1]
+    t_fm = [st[2 + 2 * b] for b in range(c["blocks"])]
+    t_mlp = [st[3 + 2 * b] for b in range(c["blocks"])]
+    t_tower = st[2 + 2 * c["blocks"]]
+    hbm, tf_burst, tf_sust, src = load_peaks()
+    emb_bytes = micro_bytes(n_ids, n, B, d, 2, 2)
+    flops = dense_flops_per_sample(c) * B
+    mlp_fl = mlp_flops_per_sample(c) * B
+    mlp_ms = statistics.mean(t_mlp)
+    mlp_achieved = mlp_fl / (mlp_ms / 1e3) / 1e12
+    dense_ms = sum(t_fm) + sum(t_mlp) + t_tower
+    fm_bytes = B * (n * d * 2 + n * c["k"] * 2 + c["nL"] * d * 2)
+
+    # e2e through the public call: pinned-host sparse batch -> H2D (copy stream, double
+    # buffered) -> forward -> D2H logits, every step inside the timed region
+    h_off = offsets.cpu().pin_memory()
+    h_ids = ids[:n_ids].cpu().pin_memory()
+    h_dom = dom.cpu().pin_memory()
+    h_out = torch.empty((B, c["heads"]), dtype=torch.float32, pin_memory=True)
+    bufs = [(torch.empty_like(offsets), torch.empty(n_ids, dtype=torch.int32, device="cuda"),
+             torch.empty_like(dom)) for _ in range(2)]
+    cstream = torch.cuda.Stream()
+    copied = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+
+    def h2d(i):
+        o, ii, dm = bufs[i % 2]
+        with torch.cuda.stream(cstream):
+            cstream.wait_event(consumed[i % 2])
+            o.copy_(h_off, non_blocking=True)
+            ii.copy_(h_ids, non_blocking=True)
+            dm.copy_(h_dom, non_blocking=True)
+            copied[i % 2].record(cstream)
+
+    def e2e_run(k):
+        for e in consumed:
+            e.record(stream)
+        h2d(0)
+        for i in range(k):
+            if i + 1 < k:
+                h2d(i + 1)
+            stream.wait_event(copied[i % 2])
+            o, ii, dm = bufs[i % 2]
+            net.forward(dm, o, ii, ptrs, rows, torch.bfloat16, logits=logits)
+            consumed[i % 2].record(stream)
+            h_out.copy_(logits, non_blocking=True)
+
+    e2e_run(2)
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    e2e_run(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+
+    launches = 3 + c["blocks"] * (1 + len(c["mlp"]) - 1) + 1
+    res = {
+        "metric": "Lattice Network samples/sec (mid config, forward step)",
+        "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (counter-based tables/bags/weights)",
+        "config": {"workload": "mid Lattice Network: 256 sparse feats x 100k rows x 128, l=4 DWFB "
+                               "blocks (nF=nL=128, k=32, MLP 8192-2048-2048-16384), 4 domains x 6 "
+                               "heads, tower 32768-512-6, B=32768/GPU",
+                   "global_batch": world * B, "ids_per_step": n_ids,
+                   "l2": "embedding rows drawn uniformly from 6.6 GB of tables; activations 2.1 GB/buffer (> L2)",
+                   "parallelism": f"replicas x{world}"},
+        "e2e": {"value": world * B / (e2e_ms / 1e3), "unit": "samples/s",
+                "h2d_bytes_per_step": (n * B + 1) * 8 + n_ids * 4 + B * 4,
+                "d2h_bytes_per_step": B * c["heads"] * 4},
+        "roofline": {"bound": "tensor", "achieved": mlp_achieved, "peak": tf_sust, "unit": "TFLOP/s",
+                     "frac": mlp_achieved / tf_sust, "traffic": None,
+                     "kernel": "gemm_kernel (FMB MLP, 3 GEMMs per block, fused swish_rn / residual-norm)",
+                     "peak_source": f"{src} sustained (kernel timed inside the step)",
+                     "algorithmic_flops_per_launch_group": mlp_fl, "ms": mlp_ms},
+        "stages": {
+            "embedding": {"ms": t_bag, "bytes": emb_bytes, "GB/s": emb_bytes / (t_bag / 1e3) / 1e9,
+                          "frac_hbm": emb_bytes / (t_bag / 1e3) / 1e9 / hbm},
+            "fm_lcb": {"ms_per_block": statistics.mean(t_fm), "bytes_per_block": fm_bytes,
+                       "GB/s": fm_bytes / (statistics.mean(t_fm) / 1e3) / 1e9,
+                       "frac_hbm": fm_bytes / (statistics.mean(t_fm) / 1e3) / 1e9 / hbm},
+            "mlp": {"ms_per_block": mlp_ms, "TFLOP/s": mlp_achieved, "frac_tensor_sustained": mlp_achieved / tf_sust,
+                    "frac_tensor_burst": mlp_achieved / tf_burst},
+            "tower": {"ms": t_tower, "TFLOP/s": 2 * B * n * d * c["tower_hidden"] / (t_tower / 1e3) / 1e12},
+            "dense_total": {"ms": dense_ms, "TFLOP": flops / 1e12,
+                            "TFLOP/s": flops / (dense_ms / 1e3) / 1e12},
+            "bucket_ms": st[0],
+        },
+        "gpu_launches": launches * args.steps,
+        "clocks": clk.summary(),
+    }
+    return res
+
+
+def cpu_baseline_mid(seconds=15.0, threads=None):
+    """Oracle port of the mid forward (embedding bag + network, fp64) on a bounded sample."""
+    import numpy as np
+    import oracle
+    c = MID
+    threads = threads or os.cpu_count() or 1
+    lib = oracle.load_oracle()
+    n, d = c["n"], c["d"]
+    # weights from the counter-based generator, on the host (no GPU needed for this leg)
+    w = host_weights(c)
+    o, i = oracle.synth_bags(n, 512, MID_MAXLEN, MID_ROWS, SEED_D)
+    dom = oracle.synth_domains(512, c["domains"], SEED_D)
+    cfg, ws, keep = oracle_net(c, w)
+    t0 = time.perf_counter()
+    done = 0
+    chunk = max(threads, 4)
+    while time.perf_counter() - t0 < seconds and done + chunk <= 512:
+        pooled, _ = oracle.embedding_bag_synth(SEED_T, n, MID_ROWS, d, 512, o, i, done, done + chunk, threads)
+        out = np.zeros((chunk, c["heads"]), np.float32)
+        dd = np.ascontiguousarray(dom[done:done + chunk])
+        lib.lo_net_forward(oracle.ctypes.byref(cfg), oracle.ctypes.byref(ws), chunk, oracle.ptr(pooled),
+                           oracle.ptr(dd), oracle.ptr(out), threads)
+        done += chunk
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"{done} samples of the mid batch ({dt:.1f} s; tables regenerated lazily; "
+                      f"rate extrapolated to the 32768-sample batch)"}
+
+
+_HOST_W = {}
+
+
+def host_weights(c):
+    """Mid weights via the oracle generator (bf16-exact), cached."""
+    import numpy as np
+    import oracle
+    key = json.dumps(c, sort_keys=True)
+    if key in _HOST_W:
+        return _HOST_W[key]
+    lib = oracle.load_oracle()
+
+    def tensor(block, kind, index, out_f, fan_in):
+        buf = np.zeros((out_f, fan_in), np.float32)
+        lib.lo_fill_weights(oracle.ptr(buf), out_f, fan_in, SEED_W, lib.lo_weight_tag(block, kind, index))
+        return buf
+
+    w = {"YT": [], "WL": [], "mlp": []}
+    for blk in range(c["blocks"]):
+        w["YT"].append(tensor(blk, 1, 0, c["k"], c["n"]))
+        w["WL"].append(tensor(blk, 2, 0, c["nL"], c["n"]))
+        for li in range(len(c["mlp"]) - 1):
+            w["mlp"].append(tensor(blk, 3, li, c["mlp"][li + 1], c["mlp"][li]))
+    nd = c["n"] * c["d"]
+    w["T1"] = np.stack([tensor(g, 4, 0, c["tower_hidden"], nd) for g in range(c["domains"])])
+    w["T2"] = np.stack([tensor(g, 5, 0, c["heads"], c["tower_hidden"]) for g in range(c["domains"])])
+    _HOST_W[key] = w
+    return w
+
+
+def oracle_net(c, w):
+    import numpy as np
+    import oracle
+    cfg = oracle.LoNetCfg()
+    cfg.n, cfg.d, cfg.blocks, cfg.nF, cfg.nL, cfg.k = c["n"], c["d"], c["blocks"], c["nF"], c["nL"], c["k"]
+    cfg.n_mlp = len(c["mlp"]) - 1
+    for i, v in enumerate(c["mlp"]):
+        cfg.mlp[i] = v
+    cfg.G, cfg.heads, cfg.tower_hidden, cfg.hard, cfg.bf16 = c["domains"], c["heads"], c["tower_hidden"], 0, 1
+    keep = [np.ascontiguousarray(a, dtype=np.float32) for a in w["YT"] + w["WL"] + w["mlp"]]
+    nb = c["blocks"]
+    P = oracle.ctypes.c_void_p
+    yt = (P * nb)(*[a.ctypes.data for a in keep[:nb]])
+    wl = (P * nb)(*[a.ctypes.data for a in keep[nb:2 * nb]])
+    ml = (P * len(w["mlp"]))(*[a.ctypes.data for a in keep[2 * nb:]])
+    T1 = np.ascontiguousarray(w["T1"], dtype=np.float32)
+    T2 = np.ascontiguousarray(w["T2"], dtype=np.float32)
+    keep += [T1, T2, yt, wl, ml]
+    ws = oracle.LoNetWeights(oracle.ctypes.cast(yt, P), oracle.ctypes.cast(wl, P), oracle.ctypes.cast(ml, P),
+                             P(T1.ctypes.data), P(T2.ctypes.data))
+    return cfg, ws, keep
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="micro", choices=["micro"])
-    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--workload", default="mid", choices=["mid", "micro"])
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"], help="micro table dtype")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
@@ -261,27 +506,39 @@ def main():
         rank = int(os.environ.get("RANK", "0"))
         if rank != 0:
             return
-        steps = []
-        for _ in range(args.warmup + args.steps):
-            steps.append(cpu_baseline_micro(seconds=max(2.0, args.cpu_seconds / max(args.steps, 1))))
-        vals = [s["value"] for s in steps[args.warmup:]]
-        v = statistics.median(vals)
+        per_step = max(0.5, min(3.0, 60.0 / (args.warmup + args.steps)))
+        base = cpu_baseline_mid if args.workload == "mid" else cpu_baseline_micro
+        steps = [base(seconds=per_step) for _ in range(args.warmup + args.steps)]
+        v = statistics.median([s["value"] for s in steps[args.warmup:]])
         cb = dict(steps[-1])
         cb["value"] = v
-        print(json.dumps({"impl": "reference", "metric": "embedding-bag samples/sec (configs[1] microbench)",
-                          "value": v, "unit": "samples/s", "n_gpus": 0, "steps": args.steps,
-                          "warmup": args.warmup, "higher_is_better": True,
-                          "config": {"workload": "micro: 64 tables x 1M rows x 128, B=16384, bags U[0,40]"},
-                          "dtype": "f32", "data": "synthetic", "cpu_baseline": cb,
+        if args.workload == "mid":
+            metric = "Lattice Network samples/sec (mid config, forward step)"
+            wl = ("mid Lattice Network (CPU oracle port, fp64 with bf16 rounding emulation): "
+                  "256 sparse feats x 100k rows x 128, l=4, B=32768")
+            dtype = "f64"
+        else:
+            metric = "embedding-bag samples/sec (configs[1] microbench)"
+            wl = "micro: 64 tables x 1M rows x 128, B=16384, bags U[0,40]"
+            dtype = "f32"
+        print(json.dumps({"impl": "reference", "metric": metric, "value": v, "unit": "samples/s",
+                          "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+                          "higher_is_better": True, "config": {"workload": wl}, "dtype": dtype,
+                          "data": "synthetic", "cpu_baseline": cb,
                           "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
                                   "d2h_bytes_per_step": 0}}))
         return
 
     rank, world, local = dist_setup(args.gpus)
-    res, _ = run_micro(args, rank, world, local)
+    if args.workload == "mid":
+        res = run_mid(args, rank, world, local)
+        base = cpu_baseline_mid
+    else:
+        res, _ = run_micro(args, rank, world, local)
+        base = cpu_baseline_micro
     if rank == 0:
         if world == 1:
-            res["cpu_baseline"] = cpu_baseline_micro(args.cpu_seconds)
+            res["cpu_baseline"] = base(args.cpu_seconds)
         print(json.dumps(res))
     if world > 1:
         import torch.distributed as dist

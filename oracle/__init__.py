@@ -81,6 +81,8 @@ def load_oracle():
         lib.lo_synth_bags.argtypes = [ctypes.c_int, _I64, ctypes.c_int, _I64, _U64, _P, _P]
         lib.lo_synth_domains.restype = None
         lib.lo_synth_domains.argtypes = [_I64, ctypes.c_int, _U64, _P]
+        lib.lo_fill_weights.restype = None
+        lib.lo_fill_weights.argtypes = [_P, _I64, _I64, _U64, _U64]
         lib.lo_bf16_round.restype = ctypes.c_float
         lib.lo_bf16_round.argtypes = [ctypes.c_float]
         _oracle = lib

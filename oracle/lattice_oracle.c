@@ -434,3 +434,13 @@ void lo_synth_bags(int F, int64_t B, int max_len, int64_t rows, uint64_t seed, i
 void lo_synth_domains(int64_t B, int G, uint64_t seed, int32_t* dom) {
     for (int64_t i = 0; i < B; ++i) dom[i] = (int32_t)(lo_gen(seed, LO_TAG_DOM, (uint64_t)i) % (uint64_t)G);
 }
+
+void lo_fill_weights(float* out, int64_t out_features, int64_t fan_in, uint64_t seed, uint64_t tag) {
+    const int shift = lo_weight_shift(fan_in);
+    const int64_t n = out_features * fan_in;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+    for (int64_t i = 0; i < n; ++i)
+        out[i] = ldexpf((float)(int8_t)(lo_gen(seed, tag, (uint64_t)i) >> 56), -shift);
+}

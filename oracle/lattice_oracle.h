@@ -74,6 +74,8 @@ float lo_table_value(uint64_t seed, int64_t f, int64_t r, int D, int64_t rows, i
  * (int8)(H(seed, tag, o*fan_in + i) >> 56) * 2^-(7 + floor(log2(fan_in)/2)). Exact in bf16. */
 float lo_weight_value(uint64_t seed, uint64_t tag, int64_t o, int64_t i, int64_t fan_in);
 int lo_weight_shift(int64_t fan_in);
+/* Whole [out_features][fan_in] tensor of lo_weight_value, OpenMP-parallel. */
+void lo_fill_weights(float* out, int64_t out_features, int64_t fan_in, uint64_t seed, uint64_t tag);
 uint64_t lo_weight_tag(int block, int kind, int index);
 
 /* ---- embedding bag (builder semantics in DESIGN.md 3.1) ----------------- */

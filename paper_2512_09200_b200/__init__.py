@@ -279,3 +279,104 @@ def gemm(A, B, epilogue=EPI_STORE, out_dtype=None, resid=None, group=128, out=No
                  resid.stride(0) if resid is not None else 0, group)
     check(_lib.lattice_gemm(ctypes.byref(a), _stream(stream)))
     return out
+
+
+# ---- network -------------------------------------------------------------------------------------
+
+class _CAI:
+    """Minimal __cuda_array_interface__ holder to view library-owned device memory."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": tuple(shape),
+                                         "typestr": typestr, "version": 3, "strides": None}
+
+
+def _view(ptr, shape, dtype):
+    import torch
+    if dtype == torch.bfloat16:
+        return torch.as_tensor(_CAI(ptr, shape, "<i2"), device="cuda").view(torch.bfloat16)
+    return torch.as_tensor(_CAI(ptr, shape, "<f4"), device="cuda")
+
+
+def _pad16(x):
+    return (x + 15) // 16 * 16
+
+
+class Network:
+    """lattice::Network over the C ABI (lattice_net_*). Weights live on the current device."""
+
+    def __init__(self, n, d, blocks, nF, nL, k, mlp, domains, heads, tower_hidden, hard=False,
+                 max_batch=32768, weight_seed=0x1A78):
+        self.cfg = dict(n=n, d=d, blocks=blocks, nF=nF, nL=nL, k=k, mlp=list(mlp), domains=domains,
+                        heads=heads, tower_hidden=tower_hidden, hard=hard, max_batch=max_batch,
+                        weight_seed=weight_seed)
+        c = NetConfig()
+        c.n, c.d, c.blocks, c.nF, c.nL, c.k = n, d, blocks, nF, nL, k
+        c.n_mlp = len(mlp) - 1
+        for i, w in enumerate(mlp):
+            c.mlp[i] = w
+        c.domains, c.heads, c.tower_hidden, c.hard = domains, heads, tower_hidden, int(hard)
+        c.max_batch, c.weight_seed = max_batch, weight_seed
+        h = ctypes.c_void_p()
+        check(_lib.lattice_net_create(ctypes.byref(c), ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lattice_net_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def forward(self, domain, offsets=None, ids=None, table_ptrs=None, rows=None,
+                table_dtype=None, pooled=None, logits=None, stream=None):
+        import torch
+        B = domain.shape[0]
+        if logits is None:
+            logits = torch.empty((B, self.cfg["heads"]), dtype=torch.float32, device=domain.device)
+        b = Batch()
+        b.batch = B
+        b.domain = _p(domain)
+        if pooled is not None:
+            b.table_dtype = F32 if pooled.dtype == torch.float32 else BF16
+            b.pooled = _p(pooled)
+        else:
+            b.table_dtype = F32 if table_dtype == torch.float32 else BF16
+            b.tables, b.rows, b.offsets, b.ids = _p(table_ptrs), _p(rows), _p(offsets), _p(ids)
+        check(_lib.lattice_net_forward(self._h, ctypes.byref(b), _p(logits), _stream(stream)))
+        return logits
+
+    def set_timing(self, on=True):
+        check(_lib.lattice_net_set_timing(self._h, 1 if on else 0))
+
+    def stage_times(self):
+        buf = (ctypes.c_float * 64)()
+        n = _I32()
+        check(_lib.lattice_net_stage_times(self._h, buf, 64, ctypes.byref(n)))
+        return [buf[i] for i in range(n.value)]
+
+    def weights(self):
+        """Host fp32 copies of every weight, unpadded, in the oracle's layout."""
+        import torch
+        c = self.cfg
+        n, d, k, nL = c["n"], c["d"], c["k"], c["nL"]
+        out = {"YT": [], "WL": [], "mlp": []}
+        for blk in range(c["blocks"]):
+            yt = _view(_lib.lattice_net_weight(self._h, blk, 1, 0), (_pad16(k), _pad16(n)), torch.bfloat16)
+            wl = _view(_lib.lattice_net_weight(self._h, blk, 2, 0), (128, _pad16(n)), torch.bfloat16)
+            out["YT"].append(yt[:k, :n].float().cpu().numpy().copy())
+            out["WL"].append(wl[:nL, :n].float().cpu().numpy().copy())
+            for li in range(len(c["mlp"]) - 1):
+                w = _view(_lib.lattice_net_weight(self._h, blk, 3, li),
+                          (c["mlp"][li + 1], c["mlp"][li]), torch.bfloat16)
+                out["mlp"].append(w.float().cpu().numpy().copy())
+        G, th, H = c["domains"], c["tower_hidden"], c["heads"]
+        out["T1"] = _view(_lib.lattice_net_weight(self._h, 0, 4, 0), (G, th, n * d),
+                          torch.bfloat16).float().cpu().numpy().copy()
+        out["T2"] = _view(_lib.lattice_net_weight(self._h, 0, 5, 0), (G, H, th),
+                          torch.float32).cpu().numpy().copy()
+        return out

@@ -40,9 +40,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int npad = p.n_pad, kpad = p.k_pad, d = p.d;
-    const int panels_d = d / 64, panels_n = npad / 64 > 0 ? (npad + 63) / 64 : 1;
-    const uint32_t xpanel = (uint32_t)npad * 128u;           // bytes of one X panel
-    const uint32_t xstage = xpanel * panels_d;                // bytes of one X stage
+    const int panels_d = d / 64, panels_n = (npad + 63) / 64;
+    // An X stage always spans 2 panels of >= 128 rows so that every M=128 operand view
+    // (F's A rows, the second MN chunk of X^T when d = 64) stays inside the allocation;
+    // rows/panels beyond the loaded n_pad x d image are never consumed.
+    const uint32_t xpanel = (uint32_t)(npad > 128 ? npad : 128) * 128u;
+    const uint32_t xstage = xpanel * 2;
+    const uint32_t xbytes = (uint32_t)npad * 128u * panels_d;  // bytes TMA actually lands
     const uint32_t wlpanel = 128u * 128u;                     // [128 rows][64] bf16
     const uint32_t ytpanel = (uint32_t)kpad * 128u;
     const uint32_t ppanel = (uint32_t)kpad * 128u;
@@ -96,7 +100,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
                 const int st = it & 1;
                 tc::mbar_wait(&x_empty[st], ((it >> 1) & 1) ^ 1);
-                tc::mbar_expect_tx(&x_full[st], xstage);
+                tc::mbar_expect_tx(&x_full[st], xbytes);
                 for (int pd = 0; pd < panels_d; ++pd)
                     tc::tma_load_3d(sX + st * xstage + pd * xpanel, &tmX, &x_full[st], pd * 64, 0, (int)b);
             }
@@ -272,7 +276,8 @@ size_t smem_bytes(const Params& p) {
     s += (size_t)128 * 128 * panels_n;            // W_L
     s += (size_t)p.k_pad * 128 * panels_n;        // Y^T
     s += ((size_t)p.k_pad * 128 * panels_d + 1023) & ~size_t(1023);  // P
-    s += 2 * (size_t)p.n_pad * 128 * panels_d;    // X stages
+    (void)panels_d;
+    s += 2 * 2 * (size_t)(p.n_pad > 128 ? p.n_pad : 128) * 128;  // X stages (2 panels each)
     s += 256;
     return s;
 }

@@ -207,8 +207,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = 0; c < BN; c += 32) {
                 float v[32];
                 tc::tmem_ld32(taddr + c, v);
+                // columns >= N may hold another group's weights (stacked towers): mask them
 #pragma unroll
-                for (int j = 0; j < 32; ++j) ss += v[j] * v[j];
+                for (int j = 0; j < 32; ++j) ss += (n0 + c + j < p.N) ? v[j] * v[j] : 0.0f;
             }
             const float total = cluster_row_sum(ss, row, C, xbuf, xbar, 0);
             const float denom = sqrtf(total / (float)p.N_full + 1e-6f);
@@ -232,16 +233,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc::tmem_ld32(taddr + c, v);
                     if (n0 + c >= p.N) continue;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = act_swish(v[j] / denom, hard);
+                    for (int j = 0; j < 32; ++j) v[j] = (n0 + c + j < p.N) ? act_swish(v[j] / denom, hard) : 0.0f;
 #pragma unroll
                     for (int h = 0; h < kMaxHeads; ++h) {
                         if (h < p.heads) {
                             const float* wr = w2 + (size_t)h * p.N_full + n0 + c;
                             float a = 0.0f;
+                            if (n0 + c + 32 <= p.N) {
 #pragma unroll
-                            for (int j = 0; j < 32; j += 4) {
-                                const float4 w = __ldg(reinterpret_cast<const float4*>(wr + j));
-                                a += v[j] * w.x + v[j + 1] * w.y + v[j + 2] * w.z + v[j + 3] * w.w;
+                                for (int j = 0; j < 32; j += 4) {
+                                    const float4 w = __ldg(reinterpret_cast<const float4*>(wr + j));
+                                    a += v[j] * w.x + v[j + 1] * w.y + v[j + 2] * w.z + v[j + 3] * w.w;
+                                }
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 32; ++j)
+                                    if (n0 + c + j < p.N) a += v[j] * __ldg(wr + j);
                             }
                             part[h] += a;
                         }

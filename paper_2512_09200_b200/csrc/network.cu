@@ -1,0 +1,430 @@
+// network.cu -- lattice_net: the consolidated MDMO forward step on one GPU.
+//
+//   K6 domain_bucket      stable counting sort by domain -> pos/order/seg + tower tile table
+//   K1 embedding_bag      pooled sums, rms_norm over d, written straight into domain-sorted
+//                         rows of X0 (so towers read contiguous segments, no permute copy)
+//   per block (l times):  K2 fm_lcb (P, F, Fin, LCB half of X')  ->  K3 MLP GEMMs with fused
+//                         swish_rn  ->  K3 last GEMM with fused residual + rms_norm_d (FMB half)
+//   K4 towers             one grouped GEMM over the G domain segments, swish_rn + heads fused,
+//                         logits written back in the caller's sample order
+// All weights are bf16 (tower heads fp32), generated on device from weight_seed with the
+// counter-based scheme shared with oracle/lattice_oracle.c.
+#include <cuda_bf16.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "fm_lcb.h"
+#include "gemm_host.h"
+
+namespace lat {
+namespace {
+
+__global__ void tiles_kernel(const int32_t* __restrict__ seg, int G, int4* __restrict__ tiles,
+                             int* __restrict__ n_tiles) {
+    __shared__ int pre[65];
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int g = 0; g < G; ++g) {
+            pre[g] = run;
+            run += (seg[g + 1] - seg[g] + 127) / 128;
+        }
+        pre[G] = run;
+        *n_tiles = run;
+    }
+    __syncthreads();
+    const int total = pre[G];
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+        int g = 0;
+        while (pre[g + 1] <= t) ++g;
+        const int r0 = seg[g] + (t - pre[g]) * 128;
+        tiles[t] = make_int4(g, r0, seg[g + 1], 0);
+    }
+}
+
+// pooled sums (caller order, [B][n][d] f32 or bf16) -> rms_norm_d -> bf16 row pos[b] of X0
+template <typename T>
+__global__ void pooled_norm_kernel(int64_t B, int n, int d, const T* __restrict__ in,
+                                   const int32_t* __restrict__ pos, __nv_bfloat16* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < B * n;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t b = w / n;
+        const int f = (int)(w - b * n);
+        const T* src = in + w * d;
+        float v[4];
+        float ss = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = lane + 32 * i;
+            v[i] = c < d ? (float)src[c] : 0.0f;
+            ss += v[i] * v[i];
+        }
+        ss = warp_sum(ss);
+        const float denom = sqrtf(ss / (float)d + 1e-6f);
+        __nv_bfloat16* dst = out + ((int64_t)pos[b] * n + f) * d;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = lane + 32 * i;
+            if (c < d) dst[c] = __float2bfloat16_rn(v[i] / denom);
+        }
+    }
+}
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+}  // namespace
+}  // namespace lat
+
+struct lattice_net {
+    lattice_net_config cfg;
+    int n_pad, k_pad;
+    int device;
+    // weights
+    std::vector<__nv_bfloat16*> YT, WL;  // padded [k_pad][n_pad], [128][n_pad]
+    std::vector<__nv_bfloat16*> mlp;     // [blocks * n_mlp] -> [out][in]
+    __nv_bfloat16* T1 = nullptr;         // [G * th][n*d]
+    float* T2 = nullptr;                 // [G][heads][th]
+    // workspace
+    int32_t *pos = nullptr, *order = nullptr, *seg = nullptr;
+    int4* tiles = nullptr;
+    int* n_tiles = nullptr;
+    __nv_bfloat16* X[2] = {nullptr, nullptr};
+    __nv_bfloat16* Fbuf = nullptr;
+    __nv_bfloat16* H[2] = {nullptr, nullptr};
+    // plans (tensor maps built once for max_batch)
+    std::vector<lat::fm::Plan> fm_plans;              // [blocks]
+    std::vector<lat::gemm::GemmPlan> mlp_plans;       // [blocks * n_mlp]
+    lat::gemm::GemmPlan tower_plan;
+    // timing
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;
+    std::vector<float> stage_ms;
+    std::vector<void*> allocs;
+};
+
+namespace {
+
+template <typename T>
+lattice_status dalloc(lattice_net* net, T** p, size_t count) {
+    void* q = nullptr;
+    LAT_CUDA(cudaMalloc(&q, count * sizeof(T) > 0 ? count * sizeof(T) : 16));
+    net->allocs.push_back(q);
+    *p = static_cast<T*>(q);
+    return LATTICE_OK;
+}
+
+lattice_status fill_padded(lattice_net* net, __nv_bfloat16* dst, int rows, int cols, int rows_pad,
+                           int cols_pad, uint64_t tag) {
+    LAT_CUDA(cudaMemset(dst, 0, sizeof(__nv_bfloat16) * (size_t)rows_pad * cols_pad));
+    __nv_bfloat16* tmp = nullptr;
+    LAT_CUDA(cudaMalloc(&tmp, sizeof(__nv_bfloat16) * (size_t)rows * cols));
+    lattice_status s = lattice_fill_weights(tmp, LATTICE_BF16, rows, cols, net->cfg.weight_seed, tag, nullptr);
+    if (s == LATTICE_OK) {
+        cudaError_t e = cudaMemcpy2D(dst, sizeof(__nv_bfloat16) * cols_pad, tmp, sizeof(__nv_bfloat16) * cols,
+                                     sizeof(__nv_bfloat16) * cols, rows, cudaMemcpyDeviceToDevice);
+        if (e != cudaSuccess) s = lat::check_cuda(e, "weight pad copy");
+    }
+    cudaFree(tmp);
+    return s;
+}
+
+lattice_status validate(const lattice_net_config* c) {
+    using lat::set_error;
+    if (!c) return set_error(LATTICE_USAGE, "lattice_net_create: null config");
+    if (c->n < 1 || c->n > 256) return set_error(LATTICE_USAGE, "network: n must be in [1, 256]");
+    if (c->d != 64 && c->d != 128) return set_error(LATTICE_USAGE, "network: d must be 64 or 128");
+    if (c->blocks < 1) return set_error(LATTICE_USAGE, "network: need at least one block");
+    if (c->nF < 1 || c->nL < 0 || c->nF + c->nL != c->n || c->nL > 128)
+        return set_error(LATTICE_USAGE, "network: need nF >= 1, nL <= 128 and nF + nL == n");
+    if (c->k < 1 || c->k > 64) return set_error(LATTICE_USAGE, "network: k must be in [1, 64]");
+    if (c->n_mlp < 1 || c->n_mlp > 5) return set_error(LATTICE_USAGE, "network: n_mlp must be in [1, 5]");
+    if (c->mlp[0] != c->n * c->k) return set_error(LATTICE_USAGE, "network: mlp[0] must equal n*k");
+    if (c->mlp[c->n_mlp] != c->nF * c->d) return set_error(LATTICE_USAGE, "network: mlp[n_mlp] must equal nF*d");
+    for (int i = 0; i <= c->n_mlp; ++i)
+        if (c->mlp[i] < 8 || c->mlp[i] % 8) return set_error(LATTICE_USAGE, "network: MLP widths must be multiples of 8");
+    for (int i = 1; i < c->n_mlp; ++i)
+        if (c->mlp[i] > 2048) return set_error(LATTICE_USAGE, "network: hidden widths above 2048 are not supported");
+    if (c->domains < 1 || c->domains > 32) return set_error(LATTICE_USAGE, "network: domains must be in [1, 32]");
+    if (c->heads < 1 || c->heads > 16) return set_error(LATTICE_USAGE, "network: heads must be in [1, 16]");
+    if (c->tower_hidden < 8 || c->tower_hidden > 2048 || c->tower_hidden % 8)
+        return set_error(LATTICE_USAGE, "network: tower_hidden must be a multiple of 8 in [8, 2048]");
+    if (c->max_batch < 1 || c->max_batch > (1ll << 30)) return set_error(LATTICE_USAGE, "network: bad max_batch");
+    return LATTICE_OK;
+}
+
+lattice_status build_plans(lattice_net* net) {
+    using namespace lat;
+    const lattice_net_config& c = net->cfg;
+    const int64_t Bm = c.max_batch;
+    const int nd = c.n * c.d;
+    net->fm_plans.resize(c.blocks);
+    net->mlp_plans.resize((size_t)c.blocks * c.n_mlp);
+    for (int blk = 0; blk < c.blocks; ++blk) {
+        __nv_bfloat16* Xc = net->X[blk & 1];
+        __nv_bfloat16* Xn = net->X[(blk + 1) & 1];
+        fm::Plan& fp = net->fm_plans[blk];
+        fp.p.B = Bm;
+        fp.p.n = c.n;
+        fp.p.d = c.d;
+        fp.p.k = c.k;
+        fp.p.nF = c.nF;
+        fp.p.nL = c.nL;
+        fp.p.n_pad = net->n_pad;
+        fp.p.k_pad = net->k_pad;
+        fp.p.tmem_cols = (64 + c.d + ((net->n_pad + 127) / 128) * net->k_pad) <= 256 ? 256 : 512;
+        fp.p.Fout = net->Fbuf;
+        fp.p.Xout = Xn;
+        lattice_status s = fm::check(fp.p);
+        if (s != LATTICE_OK) return s;
+        s = fm::make_maps(&fp, Xc, net->WL[blk], net->YT[blk]);
+        if (s != LATTICE_OK) return s;
+        for (int li = 0; li < c.n_mlp; ++li) {
+            const int in = c.mlp[li], out = c.mlp[li + 1];
+            const bool last = li + 1 == c.n_mlp;
+            const __nv_bfloat16* A = li == 0 ? net->Fbuf : net->H[(li - 1) & 1];
+            gemm::Params p = {};
+            p.M = (int)Bm;
+            p.N = out;
+            p.K = in;
+            p.out_bf16 = 1;
+            p.N_full = out;
+            p.cluster = 1;
+            if (!last) {
+                p.C = net->H[li & 1];
+                p.ldc = out;
+                p.epi = c.hard ? gemm::kSwishHard : gemm::kSwish;
+                p.cluster = (out + 255) / 256;
+            } else {
+                p.C = Xn;
+                p.ldc = nd;
+                p.epi = gemm::kResidNorm;
+                p.resid = Xc;
+                p.ldr = nd;
+                p.group = c.d;
+            }
+            s = gemm::plan(&net->mlp_plans[(size_t)blk * c.n_mlp + li], A, in, Bm, net->mlp[(size_t)blk * c.n_mlp + li],
+                           in, out, p, (int)((Bm + 127) / 128));
+            if (s != LATTICE_OK) return s;
+        }
+    }
+    gemm::Params p = {};
+    p.M = (int)Bm;
+    p.N = c.tower_hidden;
+    p.K = nd;
+    p.out_bf16 = 0;
+    p.epi = c.hard ? gemm::kTowerHard : gemm::kTower;
+    p.cluster = (c.tower_hidden + 255) / 256;
+    p.N_full = c.tower_hidden;
+    p.tiles = net->tiles;
+    p.n_tiles = net->n_tiles;
+    p.b_rows_per_group = c.tower_hidden;
+    p.W2 = net->T2;
+    p.heads = c.heads;
+    p.order = net->order;
+    return gemm::plan(&net->tower_plan, net->X[c.blocks & 1], nd, Bm, net->T1, nd,
+                      (int64_t)c.domains * c.tower_hidden, p, (int)((Bm + 127) / 128) + c.domains);
+}
+
+}  // namespace
+
+extern "C" {
+
+lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** out) {
+    using namespace lat;
+    LAT_REQUIRE(out != nullptr, "lattice_net_create: null out");
+    *out = nullptr;
+    lattice_status s = validate(cfg);
+    if (s != LATTICE_OK) return s;
+    lattice_net* net = new lattice_net();
+    net->cfg = *cfg;
+    cudaGetDevice(&net->device);
+    const lattice_net_config& c = net->cfg;
+    net->n_pad = round_up(c.n, 16);
+    net->k_pad = round_up(c.k, 16);
+    const int nd = c.n * c.d;
+    const int64_t Bm = c.max_batch;
+    auto fail = [&](lattice_status st) {
+        lattice_net_destroy(net);
+        return st;
+    };
+#define NET_TRY(x)                                 \
+    do {                                           \
+        lattice_status _s = (x);                   \
+        if (_s != LATTICE_OK) return fail(_s);     \
+    } while (0)
+    const uint64_t seed = c.weight_seed;
+    for (int blk = 0; blk < c.blocks; ++blk) {
+        __nv_bfloat16 *yt, *wl;
+        NET_TRY(dalloc(net, &yt, (size_t)net->k_pad * net->n_pad));
+        NET_TRY(dalloc(net, &wl, (size_t)128 * net->n_pad));
+        NET_TRY(fill_padded(net, yt, c.k, c.n, net->k_pad, net->n_pad, weight_tag(blk, 1, 0)));
+        NET_TRY(fill_padded(net, wl, c.nL > 0 ? c.nL : 1, c.n, 128, net->n_pad, weight_tag(blk, 2, 0)));
+        if (c.nL == 0) LAT_CUDA(cudaMemset(wl, 0, sizeof(__nv_bfloat16) * 128 * net->n_pad));
+        net->YT.push_back(yt);
+        net->WL.push_back(wl);
+        for (int li = 0; li < c.n_mlp; ++li) {
+            __nv_bfloat16* w;
+            NET_TRY(dalloc(net, &w, (size_t)c.mlp[li + 1] * c.mlp[li]));
+            NET_TRY(lattice_fill_weights(w, LATTICE_BF16, c.mlp[li + 1], c.mlp[li], seed, weight_tag(blk, 3, li), nullptr));
+            net->mlp.push_back(w);
+        }
+    }
+    NET_TRY(dalloc(net, &net->T1, (size_t)c.domains * c.tower_hidden * nd));
+    NET_TRY(dalloc(net, &net->T2, (size_t)c.domains * c.heads * c.tower_hidden));
+    for (int g = 0; g < c.domains; ++g) {
+        NET_TRY(lattice_fill_weights(net->T1 + (size_t)g * c.tower_hidden * nd, LATTICE_BF16, c.tower_hidden, nd,
+                                     seed, weight_tag(g, 4, 0), nullptr));
+        NET_TRY(lattice_fill_weights(net->T2 + (size_t)g * c.heads * c.tower_hidden, LATTICE_F32, c.heads,
+                                     c.tower_hidden, seed, weight_tag(g, 5, 0), nullptr));
+    }
+    int max_hidden = 8;
+    for (int i = 1; i < c.n_mlp; ++i) max_hidden = max_hidden > c.mlp[i] ? max_hidden : c.mlp[i];
+    NET_TRY(dalloc(net, &net->pos, (size_t)Bm));
+    NET_TRY(dalloc(net, &net->order, (size_t)Bm));
+    NET_TRY(dalloc(net, &net->seg, (size_t)c.domains + 1));
+    NET_TRY(dalloc(net, &net->tiles, (size_t)((Bm + 127) / 128 + c.domains)));
+    NET_TRY(dalloc(net, &net->n_tiles, 1));
+    NET_TRY(dalloc(net, &net->X[0], (size_t)Bm * nd));
+    NET_TRY(dalloc(net, &net->X[1], (size_t)Bm * nd));
+    NET_TRY(dalloc(net, &net->Fbuf, (size_t)Bm * c.n * c.k));
+    NET_TRY(dalloc(net, &net->H[0], (size_t)Bm * max_hidden));
+    NET_TRY(dalloc(net, &net->H[1], (size_t)Bm * max_hidden));
+    NET_TRY(build_plans(net));
+    LAT_CUDA(cudaDeviceSynchronize());
+#undef NET_TRY
+    *out = net;
+    return LATTICE_OK;
+}
+
+void lattice_net_destroy(lattice_net* net) {
+    if (!net) return;
+    for (void* p : net->allocs) cudaFree(p);
+    for (cudaEvent_t e : net->ev) cudaEventDestroy(e);
+    delete net;
+}
+
+const void* lattice_net_weight(lattice_net* net, int32_t block, int32_t kind, int32_t index) {
+    if (!net) return nullptr;
+    const lattice_net_config& c = net->cfg;
+    switch (kind) {
+        case 1: return block >= 0 && block < c.blocks ? net->YT[block] : nullptr;
+        case 2: return block >= 0 && block < c.blocks ? net->WL[block] : nullptr;
+        case 3:
+            return block >= 0 && block < c.blocks && index >= 0 && index < c.n_mlp
+                       ? net->mlp[(size_t)block * c.n_mlp + index]
+                       : nullptr;
+        case 4: return net->T1;
+        case 5: return net->T2;
+        default: return nullptr;
+    }
+}
+
+lattice_status lattice_net_set_timing(lattice_net* net, int32_t enable) {
+    LAT_REQUIRE(net != nullptr, "lattice_net_set_timing: null net");
+    net->timing = enable != 0;
+    if (net->timing && net->ev.empty()) {
+        const int stages = 2 + net->cfg.blocks * 2 + 1;
+        net->ev.resize(stages + 1);
+        for (auto& e : net->ev) LAT_CUDA(cudaEventCreate(&e));
+    }
+    return LATTICE_OK;
+}
+
+lattice_status lattice_net_stage_times(lattice_net* net, float* ms, int32_t max_stages, int32_t* n_stages) {
+    LAT_REQUIRE(net != nullptr && n_stages != nullptr, "lattice_net_stage_times: null argument");
+    *n_stages = 0;
+    if (!net->timing || net->ev.empty()) return LATTICE_OK;
+    LAT_CUDA(cudaEventSynchronize(net->ev.back()));
+    const int n = (int)net->ev.size() - 1;
+    for (int i = 0; i < n && i < max_stages; ++i) {
+        float t = 0.0f;
+        LAT_CUDA(cudaEventElapsedTime(&t, net->ev[i], net->ev[i + 1]));
+        ms[i] = t;
+        *n_stages = i + 1;
+    }
+    return LATTICE_OK;
+}
+
+// Stage boundaries recorded when timing is on: [bucket, bag, (fm_lcb, mlp) x blocks, tower]
+lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch, float* logits,
+                                   lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(net != nullptr && batch != nullptr && logits != nullptr, "lattice_net_forward: null argument");
+    const lattice_net_config& c = net->cfg;
+    const int64_t B = batch->batch;
+    LAT_REQUIRE(B >= 0 && B <= c.max_batch, "lattice_net_forward: batch exceeds max_batch");
+    if (B == 0) return LATTICE_OK;
+    LAT_REQUIRE(batch->domain != nullptr, "lattice_net_forward: null domain");
+    const int nd = c.n * c.d;
+    int ei = 0;
+    auto mark = [&]() -> lattice_status {
+        if (net->timing) LAT_CUDA(cudaEventRecord(net->ev[ei++], stream));
+        return LATTICE_OK;
+    };
+#define FWD_TRY(x)                                \
+    do {                                          \
+        lattice_status _s = (x);                  \
+        if (_s != LATTICE_OK) return _s;          \
+    } while (0)
+    FWD_TRY(mark());
+    FWD_TRY(lattice_domain_bucket(B, c.domains, batch->domain, net->pos, net->order, net->seg, stream));
+    tiles_kernel<<<1, 256, 0, stream>>>(net->seg, c.domains, net->tiles, net->n_tiles);
+    LAT_CUDA(cudaGetLastError());
+    FWD_TRY(mark());
+    if (batch->tables) {
+        lattice_bag_args a = {};
+        a.features = c.n;
+        a.batch = B;
+        a.dim = c.d;
+        a.table_dtype = batch->table_dtype;
+        a.tables = batch->tables;
+        a.rows = batch->rows;
+        a.offsets = batch->offsets;
+        a.ids = batch->ids;
+        a.out_dtype = LATTICE_BF16;
+        a.out = net->X[0];
+        a.out_row_stride = nd;
+        a.out_feature_offset = 0;
+        a.sample_pos = net->pos;
+        a.normalize = 1;
+        a.check = 0;
+        FWD_TRY(lattice_embedding_bag(&a, stream));
+    } else {
+        LAT_REQUIRE(batch->pooled != nullptr, "lattice_net_forward: need tables or pooled input");
+        const int64_t warps = B * c.n;
+        const unsigned grid = (unsigned)((warps * 32 + 255) / 256 < 148 * 64 ? (warps * 32 + 255) / 256 : 148 * 64);
+        if (batch->table_dtype == LATTICE_F32)
+            pooled_norm_kernel<float><<<grid, 256, 0, stream>>>(B, c.n, c.d, static_cast<const float*>(batch->pooled),
+                                                               net->pos, net->X[0]);
+        else
+            pooled_norm_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>(
+                B, c.n, c.d, static_cast<const __nv_bfloat16*>(batch->pooled), net->pos, net->X[0]);
+        LAT_CUDA(cudaGetLastError());
+    }
+    FWD_TRY(mark());
+    for (int blk = 0; blk < c.blocks; ++blk) {
+        fm::Plan fp = net->fm_plans[blk];
+        fp.p.B = B;
+        FWD_TRY(fm::launch(fp, stream));
+        FWD_TRY(mark());
+        for (int li = 0; li < c.n_mlp; ++li) {
+            gemm::GemmPlan g = net->mlp_plans[(size_t)blk * c.n_mlp + li];
+            g.p.M = (int)B;
+            g.grid_y = (int)((B + 127) / 128);
+            FWD_TRY(gemm::launch(g, stream));
+        }
+        FWD_TRY(mark());
+    }
+    gemm::GemmPlan t = net->tower_plan;
+    t.p.M = (int)B;
+    t.p.logits = logits;
+    t.grid_y = (int)((B + 127) / 128) + c.domains;
+    FWD_TRY(gemm::launch(t, stream));
+    FWD_TRY(mark());
+#undef FWD_TRY
+    return LATTICE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+"""Lattice Network forward (K6 -> K1 -> [K2 -> K3 x n_mlp] x blocks -> K4) on the GPU vs the
+fp64 CPU oracle (oracle/lattice_oracle.c lo_net_forward) on identical synthetic inputs and the
+network's own bf16 weights. The oracle rounds to bf16 at every point the GPU stores bf16.
+
+Tolerance (bf16 configs, stated per SURVEY.md 8d): |gpu - oracle| <= 2e-2 + 2e-2 * |oracle| on
+every logit. Order/permutation properties are checked bit-exactly."""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+SEED_T, SEED_D, SEED_W = 0x1A77, 0x1A78, 0x1A79
+
+TINY = dict(n=8, d=64, blocks=2, nF=4, nL=4, k=4, mlp=[32, 64, 256], domains=2, heads=2,
+            tower_hidden=64)
+MID = dict(n=256, d=128, blocks=4, nF=128, nL=128, k=32, mlp=[8192, 2048, 2048, 16384],
+           domains=4, heads=6, tower_hidden=512)
+SMALL = dict(n=64, d=128, blocks=2, nF=32, nL=32, k=16, mlp=[1024, 512, 4096], domains=3,
+             heads=4, tower_hidden=256)
+
+
+def build(cfg, B, rows, max_len=40, hard=False):
+    import torch
+    import paper_2512_09200_b200 as L
+    net = L.Network(**cfg, hard=hard, max_batch=B, weight_seed=SEED_W)
+    n, d = cfg["n"], cfg["d"]
+    tab = torch.empty((n, rows, d), dtype=torch.bfloat16, device="cuda")
+    L.fill_tables(tab, SEED_T)
+    ptrs = torch.tensor([t.data_ptr() for t in tab.unbind(0)], dtype=torch.int64, device="cuda")
+    rws = torch.full((n,), rows, dtype=torch.int64, device="cuda")
+    offsets, ids = L.synth_bags(n, B, max_len, rows, SEED_D)
+    dom = L.synth_domains(B, cfg["domains"], SEED_D)
+    return net, tab, ptrs, rws, offsets, ids, dom
+
+
+def oracle_logits(net, cfg, rows, offsets, ids, dom, samples, hard=False):
+    n, d = cfg["n"], cfg["d"]
+    B = dom.shape[0]
+    o_cpu = offsets.cpu().numpy()
+    i_cpu = ids.cpu().numpy()[: o_cpu[-1]]
+    pooled = np.concatenate([oracle.embedding_bag_synth(SEED_T, n, rows, d, B, o_cpu, i_cpu, s, s + 1)[0]
+                             for s in samples])
+    w = net.weights()
+    lib = oracle.load_oracle()
+    c = oracle.LoNetCfg()
+    c.n, c.d, c.blocks, c.nF, c.nL, c.k = n, d, cfg["blocks"], cfg["nF"], cfg["nL"], cfg["k"]
+    c.n_mlp = len(cfg["mlp"]) - 1
+    for i, v in enumerate(cfg["mlp"]):
+        c.mlp[i] = v
+    c.G, c.heads, c.tower_hidden, c.hard, c.bf16 = cfg["domains"], cfg["heads"], cfg["tower_hidden"], int(hard), 1
+    keep = [np.ascontiguousarray(a, dtype=np.float32) for a in w["YT"] + w["WL"] + w["mlp"]]
+    nb = cfg["blocks"]
+    P = oracle.ctypes.c_void_p
+    yt = (P * nb)(*[a.ctypes.data for a in keep[:nb]])
+    wl = (P * nb)(*[a.ctypes.data for a in keep[nb:2 * nb]])
+    ml = (P * len(w["mlp"]))(*[a.ctypes.data for a in keep[2 * nb:]])
+    T1 = np.ascontiguousarray(w["T1"], dtype=np.float32)
+    T2 = np.ascontiguousarray(w["T2"], dtype=np.float32)
+    ws = oracle.LoNetWeights(oracle.ctypes.cast(yt, P), oracle.ctypes.cast(wl, P),
+                             oracle.ctypes.cast(ml, P), P(T1.ctypes.data), P(T2.ctypes.data))
+    d_cpu = np.ascontiguousarray(dom.cpu().numpy()[samples], dtype=np.int32)
+    out = np.zeros((len(samples), cfg["heads"]), np.float32)
+    lib.lo_net_forward(oracle.ctypes.byref(c), oracle.ctypes.byref(ws), len(samples),
+                       oracle.ptr(pooled), oracle.ptr(d_cpu), oracle.ptr(out), 0)
+    return out, w
+
+
+def check_weights_against_generator(w, cfg):
+    lib = oracle.load_oracle()
+    rng = np.random.default_rng(0)
+    for blk in range(cfg["blocks"]):
+        for _ in range(20):
+            o, i = int(rng.integers(0, cfg["k"])), int(rng.integers(0, cfg["n"]))
+            assert w["YT"][blk][o, i] == lib.lo_weight_value(SEED_W, lib.lo_weight_tag(blk, 1, 0), o, i, cfg["n"])
+            li = int(rng.integers(0, len(cfg["mlp"]) - 1))
+            W = w["mlp"][blk * (len(cfg["mlp"]) - 1) + li]
+            o, i = int(rng.integers(0, W.shape[0])), int(rng.integers(0, W.shape[1]))
+            assert W[o, i] == lib.lo_weight_value(SEED_W, lib.lo_weight_tag(blk, 3, li), o, i, W.shape[1])
+    g = cfg["domains"] - 1
+    assert w["T2"][g, 1, 3] == lib.lo_weight_value(SEED_W, lib.lo_weight_tag(g, 5, 0), 1, 3, cfg["tower_hidden"])
+
+
+def assert_logits_close(got, want):
+    err = np.abs(got - want)
+    bound = 2e-2 + 2e-2 * np.abs(want)
+    assert (err <= bound).all(), f"max err {err.max():.4g} (worst ratio {(err / bound).max():.3g}); rms {np.sqrt((want ** 2).mean()):.3g}"
+
+
+@pytest.mark.parametrize("name,cfg,B,rows,hard", [("tiny", TINY, 512, 10000, False),
+                                                  ("small", SMALL, 1000, 5000, False),
+                                                  ("small_hard", SMALL, 700, 5000, True)])
+def test_forward_matches_oracle(name, cfg, B, rows, hard):
+    import torch
+    net, tab, ptrs, rws, offsets, ids, dom = build(cfg, B, rows, hard=hard)
+    logits = net.forward(dom, offsets, ids, ptrs, rws, torch.bfloat16)
+    torch.cuda.synchronize()
+    samples = list(range(0, B, max(1, B // 48)))[:48] + [B - 1]
+    want, w = oracle_logits(net, cfg, rows, offsets, ids, dom, samples, hard)
+    check_weights_against_generator(w, cfg)
+    got = logits.cpu().numpy()[samples]
+    assert np.isfinite(got).all()
+    assert_logits_close(got, want)
+
+
+def test_mid_config_matches_oracle():
+    import torch
+    B, rows = 2048, 20000
+    net, tab, ptrs, rws, offsets, ids, dom = build(MID, B, rows)
+    logits = net.forward(dom, offsets, ids, ptrs, rws, torch.bfloat16)
+    torch.cuda.synchronize()
+    samples = [0, 1, 2, 777, 1500, 2047]
+    want, _ = oracle_logits(net, MID, rows, offsets, ids, dom, samples)
+    assert_logits_close(logits.cpu().numpy()[samples], want)
+
+
+def test_permutation_invariance_and_pooled_path():
+    import torch
+    import paper_2512_09200_b200 as L
+    cfg, B, rows = SMALL, 777, 3000
+    net, tab, ptrs, rws, offsets, ids, dom = build(cfg, B, rows)
+    base = net.forward(dom, offsets, ids, ptrs, rws, torch.bfloat16).clone()
+    # same samples, reversed order, through the pooled-input entry
+    pooled = L.embedding_bag(list(tab.unbind(0)), offsets, ids, B, out_dtype=torch.float32)
+    rev = torch.arange(B - 1, -1, -1, device="cuda")
+    out = net.forward(dom[rev].contiguous(), pooled=pooled[rev].contiguous())
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(out.cpu().numpy()[::-1], base.cpu().numpy(), rtol=2e-2, atol=2e-2)
+    # reordering the batch through the sparse path is bit-exact per sample: rows are independent
+    lens = (offsets[1:] - offsets[:-1]).view(cfg["n"], B)
+    perm = torch.randperm(B, device="cuda")
+    lens_p = lens[:, perm]
+    off_p = torch.zeros(cfg["n"] * B + 1, dtype=torch.int64, device="cuda")
+    off_p[1:] = torch.cumsum(lens_p.reshape(-1), 0)
+    ids_p = torch.cat([ids[offsets[f * B + b]: offsets[f * B + b + 1]]
+                       for f in range(cfg["n"]) for b in perm.tolist()]).to(torch.int32)
+    out_p = net.forward(dom[perm].contiguous(), off_p, ids_p, ptrs, rws, torch.bfloat16)
+    assert torch.equal(out_p, base[perm])
+
+
+def test_domain_routing_uses_untied_towers():
+    import torch
+    cfg, B, rows = SMALL, 256, 3000
+    net, tab, ptrs, rws, offsets, ids, dom = build(cfg, B, rows)
+    a = net.forward(torch.zeros_like(dom), offsets, ids, ptrs, rws, torch.bfloat16).clone()
+    b = net.forward(torch.full_like(dom, 2), offsets, ids, ptrs, rws, torch.bfloat16).clone()
+    mixed = net.forward(dom, offsets, ids, ptrs, rws, torch.bfloat16)
+    assert not torch.equal(a, b)
+    d = dom.cpu().numpy()
+    assert torch.equal(mixed[torch.from_numpy(d == 0).cuda()], a[torch.from_numpy(d == 0).cuda()])
+    assert torch.equal(mixed[torch.from_numpy(d == 2).cuda()], b[torch.from_numpy(d == 2).cuda()])
+
+
+def test_config_contract():
+    import paper_2512_09200_b200 as L
+    bad = dict(SMALL)
+    bad["nL"] = 31  # nF + nL != n
+    with pytest.raises(L.UsageError):
+        L.Network(**bad, max_batch=16)
+    bad = dict(SMALL)
+    bad["mlp"] = [1024, 4096, 4096]  # last width != nF*d
+    with pytest.raises(L.UsageError):
+        L.Network(**bad, max_batch=16)
