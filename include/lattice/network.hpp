@@ -1,0 +1,104 @@
+#pragma once
+
+// lattice::Network -- the consolidated MDMO model step that the reference
+// only describes in prose. Same idiom as proj/include/lattice: value types in, value types
+// out, UsageError / DataError on contract / data violations. The work runs on the current
+// CUDA device through lattice_net_* (include/lattice_b200.h); inputs may be host vectors
+// (copied in) or device pointers (forward_device, stream-ordered, no synchronisation).
+
+#include <array>
+#include <cstdint>
+#include <vector>
+
+#include "core.hpp"
+
+namespace lattice {
+
+struct NetworkConfig {
+    int n = 8, d = 64, blocks = 2, nF = 4, nL = 4, k = 4;
+    std::vector<int> mlp{32, 64, 256};  // n*k ... nF*d
+    int domains = 2, heads = 2, tower_hidden = 64;
+    bool hard_gate = false;             // swish_rn_hard activations
+    std::int64_t max_batch = 512;
+    Seed weight_seed{0x1A79};
+};
+
+// Jagged sparse batch, feature-major CSR: bag (f, b) = ids[offsets[f*B+b] .. offsets[f*B+b+1]).
+struct SparseBatch {
+    std::int64_t batch = 0;
+    std::vector<std::int64_t> offsets;  // [n*B + 1]
+    std::vector<std::int32_t> ids;
+    std::vector<std::int32_t> domain;   // [B]
+};
+
+// Device-resident embedding tables: one pointer per feature, bf16 or fp32 [rows][d].
+struct TableSet {
+    std::vector<const void*> tables;
+    std::vector<std::int64_t> rows;
+    lattice_dtype dtype = LATTICE_BF16;
+};
+
+class Network {
+public:
+    explicit Network(const NetworkConfig& c) : cfg_(c) {
+        lattice_net_config nc{};
+        nc.n = c.n;
+        nc.d = c.d;
+        nc.blocks = c.blocks;
+        nc.nF = c.nF;
+        nc.nL = c.nL;
+        nc.k = c.k;
+        if (c.mlp.size() < 2 || c.mlp.size() > 6) throw UsageError("Network: mlp needs 2..6 widths");
+        nc.n_mlp = static_cast<std::int32_t>(c.mlp.size()) - 1;
+        for (std::size_t i = 0; i < c.mlp.size(); ++i) nc.mlp[i] = c.mlp[i];
+        nc.domains = c.domains;
+        nc.heads = c.heads;
+        nc.tower_hidden = c.tower_hidden;
+        nc.hard = c.hard_gate ? 1 : 0;
+        nc.max_batch = c.max_batch;
+        nc.weight_seed = c.weight_seed.value;
+        device::throw_status(lattice_net_create(&nc, &net_));
+    }
+    Network(const Network&) = delete;
+    Network& operator=(const Network&) = delete;
+    ~Network() { lattice_net_destroy(net_); }
+
+    const NetworkConfig& config() const { return cfg_; }
+
+    // Logits [B][heads] in batch order, heads = objectives x attribution windows.
+    std::vector<float> forward(const SparseBatch& b, const TableSet& t) const {
+        if (b.domain.size() != static_cast<std::size_t>(b.batch) ||
+            b.offsets.size() != static_cast<std::size_t>(cfg_.n * b.batch + 1))
+            throw UsageError("Network::forward: batch arrays do not match batch size");
+        if (t.tables.size() != static_cast<std::size_t>(cfg_.n) || t.rows.size() != t.tables.size())
+            throw UsageError("Network::forward: need one table per sparse feature");
+        device::Buffer<std::int64_t> d_off(b.offsets), d_rows(t.rows);
+        device::Buffer<std::int32_t> d_ids(b.ids.empty() ? std::vector<std::int32_t>{0} : b.ids);
+        device::Buffer<std::int32_t> d_dom(b.domain);
+        device::Buffer<const void*> d_tab(t.tables);
+        device::Buffer<float> d_logits(static_cast<std::size_t>(b.batch) * cfg_.heads);
+        lattice_batch lb{};
+        lb.batch = b.batch;
+        lb.domain = d_dom.get();
+        lb.table_dtype = t.dtype;
+        lb.tables = d_tab.get();
+        lb.rows = d_rows.get();
+        lb.offsets = d_off.get();
+        lb.ids = d_ids.get();
+        device::throw_status(lattice_net_forward(net_, &lb, d_logits.get(), nullptr));
+        return d_logits.download();
+    }
+
+    // Device-pointer entry: everything already on the GPU, ordered on `stream`.
+    void forward_device(const lattice_batch& b, float* logits, cudaStream_t stream) const {
+        device::throw_status(lattice_net_forward(net_, &b, logits, stream));
+    }
+
+    lattice_net* handle() const { return net_; }
+
+private:
+    NetworkConfig cfg_;
+    lattice_net* net_ = nullptr;
+};
+
+}  // namespace lattice

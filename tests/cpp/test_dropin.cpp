@@ -1,0 +1,166 @@
+// C++ drop-in test: the reference's own test expectations (proj/tests/test_core.cpp:18-43,
+// 109-120; test_numerics.cpp:93-149; SPEC.md:236-254 Zipper examples) exercised through the
+// include/lattice headers, i.e. through the B200 kernels. Built by __graft_entry__.build(),
+// run by tests/test_dropin_gpu.py. Exit code = number of failed checks.
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "lattice/core.hpp"
+#include "lattice/datasets.hpp"
+#include "lattice/network.hpp"
+#include "lattice/numerics.hpp"
+
+using namespace lattice;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                         \
+    do {                                                                    \
+        if (cond) {                                                         \
+            ++g_pass;                                                       \
+        } else {                                                            \
+            ++g_fail;                                                       \
+            std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+        }                                                                   \
+    } while (0)
+#define CHECK_THROWS_AS(expr, T)        \
+    do {                                \
+        bool ok = false;                \
+        try {                           \
+            (void)(expr);               \
+        } catch (const T&) {            \
+            ok = true;                  \
+        } catch (...) {                 \
+        }                               \
+        CHECK(ok && #T);                \
+    } while (0)
+
+static void core_goldens() {
+    struct G {
+        const char* s;
+        std::uint64_t seed, h;
+    } goldens[] = {
+        {"", 0x0, 0xef46db3751d8e999ULL},
+        {"", 0x1, 0xd5afba1336a3be4bULL},
+        {"abc", 0x0, 0x44bc2cf5ad770999ULL},
+        {"abc", 0x1, 0xbea9ca8199328908ULL},
+        {"a", 0x0, 0xd24ec4f1a98c6e5bULL},
+        {"lattice", 0x2a, 0x1643a65295b18ef1ULL},
+        {"0123456789abcdef", 0x7, 0x8fbf8acb214d5da5ULL},
+        {"0123456789abcdef0123456789abcde", 0x7, 0x9bfbacf6829bf320ULL},
+        {"The quick brown fox jumps over the lazy dog", 0x0, 0x0b242d361fda71bcULL},
+        {"The quick brown fox jumps over the lazy dog", 0x9e3779b185ebca87ULL, 0xb8a8089add7e03d9ULL},
+    };
+    for (const auto& g : goldens) CHECK(stable_hash(std::string_view(g.s), Seed{g.seed}) == g.h);
+    CHECK(stable_hash("abc", Seed{0}) != stable_hash("abc", Seed{1}));
+    ByteWriter w;
+    w.length_prefixed("ab");
+    w.u64_be(0x0102030405060708ULL);
+    const auto& buf = w.view();
+    CHECK(buf.size() == 14 && buf[3] == 2 && buf[4] == 'a' && buf[6] == 0x01 && buf[13] == 0x08);
+}
+
+static void numerics_examples() {
+    const auto c = rms_norm(std::vector<double>{2, 2});
+    CHECK(std::abs(c[0] - 1.0) < 1e-6 && std::abs(c[1] - 1.0) < 1e-6);
+    for (double v : rms_norm(std::vector<double>{0, 0, 0})) CHECK(v == 0.0);
+    const auto p = rms_norm(std::vector<double>{3, 4});
+    CHECK(std::abs(p[0] - 3.0 / std::sqrt(12.5)) < 1e-3);
+    CHECK_THROWS_AS(rms_norm(std::vector<double>{}), UsageError);
+    CHECK_THROWS_AS(rms_norm(std::vector<double>{std::nan("")}), DataError);
+    CHECK_THROWS_AS(rms_norm(std::vector<double>{1.0}, 0.0), UsageError);
+    const double s1 = 1.0 / (1.0 + std::exp(-1.0));
+    const auto s = swish_rn(std::vector<double>{2, 2});
+    CHECK(std::abs(s[0] - s1) < 1e-4);
+    const auto k = swish_rn(std::vector<double>{3, 4});
+    CHECK(std::abs(k[0] - 0.59418883661177035) < 1e-6 && std::abs(k[1] - 0.85542017401638759) < 1e-6);
+    const auto h = swish_rn_hard(std::vector<double>{3, 4});
+    CHECK(std::abs(h[0] - 0.54426404214136748) < 1e-6 && std::abs(h[1] - 0.77901871858849048) < 1e-6);
+    std::vector<double> huge(8, 1e6);
+    huge[0] = -1e6;
+    for (double v : swish_rn(huge)) CHECK(std::isfinite(v) && std::abs(v) <= std::sqrt(8.0));
+}
+
+static void zipper_examples() {
+    const auto two = ZipperConfig::create({{"90min", 5400000}, {"1d", 86400000}}, {0.5, 0.5}, Seed{7});
+    CHECK(assign_window("u1", "a1", 0, two) == 1);                              // SURVEY 8c golden
+    CHECK(assign_window("user_000042", "ad_9", 1700000000000, two) == 0);
+    const auto four = ZipperConfig::create({{"a", 1}, {"b", 2}, {"c", 3}, {"d", 4}}, {0.4, 0.3, 0.2, 0.1}, Seed{7});
+    CHECK(assign_window("u1", "a1", 0, four) == 2);
+    CHECK(assign_window("alice", "campaign-7/creative-13", 86400000, four) == 1);
+    const auto degenerate = ZipperConfig::create({{"a", 1}, {"b", 2}}, {1.0, 0.0}, Seed{3});
+    for (int i = 0; i < 50; ++i) CHECK(assign_window("u" + std::to_string(i), "x", i, degenerate) == 0);
+    CHECK_THROWS_AS(ZipperConfig::create({}, {}, Seed{1}), UsageError);
+    CHECK_THROWS_AS(ZipperConfig::create({{"a", 2}, {"b", 2}}, {0.5, 0.5}, Seed{1}), UsageError);
+    CHECK_THROWS_AS(ZipperConfig::create({{"a", 1}, {"a", 2}}, {0.5, 0.5}, Seed{1}), UsageError);
+    CHECK_THROWS_AS(ZipperConfig::create({{"a", 1}, {"b", 2}}, {0.5, 0.6}, Seed{1}), UsageError);
+
+    // windows {90min, 1d}, impression at t=0
+    std::vector<DomainRecord> recs(3);
+    for (auto& r : recs) r.domain = "d", r.user_id = "u", r.ad_id = "a";
+    recs[0].conversions["cvr"] = 7200000;  // 2h
+    recs[1].conversions["cvr"] = 5400000;  // exactly 90min: inclusive
+    recs[0].values["f1"] = 1.0;
+    recs[2].values["f2"] = 2.0;
+    const auto z = zip_dataset(recs, {"cvr"}, two);
+    CHECK(z.records.size() == 3);
+    CHECK(z.records[0].label(0, 0, 2) == 0 && z.records[0].label(0, 1, 2) == 1);
+    CHECK(z.records[1].label(0, 0, 2) == 1 && z.records[1].label(0, 1, 2) == 1);
+    CHECK(z.records[2].label(0, 0, 2) == 0 && z.records[2].label(0, 1, 2) == 0);
+    CHECK(z.schema.features.size() == 2 && z.records[0].base.values.at("f2") == 0.0);
+    recs[1].conversions["cvr"] = -1;
+    bool threw = false;
+    try {
+        zip_dataset(recs, {"cvr"}, two);
+    } catch (const DataError& e) {
+        threw = std::string(e.what()) == "zip_dataset: record #1 task 'cvr' converts before its impression";
+    }
+    CHECK(threw);
+    CHECK_THROWS_AS(zip_dataset(recs, {"cvr", "cvr"}, two), UsageError);
+}
+
+static void network_smoke() {
+    NetworkConfig c;  // tiny config (BASELINE configs[0] shapes)
+    c.max_batch = 64;
+    Network net(c);
+    const int rows = 1000;
+    std::vector<device::Buffer<float>> owned;
+    TableSet ts;
+    ts.dtype = LATTICE_F32;
+    for (int f = 0; f < c.n; ++f) {
+        std::vector<float> t(static_cast<std::size_t>(rows) * c.d);
+        for (std::size_t i = 0; i < t.size(); ++i) t[i] = static_cast<float>((i * 2654435761u + f) % 97) / 97.0f - 0.5f;
+        owned.emplace_back(t);
+        ts.tables.push_back(owned.back().get());
+        ts.rows.push_back(rows);
+    }
+    SparseBatch b;
+    b.batch = 16;
+    b.offsets.push_back(0);
+    for (int f = 0; f < c.n; ++f)
+        for (int s = 0; s < b.batch; ++s) {
+            for (int j = 0; j < (s + f) % 5; ++j) b.ids.push_back((s * 31 + f * 7 + j * 13) % rows);
+            b.offsets.push_back(static_cast<std::int64_t>(b.ids.size()));
+        }
+    for (int s = 0; s < b.batch; ++s) b.domain.push_back(s % c.domains);
+    const auto logits = net.forward(b, ts);
+    CHECK(logits.size() == static_cast<std::size_t>(b.batch * c.heads));
+    bool finite = true;
+    for (float v : logits) finite = finite && std::isfinite(v);
+    CHECK(finite);
+    const auto again = net.forward(b, ts);
+    CHECK(again == logits);  // deterministic
+    NetworkConfig bad = c;
+    bad.nL = 3;
+    CHECK_THROWS_AS(Network{bad}, UsageError);
+}
+
+int main() {
+    core_goldens();
+    numerics_examples();
+    zipper_examples();
+    network_smoke();
+    std::printf("drop-in: %d passed, %d failed\n", g_pass, g_fail);
+    return g_fail;
+}
