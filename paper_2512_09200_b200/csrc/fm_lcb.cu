@@ -11,10 +11,14 @@
 // the 128-byte swizzle, and that one image serves three tcgen05 MMAs through different
 // descriptors -- MN-major A (X^T for P), MN-major B (X for L) and K-major A (X for F).
 // W_L and Y stay resident in shared memory for the whole persistent CTA. P goes TMEM ->
-// registers -> bf16 -> swizzled shared memory to become F's B operand. Accumulators live in
-// TMEM (P | L | F columns). Warp roles: 0 TMA producer, 1 MMA issuer, 2-5 epilogue
-// (thread = TMEM lane = accumulator row). X stages are double-buffered so the next
-// sample's load overlaps this sample's MMAs and epilogue.
+// registers -> bf16 -> swizzled shared memory to become F's B operand.
+//
+// Warp roles: 0 TMA producer, 1 MMA issuer, 2-9 epilogue. Each TMEM lane quarter is
+// drained by two epilogue warps that split the columns (P, L) or the M tiles (F), so every
+// SM sub-partition runs two epilogue warps. TMEM holds two accumulator regions
+// {P | L | F}: the MMAs of sample s+1 run while sample s's epilogue drains the other region,
+// and X stages are double-buffered so loads run two samples ahead. The epilogue is the
+// critical path; values stay in registers between the sum-of-squares and the normalise pass.
 #include <cudaTypedefs.h>
 
 #include <string>
@@ -27,11 +31,17 @@
 namespace lat {
 namespace fm {
 
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kThreads = 64 + kEpiThreads;
 
 __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t col_elem) {
     // byte offset of bf16 element (row, col) inside a [rows][64] SW128 panel
     return row * 128u + ((((col_elem >> 3) ^ (row & 7u)) << 4) | ((col_elem & 7u) << 1));
+}
+
+__device__ __forceinline__ int region_cols(const Params& p) {
+    return 64 + p.d + ((p.n_pad + 127) / 128) * p.k_pad;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -53,40 +63,43 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sWL = smem;
     uint8_t* sYT = sWL + wlpanel * panels_n;
     uint8_t* sP = sYT + ytpanel * panels_n;
-    uint8_t* sX = sP + ((ppanel * panels_d + 1023) & ~1023u);
+    uint8_t* sX = sP + ((ppanel * 2 + 1023) & ~1023u);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sX + 2 * xstage);
-    uint64_t* x_full = bars;        // [2]
-    uint64_t* x_empty = bars + 2;   // [2]
-    uint64_t* w_full = bars + 4;
-    uint64_t* pl_full = bars + 5;
-    uint64_t* pbuf_full = bars + 6;
-    uint64_t* f_full = bars + 7;
-    uint64_t* tmem_empty = bars + 8;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
-    float* red = reinterpret_cast<float*>(bars + 10);  // [4] warp partials
+    uint64_t* x_full = bars;        // [2] X stage landed
+    uint64_t* x_empty = bars + 2;   // [2] X stage consumed (MMAs + residual reads)
+    uint64_t* pl_full = bars + 4;   // [2] P, L accumulators ready (per TMEM region)
+    uint64_t* f_full = bars + 6;    // [2] F accumulator ready
+    uint64_t* tmem_empty = bars + 8;// [2] region drained
+    uint64_t* w_full = bars + 10;
+    uint64_t* pbuf_full = bars + 11;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+    float* red_l = reinterpret_cast<float*>(bars + 16);       // [2][128] row partials
+    float* red_f = red_l + 256;                               // [8] warp partials
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rcols = region_cols(p);
+    const int nreg = rcols <= 256 ? 2 : 1;
+    const uint32_t tcols = nreg == 2 ? 512u : (rcols <= 256 ? 256u : 512u);
     if (warp == 0 && lane == 0) {
         tc::tma_prefetch(&tmX);
         tc::tma_prefetch(&tmWL);
         tc::tma_prefetch(&tmYT);
         for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&x_full[i], 1);
-            tc::mbar_init(&x_empty[i], 128);
+            tc::mbar_init(&x_empty[i], kEpiThreads);
+            tc::mbar_init(&pl_full[i], 1);
+            tc::mbar_init(&f_full[i], 1);
+            tc::mbar_init(&tmem_empty[i], kEpiThreads);
         }
         tc::mbar_init(w_full, 1);
-        tc::mbar_init(pl_full, 1);
-        tc::mbar_init(pbuf_full, 128);
-        tc::mbar_init(f_full, 1);
-        tc::mbar_init(tmem_empty, 128);
+        tc::mbar_init(pbuf_full, kEpiThreads);
         tc::fence_mbar_init();
     }
-    if (warp == 1) tc::tmem_alloc(tmem_slot, p.tmem_cols);
+    if (warp == 1) tc::tmem_alloc(tmem_slot, tcols);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t t_P = tmem + 0, t_L = tmem + 64, t_F = tmem + 64 + (uint32_t)d;
     const int m_tiles = (npad + 127) / 128;
 
     if (warp == 0) {
@@ -111,17 +124,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t id_L = tc::idesc_bf16(128, d, 0, 1);     // B = X (MN-major)
             const uint32_t id_F = tc::idesc_bf16(128, kpad, 0, 0);
             tc::mbar_wait(w_full, 0);
+            const uint32_t wl = tc::smem_u32(sWL), yt = tc::smem_u32(sYT), pb = tc::smem_u32(sP);
             int it = 0;
             for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
                 const int st = it & 1;
+                const int rg = nreg == 2 ? (it & 1) : 0;
+                const uint32_t rph = nreg == 2 ? ((it >> 1) & 1) : (it & 1);
+                const uint32_t t_P = tmem + rg * 256, t_L = t_P + 64, t_F = t_L + d;
                 tc::mbar_wait(&x_full[st], (it >> 1) & 1);
-                tc::mbar_wait(tmem_empty, (it & 1) ^ 1);
+                tc::mbar_wait(&tmem_empty[rg], rph ^ 1);
                 tc::fence_after();
                 const uint32_t xs = tc::smem_u32(sX + st * xstage);
-                const uint32_t wl = tc::smem_u32(sWL), yt = tc::smem_u32(sYT);
                 for (int kk = 0; kk < npad / 16; ++kk) {
                     const int k16 = kk * 16;
-                    const uint32_t kb_off = (uint32_t)(k16 / 64) , kin = (uint32_t)(k16 % 64) * 2;
+                    const uint32_t kb_off = (uint32_t)(k16 / 64), kin = (uint32_t)(k16 % 64) * 2;
                     // P += X^T[:, k16:k16+16] . Y[k16:k16+16, :]
                     const uint64_t a_xt = tc::sdesc(xs + k16 * 128, xpanel, 1024, 2);
                     const uint64_t b_y = tc::sdesc(yt + kb_off * ytpanel + kin, 16, 1024, 2);
@@ -131,39 +147,47 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint64_t b_x = tc::sdesc(xs + k16 * 128, xpanel, 1024, 2);
                     tc::mma_f16(t_L, a_wl, b_x, id_L, kk != 0);
                 }
-                tc::mma_commit(pl_full);
+                tc::mma_commit(&pl_full[rg]);
                 tc::mbar_wait(pbuf_full, it & 1);
                 tc::fence_after();
-                const uint32_t pb = tc::smem_u32(sP);
+                const uint32_t pbs = pb;
                 for (int mt = 0; mt < m_tiles; ++mt) {
                     for (int kk = 0; kk < d / 16; ++kk) {
                         const int k16 = kk * 16;
                         const uint32_t pan = (uint32_t)(k16 / 64), kin = (uint32_t)(k16 % 64) * 2;
                         const uint64_t a_x = tc::sdesc(xs + pan * xpanel + mt * 16384 + kin, 16, 1024, 2);
-                        const uint64_t b_p = tc::sdesc(pb + pan * ppanel + kin, 16, 1024, 2);
+                        const uint64_t b_p = tc::sdesc(pbs + pan * ppanel + kin, 16, 1024, 2);
                         tc::mma_f16(t_F + mt * kpad, a_x, b_p, id_F, kk != 0);
                     }
                 }
-                tc::mma_commit(f_full);
+                tc::mma_commit(&f_full[rg]);
             }
         }
-    } else {  // ---- epilogue warps 2..5
-        const int q = warp & 3;
-        const int row = q * 32 + lane;  // TMEM lane
+    } else {  // ---- epilogue warps 2..9
+        const int e = warp - 2;
+        const int q = warp & 3;        // TMEM lane quarter this warp may access
+        const int half = e >> 2;       // which column half / M tile
+        const int row = q * 32 + lane; // TMEM lane
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const float inv_nk = 1.0f / (float)(p.n * p.k), inv_d = 1.0f / (float)d;
         int it = 0;
         for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
             const int st = it & 1;
-            const uint32_t ph = it & 1;
-            uint8_t* xs = sX + st * xstage;
-            tc::mbar_wait(pl_full, ph);
+            const int rg = nreg == 2 ? (it & 1) : 0;
+            const uint32_t rph = nreg == 2 ? ((it >> 1) & 1) : (it & 1);
+            const uint32_t t_P = tmem + rg * 256 + lane_off, t_L = t_P + 64, t_F = t_L + d;
+            const uint8_t* xs = sX + st * xstage;
+            tc::mbar_wait(&pl_full[rg], rph);
             tc::fence_after();
-            // P row `row` (= d index) -> bf16 -> Pbuf[j][row] (K-major B operand of F)
-            for (int c0 = 0; c0 < kpad; c0 += 16) {
+            // ---- P row `row` (= d index), 16-column chunks split across the two halves,
+            //      -> bf16 -> Pbuf[j][row] (K-major B operand of F). One Pbuf suffices: this
+            //      sample's writes start after the previous sample's F MMAs completed.
+            uint8_t* pbuf = sP;
+            for (int c0 = 16 * half; c0 < kpad; c0 += 32) {
                 float v[16];
-                tc::tmem_ld16(t_P + lane_off + c0, v);
+                tc::tmem_ld16(t_P + c0, v);
                 if (row < d) {
-                    uint8_t* pan = sP + (row / 64) * ppanel;
+                    uint8_t* pan = pbuf + (row / 64) * ppanel;
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
                         *reinterpret_cast<__nv_bfloat16*>(pan + swz(c0 + j, row & 63)) = __float2bfloat16_rn(v[j]);
@@ -171,18 +195,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tc::fence_async_shared();
             tc::mbar_arrive(pbuf_full);
-            // LCB half: X'[nF+row] = rms_norm_d(L[row] + X[nF+row])
+            // ---- LCB half: X'[nF+row] = rms_norm_d(L[row] + X[nF+row]); this warp owns
+            //      columns [half*d/2, (half+1)*d/2)
             {
-                float ss = 0.0f;
-                const bool live = row < p.nL;
                 const int xr = p.nF + row;
-                for (int c0 = 0; c0 < d; c0 += 32) {
-                    float v[32];
-                    tc::tmem_ld32(t_L + lane_off + c0, v);
-                    if (live) {
+                const bool live = row < p.nL;
+                const int cbase = half * (d / 2);
+                float v[64];
+                tc::tmem_ld32(t_L + cbase, v);
+                if (d == 128) tc::tmem_ld32(t_L + cbase + 32, v + 32);
+                float ss = 0.0f;
+                if (live) {
 #pragma unroll
-                        for (int j = 0; j < 32; j += 8) {
-                            const int c = c0 + j;
+                    for (int j = 0; j < 64; j += 8) {
+                        if (j < d / 2) {
+                            const int c = cbase + j;
                             const uint4 r = *reinterpret_cast<const uint4*>(xs + (c / 64) * xpanel + swz(xr, c & 63));
                             const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
@@ -190,95 +217,84 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 v[j + 2 * i] += bf16_lo(w[i]);
                                 v[j + 2 * i + 1] += bf16_hi(w[i]);
                             }
-                        }
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) ss += v[j] * v[j];
+                            for (int i = 0; i < 8; ++i) ss += v[j + i] * v[j + i];
+                        }
                     }
                 }
-                const float denom = sqrtf(ss / (float)d + 1e-6f);
-                for (int c0 = 0; c0 < d; c0 += 32) {
-                    float v[32];
-                    tc::tmem_ld32(t_L + lane_off + c0, v);
-                    if (live) {
-                        __nv_bfloat16* dst = p.Xout + (b * p.n + xr) * (int64_t)d + c0;
+                red_l[half * 128 + row] = ss;
+                tc::named_bar(1, kEpiThreads);
+                const float total = red_l[row] + red_l[128 + row];
+                const float inv = 1.0f / sqrtf(total * inv_d + 1e-6f);
+                if (live) {
+                    __nv_bfloat16* dst = p.Xout + (b * p.n + xr) * (int64_t)d + cbase;
 #pragma unroll
-                        for (int j = 0; j < 32; j += 8) {
-                            const int c = c0 + j;
-                            const uint4 r = *reinterpret_cast<const uint4*>(xs + (c / 64) * xpanel + swz(xr, c & 63));
-                            const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-                            float o[8];
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                o[2 * i] = (v[j + 2 * i] + bf16_lo(w[i])) / denom;
-                                o[2 * i + 1] = (v[j + 2 * i + 1] + bf16_hi(w[i])) / denom;
-                            }
+                    for (int j = 0; j < 64; j += 8)
+                        if (j < d / 2)
                             *reinterpret_cast<uint4*>(dst + j) =
-                                make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]),
-                                           pack_bf16x2(o[4], o[5]), pack_bf16x2(o[6], o[7]));
-                        }
-                    }
+                                make_uint4(pack_bf16x2(v[j] * inv, v[j + 1] * inv), pack_bf16x2(v[j + 2] * inv, v[j + 3] * inv),
+                                           pack_bf16x2(v[j + 4] * inv, v[j + 5] * inv), pack_bf16x2(v[j + 6] * inv, v[j + 7] * inv));
                 }
             }
-            // FM: Fin = rms_norm(flatten(X P)) over the n*k real entries
-            tc::mbar_wait(f_full, ph);
+            // ---- FM: Fin = rms_norm(flatten(X P)) over the n*k real entries; this warp
+            //      drains M tile `half`
+            tc::mbar_wait(&f_full[rg], rph);
             tc::fence_after();
-            float ss = 0.0f;
-            for (int mt = 0; mt < m_tiles; ++mt) {
-                const int r = mt * 128 + row;
-                for (int c0 = 0; c0 < kpad; c0 += 16) {
-                    float v[16];
-                    tc::tmem_ld16(t_F + lane_off + mt * kpad + c0, v);
+            {
+                const bool has_tile = half < m_tiles;
+                const int r = half * 128 + row;
+                float v[64];
+                float ss = 0.0f;
+                if (has_tile) {
+                    tc::tmem_ld32(t_F + half * kpad, v);
+                    if (kpad > 32) tc::tmem_ld32(t_F + half * kpad + 32, v + 32);
                     if (r < p.n) {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (c0 + j < p.k) ss += v[j] * v[j];
+                        for (int j = 0; j < 64; ++j)
+                            if (j < p.k) ss += v[j] * v[j];
                     }
                 }
-            }
-            ss = warp_sum(ss);
-            if (lane == 0) red[q] = ss;
-            tc::named_bar(1, 128);
-            const float total = red[0] + red[1] + red[2] + red[3];
-            const float denom = sqrtf(total / (float)(p.n * p.k) + 1e-6f);
-            for (int mt = 0; mt < m_tiles; ++mt) {
-                const int r = mt * 128 + row;
-                for (int c0 = 0; c0 < kpad; c0 += 16) {
-                    float v[16];
-                    tc::tmem_ld16(t_F + lane_off + mt * kpad + c0, v);
-                    if (r < p.n) {
-                        __nv_bfloat16* dst = p.Fout + b * (int64_t)p.n * p.k + (int64_t)r * p.k + c0;
-                        if ((p.k & 15) == 0) {
+                tc::fence_before();
+                tc::mbar_arrive(&tmem_empty[rg]);  // this thread's TMEM reads of the region are done
+                ss = warp_sum(ss);
+                if (lane == 0) red_f[e] = ss;
+                tc::named_bar(1, kEpiThreads);
+                float total = 0.0f;
 #pragma unroll
-                            for (int j = 0; j < 16; j += 8)
+                for (int i = 0; i < kEpiWarps; ++i) total += red_f[i];
+                const float inv = 1.0f / sqrtf(total * inv_nk + 1e-6f);
+                if (has_tile && r < p.n) {
+                    __nv_bfloat16* dst = p.Fout + b * (int64_t)p.n * p.k + (int64_t)r * p.k;
+                    if ((p.k & 7) == 0) {
+#pragma unroll
+                        for (int j = 0; j < 64; j += 8)
+                            if (j < p.k)
                                 *reinterpret_cast<uint4*>(dst + j) = make_uint4(
-                                    pack_bf16x2(v[j] / denom, v[j + 1] / denom), pack_bf16x2(v[j + 2] / denom, v[j + 3] / denom),
-                                    pack_bf16x2(v[j + 4] / denom, v[j + 5] / denom), pack_bf16x2(v[j + 6] / denom, v[j + 7] / denom));
-                        } else {
-                            for (int j = 0; j < 16 && c0 + j < p.k; ++j) dst[j] = __float2bfloat16_rn(v[j] / denom);
-                        }
+                                    pack_bf16x2(v[j] * inv, v[j + 1] * inv), pack_bf16x2(v[j + 2] * inv, v[j + 3] * inv),
+                                    pack_bf16x2(v[j + 4] * inv, v[j + 5] * inv), pack_bf16x2(v[j + 6] * inv, v[j + 7] * inv));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j)
+                            if (j < p.k) dst[j] = __float2bfloat16_rn(v[j] * inv);
                     }
                 }
             }
-            tc::named_bar(1, 128);  // red[] reuse guard
-            tc::fence_before();
-            tc::mbar_arrive(tmem_empty);
             tc::mbar_arrive(&x_empty[st]);
         }
     }
     tc::fence_before();
     __syncthreads();
-    if (warp == 1) tc::tmem_dealloc(tmem, p.tmem_cols);
+    if (warp == 1) tc::tmem_dealloc(tmem, tcols);
 }
 
 size_t smem_bytes(const Params& p) {
-    const int panels_d = p.d / 64, panels_n = (p.n_pad + 63) / 64;
+    const int panels_n = (p.n_pad + 63) / 64;
     size_t s = 1024;
-    s += (size_t)128 * 128 * panels_n;            // W_L
-    s += (size_t)p.k_pad * 128 * panels_n;        // Y^T
-    s += ((size_t)p.k_pad * 128 * panels_d + 1023) & ~size_t(1023);  // P
-    (void)panels_d;
+    s += (size_t)128 * 128 * panels_n;                      // W_L
+    s += (size_t)p.k_pad * 128 * panels_n;                  // Y^T
+    s += ((size_t)p.k_pad * 128 * 2 + 1023) & ~size_t(1023);  // P (2 panels)
     s += 2 * 2 * (size_t)(p.n_pad > 128 ? p.n_pad : 128) * 128;  // X stages (2 panels each)
-    s += 256;
+    s += 128 + 2 * 128 * 4 + 8 * 4 + 64;                    // barriers + reductions
     return s;
 }
 
@@ -290,6 +306,8 @@ lattice_status check(const Params& p) {
         return set_error(LATTICE_USAGE, "fm_lcb: k must be <= 64");
     if (p.nL < 0 || p.nL > 128 || p.nF + p.nL != p.n)
         return set_error(LATTICE_USAGE, "fm_lcb: nL must be <= 128 and nF + nL == n");
+    if (64 + p.d + ((p.n_pad + 127) / 128) * p.k_pad > 512)
+        return set_error(LATTICE_USAGE, "fm_lcb: accumulators exceed TMEM");
     if (smem_bytes(p) > 227 * 1024) return set_error(LATTICE_USAGE, "fm_lcb: shared memory budget exceeded");
     return LATTICE_OK;
 }

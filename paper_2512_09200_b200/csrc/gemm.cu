@@ -1,4 +1,11 @@
-// gemm.cu -- tcgen05 GEMM kernel (see gemm.cuh) + host launch helpers + lattice_gemm.
+// gemm.cu -- persistent tcgen05 GEMM kernel (see gemm.cuh) + host plan/launch + lattice_gemm.
+//
+// Persistent: one CTA per SM (or one cluster of C CTAs per C SMs) walks a static schedule of
+// output tiles. The TMA warp runs ahead through a STAGES-deep smem ring across tile
+// boundaries; the MMA warp accumulates tile i into TMEM region (i & 1) while the epilogue
+// warps drain region ((i-1) & 1), so epilogues (and their DSMEM exchanges) hide under the
+// next tile's mainloop. Dense tiles are rasterised in bands of 16 M-tiles so concurrently
+// running CTAs share A and B tiles in L2.
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -9,6 +16,9 @@
 
 namespace lat {
 namespace gemm {
+
+constexpr int BN = 256;
+constexpr int kRasterGroup = 16;
 
 // ---------------------------------------------------------------------------------------------
 // epilogue helpers (thread = accumulator row)
@@ -23,7 +33,9 @@ __device__ __forceinline__ void store_row32(const Params& p, int64_t m, int n, c
                     make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
                                pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
         } else {
-            for (int j = 0; j < 32 && n + j < p.N; ++j) dst[j] = __float2bfloat16_rn(v[j]);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (n + j < p.N) dst[j] = __float2bfloat16_rn(v[j]);
         }
     } else {
         float* dst = static_cast<float*>(p.C) + m * p.ldc + n;
@@ -32,13 +44,16 @@ __device__ __forceinline__ void store_row32(const Params& p, int64_t m, int n, c
             for (int j = 0; j < 32; j += 4)
                 *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         } else {
-            for (int j = 0; j < 32 && n + j < p.N; ++j) dst[j] = v[j];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (n + j < p.N) dst[j] = v[j];
         }
     }
 }
 
-// Sum a per-row partial across the cluster (rank order), via DSMEM. Every thread of the 4
-// epilogue warps calls this exactly once per exchange `slot` with its own row.
+// Sum a per-row partial across the cluster (rank order) through DSMEM. Every epilogue thread
+// of every CTA in the cluster calls this once per tile with its own row; `slot` alternates
+// with the tile so a fast CTA can run one tile ahead without clobbering a slow one.
 __device__ __forceinline__ float cluster_row_sum(float part, int row, int C, float* xbuf,
                                                  uint64_t* xbar, uint32_t phase) {
     if (C == 1) return part;
@@ -76,17 +91,54 @@ __device__ __forceinline__ void resid_norm_group(const Params& p, uint32_t taddr
     float ss = 0.0f;
 #pragma unroll
     for (int c = 0; c < GROUP; ++c) ss += v[c] * v[c];
-    const float denom = sqrtf(ss / (float)GROUP + 1e-6f);
+    const float inv = 1.0f / sqrtf(ss * (1.0f / (float)GROUP) + 1e-6f);
 #pragma unroll
-    for (int c = 0; c < GROUP; ++c) v[c] = v[c] / denom;
+    for (int c = 0; c < GROUP; ++c) v[c] *= inv;
 #pragma unroll
     for (int c = 0; c < GROUP; c += 32) store_row32(p, m, n + c, v + c);
+}
+
+// Tile schedule shared by all three roles.
+struct Sched {
+    int units;    // work units (C>1: M-tiles processed by a whole cluster; C==1: output tiles)
+    int first, stride;
+    int nt;       // N tiles
+    int mt;       // M tiles (dense)
+};
+
+__device__ __forceinline__ void decode(const Params& p, const Sched& s, int u, int rank, int& group,
+                                       int& m0, int& m_end, int& n0) {
+    int mu, nn;
+    if (p.cluster > 1) {
+        mu = u;
+        nn = rank;
+    } else if (p.tiles) {
+        mu = u / s.nt;
+        nn = u % s.nt;
+    } else {  // banded raster: kRasterGroup M-tiles share each N-tile sweep
+        const int per = kRasterGroup * s.nt;
+        const int g = u / per, in = u % per;
+        const int rows = min(kRasterGroup, s.mt - g * kRasterGroup);
+        mu = g * kRasterGroup + in % rows;
+        nn = in / rows;
+    }
+    if (p.tiles) {
+        const int4 t = p.tiles[mu];
+        group = t.x;
+        m0 = t.y;
+        m_end = t.z;
+    } else {
+        group = 0;
+        m0 = mu * BM;
+        m_end = p.M;
+    }
+    n0 = nn * BN;
 }
 
 // ---------------------------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------------------------
-template <int BN, int STAGES>
+template <int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const Params p) {
@@ -98,45 +150,48 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sB = smem + STAGES * A_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
     uint64_t* empty = full + STAGES;
-    uint64_t* accum_full = empty + STAGES;
-    uint64_t* xbar = accum_full + 1;     // row-stat exchange (phase 0)
-    uint64_t* hbar = xbar + 1;           // head-partial exchange (phase 0)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hbar + 1);
-    float* xbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);
-    float* hbuf = xbuf + kMaxCluster * BM;
+    uint64_t* tfull = empty + STAGES;    // [2] accumulator region ready
+    uint64_t* tempty = tfull + 2;        // [2] accumulator region drained
+    uint64_t* xbar = tempty + 2;         // [2] row-stat exchange
+    uint64_t* hbar = xbar + 2;           // [2] head-partial exchange
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hbar + 2);
+    float* xbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);  // [2][8][128]
+    float* hbuf = xbuf + 2 * kMaxCluster * BM;                                       // [2][C][heads][128]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int C = p.cluster;
+    const int rank = C > 1 ? (int)tc::cluster_rank() : 0;
 
-    // tile coordinates
-    int group = 0, m0, m_end;
-    if (p.tiles) {
-        if ((int)blockIdx.y >= *p.n_tiles) return;  // whole cluster shares blockIdx.y
-        const int4 t = p.tiles[blockIdx.y];
-        group = t.x;
-        m0 = t.y;
-        m_end = t.z;
+    Sched s;
+    s.nt = (p.N + BN - 1) / BN;
+    s.mt = (p.M + BM - 1) / BM;
+    if (C > 1) {
+        s.units = p.tiles ? *p.n_tiles : s.mt;
+        s.first = blockIdx.x / C;
+        s.stride = gridDim.x / C;
     } else {
-        m0 = blockIdx.y * BM;
-        m_end = p.M;
+        s.units = (p.tiles ? *p.n_tiles : s.mt) * s.nt;
+        s.first = blockIdx.x;
+        s.stride = gridDim.x;
     }
-    const int n0 = blockIdx.x * BN;
-    const int b_row0 = group * p.b_rows_per_group + n0;
     const int nk = (p.K + BK - 1) / BK;
 
     if (warp == 0 && lane == 0) {
         tc::tma_prefetch(&tmA);
         tc::tma_prefetch(&tmB);
-        for (int s = 0; s < STAGES; ++s) {
-            tc::mbar_init(&full[s], 1);
-            tc::mbar_init(&empty[s], 1);
+        for (int i = 0; i < STAGES; ++i) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&empty[i], 1);
         }
-        tc::mbar_init(accum_full, 1);
-        tc::mbar_init(xbar, BM * C);
-        tc::mbar_init(hbar, BM * C);
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&tfull[i], 1);
+            tc::mbar_init(&tempty[i], BM);
+            tc::mbar_init(&xbar[i], BM * C);
+            tc::mbar_init(&hbar[i], BM * C);
+        }
         tc::fence_mbar_init();
     }
-    if (warp == 1) tc::tmem_alloc(tmem_slot, BN);
+    if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * BN);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
@@ -145,143 +200,170 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                tc::mbar_wait(&empty[s], ph ^ 1);
-                tc::mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-                tc::tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, m0);
-                tc::tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, b_row0);
+            int g = 0;
+            for (int u = s.first; u < s.units; u += s.stride) {
+                int group, m0, m_end, n0;
+                decode(p, s, u, rank, group, m0, m_end, n0);
+                const int b_row0 = group * p.b_rows_per_group + n0;
+                for (int kb = 0; kb < nk; ++kb, ++g) {
+                    const int st = g % STAGES;
+                    const uint32_t ph = (g / STAGES) & 1;
+                    tc::mbar_wait(&empty[st], ph ^ 1);
+                    tc::mbar_expect_tx(&full[st], A_BYTES + B_BYTES);
+                    tc::tma_load_2d(sA + st * A_BYTES, &tmA, &full[st], kb * BK, m0);
+                    tc::tma_load_2d(sB + st * B_BYTES, &tmB, &full[st], kb * BK, b_row0);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---- MMA issuer
             constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                tc::mbar_wait(&full[s], ph);
+            int g = 0, i = 0;
+            for (int u = s.first; u < s.units; u += s.stride, ++i) {
+                const int acc = i & 1;
+                tc::mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
                 tc::fence_after();
-                const uint32_t a_base = tc::smem_u32(sA + s * A_BYTES);
-                const uint32_t b_base = tc::smem_u32(sB + s * B_BYTES);
+                const uint32_t d_tmem = tmem + acc * BN;
+                for (int kb = 0; kb < nk; ++kb, ++g) {
+                    const int st = g % STAGES;
+                    const uint32_t ph = (g / STAGES) & 1;
+                    tc::mbar_wait(&full[st], ph);
+                    tc::fence_after();
+                    const uint32_t a_base = tc::smem_u32(sA + st * A_BYTES);
+                    const uint32_t b_base = tc::smem_u32(sB + st * B_BYTES);
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                    const uint64_t ad = tc::sdesc(a_base + k * 32, 16, 1024, 2);
-                    const uint64_t bd = tc::sdesc(b_base + k * 32, 16, 1024, 2);
-                    tc::mma_f16(tmem, ad, bd, idesc, (kb | k) != 0);
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t ad = tc::sdesc(a_base + k * 32, 16, 1024, 2);
+                        const uint64_t bd = tc::sdesc(b_base + k * 32, 16, 1024, 2);
+                        tc::mma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    tc::mma_commit(&empty[st]);
                 }
-                tc::mma_commit(&empty[s]);
+                tc::mma_commit(&tfull[acc]);
             }
-            tc::mma_commit(accum_full);
         }
     } else {  // ---- epilogue warps 2..5
         const int q = warp & 3;
         const int row = q * 32 + lane;
-        const int64_t m = (int64_t)m0 + row;
-        const bool valid = m < m_end;
-        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16);
-        tc::mbar_wait(accum_full, 0);
-        tc::fence_after();
         const int epi = p.epi;
-        if (epi == kStore) {
-#pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
-                float v[32];
-                tc::tmem_ld32(taddr + c, v);
-                if (valid && n0 + c < p.N) store_row32(p, m, n0 + c, v);
-            }
-        } else if (epi == kResidNorm) {
-            if (p.group == 128) {
-#pragma unroll 1
-                for (int g = 0; g < BN; g += 128)
-                    if (n0 + g < p.N) resid_norm_group<128>(p, taddr + g, m, n0 + g, valid);
-            } else {
-#pragma unroll 1
-                for (int g = 0; g < BN; g += 64)
-                    if (n0 + g < p.N) resid_norm_group<64>(p, taddr + g, m, n0 + g, valid);
-            }
-        } else {  // row-wide swish_rn (+ tower heads)
-            const bool hard = epi == kSwishHard || epi == kTowerHard;
-            float ss = 0.0f;
-#pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
-                float v[32];
-                tc::tmem_ld32(taddr + c, v);
-                // columns >= N may hold another group's weights (stacked towers): mask them
-#pragma unroll
-                for (int j = 0; j < 32; ++j) ss += (n0 + c + j < p.N) ? v[j] * v[j] : 0.0f;
-            }
-            const float total = cluster_row_sum(ss, row, C, xbuf, xbar, 0);
-            const float denom = sqrtf(total / (float)p.N_full + 1e-6f);
-            if (epi == kSwish || epi == kSwishHard) {
+        const bool hard = epi == kSwishHard || epi == kTowerHard;
+        int i = 0;
+        for (int u = s.first; u < s.units; u += s.stride, ++i) {
+            int group, m0, m_end, n0;
+            decode(p, s, u, rank, group, m0, m_end, n0);
+            const int acc = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            const int64_t m = (int64_t)m0 + row;
+            const bool valid = m < m_end;
+            const uint32_t taddr = tmem + acc * BN + ((uint32_t)(q * 32) << 16);
+            tc::mbar_wait(&tfull[acc], ph);
+            tc::fence_after();
+            if (epi == kStore) {
 #pragma unroll 1
                 for (int c = 0; c < BN; c += 32) {
                     float v[32];
                     tc::tmem_ld32(taddr + c, v);
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = act_swish(v[j] / denom, hard);
                     if (valid && n0 + c < p.N) store_row32(p, m, n0 + c, v);
                 }
-            } else {  // tower: heads = W2_g . swish_rn(row)
-                float part[kMaxHeads];
-#pragma unroll
-                for (int j = 0; j < kMaxHeads; ++j) part[j] = 0.0f;
-                const float* w2 = p.W2 + (size_t)group * p.heads * p.N_full;
+                tc::fence_before();
+                tc::mbar_arrive(&tempty[acc]);
+            } else if (epi == kResidNorm) {
+                if (p.group == 128) {
+#pragma unroll 1
+                    for (int gc = 0; gc < BN; gc += 128)
+                        if (n0 + gc < p.N) resid_norm_group<128>(p, taddr + gc, m, n0 + gc, valid);
+                } else {
+#pragma unroll 1
+                    for (int gc = 0; gc < BN; gc += 64)
+                        if (n0 + gc < p.N) resid_norm_group<64>(p, taddr + gc, m, n0 + gc, valid);
+                }
+                tc::fence_before();
+                tc::mbar_arrive(&tempty[acc]);
+            } else {  // row-wide swish_rn (+ tower heads)
+                float ss = 0.0f;
 #pragma unroll 1
                 for (int c = 0; c < BN; c += 32) {
                     float v[32];
                     tc::tmem_ld32(taddr + c, v);
-                    if (n0 + c >= p.N) continue;
+                    // columns >= N may hold another group's weights (stacked towers): mask them
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = (n0 + c + j < p.N) ? act_swish(v[j] / denom, hard) : 0.0f;
+                    for (int j = 0; j < 32; ++j) ss += (n0 + c + j < p.N) ? v[j] * v[j] : 0.0f;
+                }
+                const float total = cluster_row_sum(ss, row, C, xbuf + acc * kMaxCluster * BM, &xbar[acc], ph);
+                const float inv = 1.0f / sqrtf(total / (float)p.N_full + 1e-6f);
+                if (epi == kSwish || epi == kSwishHard) {
+#pragma unroll 1
+                    for (int c = 0; c < BN; c += 32) {
+                        float v[32];
+                        tc::tmem_ld32(taddr + c, v);
 #pragma unroll
-                    for (int h = 0; h < kMaxHeads; ++h) {
-                        if (h < p.heads) {
-                            const float* wr = w2 + (size_t)h * p.N_full + n0 + c;
-                            float a = 0.0f;
-                            if (n0 + c + 32 <= p.N) {
-#pragma unroll
-                                for (int j = 0; j < 32; j += 4) {
-                                    const float4 w = __ldg(reinterpret_cast<const float4*>(wr + j));
-                                    a += v[j] * w.x + v[j + 1] * w.y + v[j + 2] * w.z + v[j + 3] * w.w;
-                                }
-                            } else {
-#pragma unroll
-                                for (int j = 0; j < 32; ++j)
-                                    if (n0 + c + j < p.N) a += v[j] * __ldg(wr + j);
-                            }
-                            part[h] += a;
-                        }
+                        for (int j = 0; j < 32; ++j) v[j] = act_swish(v[j] * inv, hard);
+                        if (valid && n0 + c < p.N) store_row32(p, m, n0 + c, v);
                     }
-                }
-                // reduce head partials into cluster rank 0 (rank order), then write
-                const uint32_t my = C > 1 ? tc::cluster_rank() : 0;
-                if (C > 1) {
+                    tc::fence_before();
+                    tc::mbar_arrive(&tempty[acc]);
+                } else {  // tower: heads = W2_g . swish_rn(row)
+                    float part[kMaxHeads];
 #pragma unroll
-                    for (int h = 0; h < kMaxHeads; ++h)
-                        if (h < p.heads)
-                            tc::st_cluster_f32(
-                                tc::mapa(tc::smem_u32(&hbuf[(my * p.heads + h) * BM + row]), 0), part[h]);
-                    tc::mbar_arrive_remote(tc::mapa(tc::smem_u32(hbar), 0));
-                }
-                if (my == 0) {
-                    if (C > 1) {
-                        // hbar expects BM*C arrivals; each CTA's 128 threads arrive once
-                        tc::mbar_wait_cluster(hbar, 0);
+                    for (int h = 0; h < kMaxHeads; ++h) part[h] = 0.0f;
+                    const float* w2 = p.W2 + (size_t)group * p.heads * p.N_full;
+#pragma unroll 1
+                    for (int c = 0; c < BN; c += 32) {
+                        float v[32];
+                        tc::tmem_ld32(taddr + c, v);
+                        if (n0 + c >= p.N) continue;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = (n0 + c + j < p.N) ? act_swish(v[j] * inv, hard) : 0.0f;
 #pragma unroll
                         for (int h = 0; h < kMaxHeads; ++h) {
                             if (h < p.heads) {
-                                float s = 0.0f;
-                                for (int r = 0; r < C; ++r) s += hbuf[(r * p.heads + h) * BM + row];
-                                part[h] = s;
+                                const float* wr = w2 + (size_t)h * p.N_full + n0 + c;
+                                float a = 0.0f;
+                                if (n0 + c + 32 <= p.N) {
+#pragma unroll
+                                    for (int j = 0; j < 32; j += 4) {
+                                        const float4 w = __ldg(reinterpret_cast<const float4*>(wr + j));
+                                        a += v[j] * w.x + v[j + 1] * w.y + v[j + 2] * w.z + v[j + 3] * w.w;
+                                    }
+                                } else {
+#pragma unroll
+                                    for (int j = 0; j < 32; ++j)
+                                        if (n0 + c + j < p.N) a += v[j] * __ldg(wr + j);
+                                }
+                                part[h] += a;
                             }
                         }
                     }
-                    if (valid) {
-                        const int64_t b = p.order ? (int64_t)p.order[m] : m;
+                    tc::fence_before();
+                    tc::mbar_arrive(&tempty[acc]);
+                    // reduce head partials into cluster rank 0 (rank order), then write
+                    float* hb = hbuf + (size_t)acc * C * p.heads * BM;
+                    if (C > 1) {
 #pragma unroll
                         for (int h = 0; h < kMaxHeads; ++h)
-                            if (h < p.heads) p.logits[b * p.heads + h] = part[h];
+                            if (h < p.heads)
+                                tc::st_cluster_f32(tc::mapa(tc::smem_u32(&hb[(rank * p.heads + h) * BM + row]), 0),
+                                                   part[h]);
+                        tc::mbar_arrive_remote(tc::mapa(tc::smem_u32(&hbar[acc]), 0));
+                    }
+                    if (rank == 0) {
+                        if (C > 1) {
+                            tc::mbar_wait_cluster(&hbar[acc], ph);
+#pragma unroll
+                            for (int h = 0; h < kMaxHeads; ++h) {
+                                if (h < p.heads) {
+                                    float sum = 0.0f;
+                                    for (int r = 0; r < C; ++r) sum += hb[(r * p.heads + h) * BM + row];
+                                    part[h] = sum;
+                                }
+                            }
+                        }
+                        if (valid) {
+                            const int64_t b = p.order ? (int64_t)p.order[m] : m;
+#pragma unroll
+                            for (int h = 0; h < kMaxHeads; ++h)
+                                if (h < p.heads) p.logits[b * p.heads + h] = part[h];
+                        }
                     }
                 }
             }
@@ -289,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc::fence_before();
     __syncthreads();
-    if (warp == 1) tc::tmem_dealloc(tmem, BN);
+    if (warp == 1) tc::tmem_dealloc(tmem, 2 * BN);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -309,31 +391,36 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <int BN, int STAGES>
-lattice_status launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid_y,
+template <int STAGES>
+lattice_status launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int units,
                         cudaStream_t st) {
-    const size_t smem = smem_bytes(BN, STAGES, p.cluster, p.heads);
+    const size_t smem = smem_bytes(BN, STAGES, p.cluster, p.heads) + kMaxCluster * BM * 4 +
+                        (size_t)p.cluster * p.heads * BM * 4;  // double-buffered exchange slots
     static bool attr_done = false;
     if (!attr_done) {
-        LAT_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, STAGES>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        LAT_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, STAGES>,
-                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        LAT_CUDA(cudaFuncSetAttribute(gemm_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      227 * 1024));
+        LAT_CUDA(cudaFuncSetAttribute(gemm_kernel<STAGES>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         attr_done = true;
     }
+    if (smem > 227 * 1024) return set_error(LATTICE_USAGE, "gemm: shared memory budget exceeded");
+    const int C = p.cluster;
+    int clusters = num_sms() / C;
+    if (clusters > units) clusters = units;
+    if (clusters < 1) clusters = 1;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((p.N + BN - 1) / BN, grid_y, 1);
+    cfg.gridDim = dim3(clusters * C, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = p.cluster;
+    at[0].val.clusterDim.x = C;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    LAT_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, STAGES>, ta, tb, p));
+    LAT_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<STAGES>, ta, tb, p));
     return LATTICE_OK;
 }
 }  // namespace
@@ -356,30 +443,22 @@ lattice_status make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uin
     return LATTICE_OK;
 }
 
-int default_stages() {
-    static int s = -1;
-    if (s < 0) {
-        const char* e = std::getenv("LATTICE_GEMM_STAGES");
-        s = e ? std::atoi(e) : 4;
-        if (s != 2 && s != 4) s = 4;
-    }
-    return s;
-}
-
 lattice_status launch(const GemmPlan& g, cudaStream_t st) {
-    if (g.stages == 2) return launch_t<256, 2>(g.ta, g.tb, g.p, g.grid_y, st);
-    return launch_t<256, 4>(g.ta, g.tb, g.p, g.grid_y, st);
+    // grid_y carries the number of M units (dense M-tiles, or the tile-table capacity)
+    const int nt = (g.p.N + BN - 1) / BN;
+    const int units = g.p.cluster > 1 ? g.grid_y : g.grid_y * nt;
+    return launch_t<4>(g.ta, g.tb, g.p, units, st);
 }
 
 lattice_status plan(GemmPlan* g, const void* A, int64_t lda, int64_t a_rows, const void* B,
                     int64_t ldb, int64_t b_rows, const Params& p, int grid_y) {
     lattice_status s = make_map_2d(&g->ta, A, (uint64_t)p.K, (uint64_t)a_rows, (uint64_t)lda * 2, BK, BM);
     if (s != LATTICE_OK) return s;
-    s = make_map_2d(&g->tb, B, (uint64_t)p.K, (uint64_t)b_rows, (uint64_t)ldb * 2, BK, 256);
+    s = make_map_2d(&g->tb, B, (uint64_t)p.K, (uint64_t)b_rows, (uint64_t)ldb * 2, BK, BN);
     if (s != LATTICE_OK) return s;
     g->p = p;
     g->grid_y = grid_y;
-    g->stages = default_stages();
+    g->stages = 4;
     return LATTICE_OK;
 }
 
@@ -411,7 +490,7 @@ extern "C" lattice_status lattice_gemm(const lattice_gemm_args* a, lattice_strea
     p.cluster = 1;
     p.heads = 0;
     if (p.epi == kSwish || p.epi == kSwishHard) {
-        p.cluster = (p.N + 255) / 256;
+        p.cluster = (p.N + BN - 1) / BN;
         LAT_REQUIRE(p.cluster <= kMaxCluster, "lattice_gemm: swish_rn rows wider than 2048 are not supported");
     }
     if (p.epi == kResidNorm) {
