@@ -272,18 +272,43 @@ def run_mid(args, rank, world, local):
     c = MID
     n, d, B = c["n"], c["d"], MID_B
     net = L.Network(**c, max_batch=B, weight_seed=SEED_W)
-    tab = torch.empty((n, MID_ROWS, d), dtype=torch.bfloat16, device="cuda")
-    L.fill_tables(tab, SEED_T)
-    ptrs = torch.tensor([t.data_ptr() for t in tab.unbind(0)], dtype=torch.int64, device="cuda")
-    rows = torch.full((n,), MID_ROWS, dtype=torch.int64, device="cuda")
+    sharded = world > 1
+    if sharded:  # table-wise: this rank owns features [rank*n/W, (rank+1)*n/W)
+        from paper_2512_09200_b200.sharded import ShardedBags
+        sb = ShardedBags(n, B, d, world, rank)
+        n_tab = sb.Fl
+        tab = torch.empty((n_tab, MID_ROWS, d), dtype=torch.bfloat16, device="cuda")
+        L.fill_tables(tab, SEED_T, feature_base=sb.owned()[0], rows_total=MID_ROWS)
+        send = torch.empty((world * B, sb.Fl, d), dtype=torch.bfloat16, device="cuda")
+        recv = torch.empty_like(send)
+    else:
+        n_tab = n
+        tab = torch.empty((n, MID_ROWS, d), dtype=torch.bfloat16, device="cuda")
+        L.fill_tables(tab, SEED_T)
+    tables = list(tab.unbind(0))
+    ptrs = torch.tensor([t.data_ptr() for t in tables], dtype=torch.int64, device="cuda")
+    rows = torch.full((n_tab,), MID_ROWS, dtype=torch.int64, device="cuda")
     offsets, ids = L.synth_bags(n, B, MID_MAXLEN, MID_ROWS, SEED_D + rank)
     dom = L.synth_domains(B, c["domains"], SEED_D + rank)
     n_ids = int(offsets[-1].item())
+    if sharded:  # static exchange capacity (setup, outside the timed region): max slice over ranks
+        import torch.distributed as dist
+        cnt, _ = sb.slice_counts(offsets)
+        cap = cnt.max().reshape(1)
+        dist.all_reduce(cap, op=dist.ReduceOp.MAX)
+        sb.capacity = int(cap.item())
     logits = torch.empty((B, c["heads"]), dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
 
+    def forward(dm, off, ii, out):
+        if sharded:
+            pooled = sb.forward_embeddings(off, ii, tables, ptrs, rows, send=send, recv=recv)
+            net.forward(dm, pooled=pooled, shards=world, logits=out)
+        else:
+            net.forward(dm, off, ii, ptrs, rows, torch.bfloat16, logits=out)
+
     def step():
-        net.forward(dom, offsets, ids, ptrs, rows, torch.bfloat16, logits=logits)
+        forward(dom, offsets, ids, logits)
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -305,14 +330,23 @@ def run_mid(args, rank, world, local):
 
     # per-stage device times (separate pass, events between stages)
     net.set_timing(True)
-    stages = []
+    stages, emb_ms = [], []
     for _ in range(3):
-        step()
+        if sharded:  # ids a2a + owner pooling + pooled a2a, timed on the stream
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            pooled = sb.forward_embeddings(offsets, ids, tables, ptrs, rows, send=send, recv=recv)
+            a1.record(stream)
+            net.forward(dom, pooled=pooled, shards=world, logits=logits)
+            torch.cuda.synchronize()
+            emb_ms.append(a0.elapsed_time(a1))
+        else:
+            step()
         stages.append(net.stage_times())
     net.set_timing(False)
     st = [statistics.median(s[i] for s in stages) for i in range(len(stages[0]))]
-    # stages: [bucket, bag, (fm_lcb, mlp) x blocks, tower]
-    t_bag = st[1]
+    # stages: [bucket, bag (or shard gather), (fm_lcb, mlp) x blocks, tower]
+    t_bag = st[1] + (statistics.median(emb_ms) if sharded else 0.0)
     t_fm = [st[2 + 2 * b] for b in range(c["blocks"])]
     t_mlp = [st[3 + 2 * b] for b in range(c["blocks"])]
     t_tower = st[2 + 2 * c["blocks"]]
@@ -355,7 +389,7 @@ def run_mid(args, rank, world, local):
                 h2d(i + 1)
             stream.wait_event(copied[i % 2])
             o, ii, dm = bufs[i % 2]
-            net.forward(dm, o, ii, ptrs, rows, torch.bfloat16, logits=logits)
+            forward(dm, o, ii, logits)
             consumed[i % 2].record(stream)
             h_out.copy_(logits, non_blocking=True)
 
@@ -370,6 +404,9 @@ def run_mid(args, rank, world, local):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
 
     launches = 3 + c["blocks"] * (1 + len(c["mlp"]) - 1) + 1
+    if sharded:
+        sb.check_overflow()
+        launches += 2  # owner bag kernel + offsets scan (the bag slot above is the shard gather)
     res = {
         "metric": "Lattice Network samples/sec (mid config, forward step)",
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
@@ -380,7 +417,8 @@ def run_mid(args, rank, world, local):
                                "heads, tower 32768-512-6, B=32768/GPU",
                    "global_batch": world * B, "ids_per_step": n_ids,
                    "l2": "embedding rows drawn uniformly from 6.6 GB of tables; activations 2.1 GB/buffer (> L2)",
-                   "parallelism": f"replicas x{world}"},
+                   "parallelism": (f"table-wise sharded embeddings over {world} GPUs (ids + pooled "
+                                   f"all-to-all, NCCL/NVLink) + dense replicas") if sharded else "1 GPU"},
         "e2e": {"value": world * B / (e2e_ms / 1e3), "unit": "samples/s",
                 "h2d_bytes_per_step": (n * B + 1) * 8 + n_ids * 4 + B * 4,
                 "d2h_bytes_per_step": B * c["heads"] * 4},

@@ -102,7 +102,15 @@ typedef struct {
     const int32_t* sample_pos;   /* optional DEVICE [B]: output row of sample b (NULL = b) */
     int32_t normalize;           /* 1: rms_norm over D of each pooled row (numerics.hpp:81) */
     int32_t check;               /* 1: synchronise and return DATA on an id outside [0, rows) */
+    int32_t sources;             /* R >= 1: bags laid out [R][F][B] (after an ids all-to-all,
+                                    R = source ranks); bag (r, f, b) writes output row r*B + b.
+                                    0 is treated as 1. */
 } lattice_bag_args;
+
+/* Exclusive prefix sum of bag lengths into CSR offsets (n+1 entries): the owner side of the
+ * ids all-to-all rebuilds its offsets with this. */
+lattice_status lattice_lengths_to_offsets(int64_t n, const int32_t* lengths, int64_t* offsets,
+                                          lattice_stream stream);
 
 lattice_status lattice_embedding_bag(const lattice_bag_args* args, lattice_stream stream);
 
@@ -200,8 +208,13 @@ typedef struct {
     const int64_t* rows;
     const int64_t* offsets;
     const int32_t* ids;
-    /* or, when tables == NULL: already pooled sums [B][n][d] in table_dtype */
+    /* or, when tables == NULL: already pooled embeddings in table_dtype */
     const void* pooled;
+    int32_t pooled_layout;       /* 0: raw sums [B][n][d], caller order (the net normalises)
+                                    1: table-wise shards [S][B][n/S][d] bf16, already
+                                       rms-normalised by the owners (lattice_embedding_bag
+                                       with normalize = 1), S = shards */
+    int32_t shards;
 } lattice_batch;
 
 /* logits: DEVICE fp32 [B][heads] in the caller's sample order. */

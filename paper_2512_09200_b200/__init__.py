@@ -61,7 +61,7 @@ class BagArgs(ctypes.Structure):
     _fields_ = [("features", _I32), ("batch", _I64), ("dim", _I32), ("table_dtype", _I32),
                 ("tables", _P), ("rows", _P), ("offsets", _P), ("ids", _P), ("out_dtype", _I32),
                 ("out", _P), ("out_row_stride", _I64), ("out_feature_offset", _I32),
-                ("sample_pos", _P), ("normalize", _I32), ("check", _I32)]
+                ("sample_pos", _P), ("normalize", _I32), ("check", _I32), ("sources", _I32)]
 
 
 class GemmArgs(ctypes.Structure):
@@ -79,7 +79,8 @@ class NetConfig(ctypes.Structure):
 
 class Batch(ctypes.Structure):
     _fields_ = [("batch", _I64), ("domain", _P), ("table_dtype", _I32), ("tables", _P),
-                ("rows", _P), ("offsets", _P), ("ids", _P), ("pooled", _P)]
+                ("rows", _P), ("offsets", _P), ("ids", _P), ("pooled", _P),
+                ("pooled_layout", _I32), ("shards", _I32)]
 
 
 def _sig(name, res, args):
@@ -102,6 +103,7 @@ _sig("lattice_fill_weights", ctypes.c_int, [_P, _I32, _I64, _I64, _U64, _U64, _P
 _sig("lattice_synth_bags", ctypes.c_int, [_I32, _I64, _I32, _I64, _U64, _P, _P, _P])
 _sig("lattice_synth_domains", ctypes.c_int, [_I64, _I32, _U64, _P, _P])
 _sig("lattice_domain_bucket", ctypes.c_int, [_I64, _I32, _P, _P, _P, _P, _P])
+_sig("lattice_lengths_to_offsets", ctypes.c_int, [_I64, _P, _P, _P])
 _sig("lattice_gemm", ctypes.c_int, [ctypes.POINTER(GemmArgs), _P])
 _sig("lattice_net_create", ctypes.c_int, [ctypes.POINTER(NetConfig), ctypes.POINTER(_P)])
 _sig("lattice_net_destroy", None, [_P])
@@ -115,7 +117,8 @@ EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_versio
            "lattice_stable_hash", "lattice_zipper_validate", "lattice_zipper_assign_labels",
            "lattice_embedding_bag", "lattice_rownorm", "lattice_fill_tables",
            "lattice_fill_weights", "lattice_synth_bags", "lattice_synth_domains",
-           "lattice_domain_bucket", "lattice_gemm", "lattice_net_create", "lattice_net_destroy",
+           "lattice_domain_bucket", "lattice_lengths_to_offsets", "lattice_gemm",
+           "lattice_net_create", "lattice_net_destroy",
            "lattice_net_weight", "lattice_net_forward", "lattice_net_set_timing",
            "lattice_net_stage_times"]
 
@@ -184,9 +187,10 @@ def stable_hash(bytes_, off, seed, stream=None):
 
 def embedding_bag(tables, offsets, ids, batch, out=None, out_dtype=None, sample_pos=None,
                   normalize=False, out_row_stride=None, out_feature_offset=0, check_errors=True,
-                  stream=None, table_ptrs=None, rows=None):
+                  stream=None, table_ptrs=None, rows=None, sources=1):
     """Sum-pooled embedding bags. tables: list of [rows_f, D] CUDA tensors (f32 or bf16).
-    offsets int64 [F*B+1] feature-major CSR, ids int32. Returns out [B, F, D]."""
+    offsets int64 [R*F*B+1] CSR with bags laid out [R][F][B] (R = sources, 1 = plain
+    feature-major), ids int32. Returns out [R*B, F, D]."""
     import torch
     F = len(tables)
     D = tables[0].shape[1]
@@ -198,12 +202,23 @@ def embedding_bag(tables, offsets, ids, batch, out=None, out_dtype=None, sample_
     if rows is None:
         rows = torch.tensor([t.shape[0] for t in tables], dtype=torch.int64, device=dev)
     if out is None:
-        out = torch.empty((batch, F, D), dtype=odt, device=dev)
+        out = torch.empty((sources * batch, F, D), dtype=odt, device=dev)
     stride = out_row_stride if out_row_stride is not None else F * D
     a = BagArgs(F, batch, D, F32 if tdt == torch.float32 else BF16, _p(table_ptrs), _p(rows),
                 _p(offsets), _p(ids), F32 if odt == torch.float32 else BF16, _p(out), stride,
-                out_feature_offset, _p(sample_pos), 1 if normalize else 0, 1 if check_errors else 0)
+                out_feature_offset, _p(sample_pos), 1 if normalize else 0, 1 if check_errors else 0,
+                sources)
     check(_lib.lattice_embedding_bag(ctypes.byref(a), _stream(stream)))
+    return out
+
+
+def lengths_to_offsets(lengths, out=None, stream=None):
+    """int32 bag lengths [n] -> int64 CSR offsets [n+1] (exclusive scan on the GPU)."""
+    import torch
+    n = lengths.numel()
+    if out is None:
+        out = torch.empty(n + 1, dtype=torch.int64, device=lengths.device)
+    check(_lib.lattice_lengths_to_offsets(n, _p(lengths), _p(out), _stream(stream)))
     return out
 
 
@@ -333,7 +348,9 @@ class Network:
             pass
 
     def forward(self, domain, offsets=None, ids=None, table_ptrs=None, rows=None,
-                table_dtype=None, pooled=None, logits=None, stream=None):
+                table_dtype=None, pooled=None, logits=None, stream=None, shards=0):
+        """shards > 0: `pooled` is the table-wise sharded, owner-normalised bf16 layout
+        [S][B][n/S][d] received from the pooled all-to-all."""
         import torch
         B = domain.shape[0]
         if logits is None:
@@ -344,6 +361,8 @@ class Network:
         if pooled is not None:
             b.table_dtype = F32 if pooled.dtype == torch.float32 else BF16
             b.pooled = _p(pooled)
+            b.pooled_layout = 1 if shards else 0
+            b.shards = shards
         else:
             b.table_dtype = F32 if table_dtype == torch.float32 else BF16
             b.tables, b.rows, b.offsets, b.ids = _p(table_ptrs), _p(rows), _p(offsets), _p(ids)

@@ -11,6 +11,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -32,6 +33,7 @@ struct BagParams {
     const int32_t* pos;
     int32_t normalize;
     unsigned long long* err;
+    int32_t R;  // source ranks: bags laid out [R][F][B]
 };
 
 __device__ __forceinline__ uint4 ld_stream(const void* p) {
@@ -93,20 +95,34 @@ __device__ __forceinline__ void store_out<__nv_bfloat16, 8>(__nv_bfloat16* dst, 
 
 constexpr int kBagWarps = 8;
 
-template <typename TT, typename OT, int LPR, int CPL>
-__global__ void __launch_bounds__(kBagWarps * 32) bag_kernel(const BagParams p) {
+// Persistent: each warp walks bags bag0, bag0 + nwarps, ... While the current bag's rows are
+// in flight, the next bag's offsets and first 32 ids are already being fetched, so the
+// offsets -> ids -> rows dependency chain of one bag overlaps the row traffic of the previous.
+template <typename TT, typename OT, int LPR, int CPL, int U, int MINB>
+__global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagParams p) {
     constexpr int EPC = Elem<TT>::kPerChunk;
-    constexpr int RPP = 32 / LPR;  // rows per pass
-    constexpr int U = 4;           // passes in flight
+    constexpr int RPP = 32 / LPR;  // rows per pass; U passes in flight
     const int lane = threadIdx.x & 31;
-    const int64_t bag = (int64_t)blockIdx.x * kBagWarps + (threadIdx.x >> 5);
-    if (bag >= (int64_t)p.F * p.B) return;
-    const int f = (int)(bag / p.B);
-    const int64_t b = bag - (int64_t)f * p.B;
+    const int64_t total = (int64_t)p.R * p.F * p.B;
+    const int64_t nwarps = (int64_t)gridDim.x * kBagWarps;
+    int64_t bag = (int64_t)blockIdx.x * kBagWarps + (threadIdx.x >> 5);
+    if (bag >= total) return;
+    const int sub = lane / LPR, cl = lane % LPR;
+    int64_t s = p.offsets[bag], e = p.offsets[bag + 1];
+    int first_id = lane < (e - s) ? __ldg(p.ids + s + lane) : 0;
+
+    while (bag < total) {
+    const int64_t nbag = bag + nwarps;
+    int64_t ns = 0, ne = 0;
+    if (nbag < total) {
+        ns = p.offsets[nbag];
+        ne = p.offsets[nbag + 1];
+    }
+    const int64_t rf = bag / p.B;  // r * F + f
+    const int f = (int)(rf % p.F);
+    const int64_t b = (rf / p.F) * p.B + (bag - rf * p.B);  // output sample r*B + b
     const TT* __restrict__ table = static_cast<const TT*>(p.tables[f]);
     const int64_t rows = p.rows[f];
-    const int64_t s = p.offsets[bag], e = p.offsets[bag + 1];
-    const int sub = lane / LPR, cl = lane % LPR;
 
     float acc[CPL * EPC];
 #pragma unroll
@@ -114,7 +130,7 @@ __global__ void __launch_bounds__(kBagWarps * 32) bag_kernel(const BagParams p) 
 
     for (int64_t base = s; base < e; base += 32) {
         const int cnt = (int)((e - base) < 32 ? (e - base) : 32);
-        const int my_id = lane < cnt ? __ldg(p.ids + base + lane) : 0;
+        const int my_id = base == s ? first_id : (lane < cnt ? __ldg(p.ids + base + lane) : 0);
         for (int j = 0; j < cnt; j += RPP * U) {
             uint4 v[U][CPL];
             bool ok[U];
@@ -136,6 +152,8 @@ __global__ void __launch_bounds__(kBagWarps * 32) bag_kernel(const BagParams p) 
                 for (int c = 0; c < CPL; ++c) Elem<TT>::add(acc + c * EPC, v[u][c]);
         }
     }
+    // next bag's first ids (its offsets were requested before this bag's rows)
+    const int next_id = (nbag < total && lane < (ne - ns)) ? __ldg(p.ids + ns + lane) : 0;
     // fold the RPP row groups: lanes with equal cl end up with the full sum
 #pragma unroll
     for (int o = LPR; o < 32; o <<= 1)
@@ -158,18 +176,62 @@ __global__ void __launch_bounds__(kBagWarps * 32) bag_kernel(const BagParams p) 
 #pragma unroll
         for (int c = 0; c < CPL; ++c) store_out<OT, EPC>(dst + (c * LPR + cl) * EPC, acc + c * EPC);
     }
+    bag = nbag;
+    s = ns;
+    e = ne;
+    first_id = next_id;
+    }
+}
+
+template <typename K>
+unsigned persistent_grid(K kernel, int64_t bags) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBagWarps * 32, 0) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 4;
+    const int64_t want = (bags + kBagWarps - 1) / kBagWarps;
+    const int64_t cap = (int64_t)num_sms() * per_sm;
+    return (unsigned)(want < cap ? want : cap);
+}
+
+// Variant: 0 -> U=4 at 5 blocks/SM (40 warps), 1 -> U=8 at 3 blocks/SM (24 warps),
+// 2 -> U=8 at 4 blocks/SM. LATTICE_BAG_VARIANT overrides the default (tuning sweeps).
+int bag_variant(int row_bytes) {
+    static int forced = -2;
+    if (forced == -2) {
+        const char* e = std::getenv("LATTICE_BAG_VARIANT");
+        forced = e ? std::atoi(e) : -1;
+    }
+    if (forced >= 0 && forced <= 2) return forced;
+    (void)row_bytes;
+    return 1;  // measured best for fp32 and bf16 rows on B200 (scripts/bag_sweep.py)
+}
+
+template <typename TT, typename OT, int LPR, int CPL>
+void launch_one(const BagParams& p, cudaStream_t st, int row_bytes) {
+    const int64_t bags = (int64_t)p.R * p.F * p.B;
+    switch (bag_variant(row_bytes)) {
+        case 0:
+            bag_kernel<TT, OT, LPR, CPL, 4, 5>
+                <<<persistent_grid(bag_kernel<TT, OT, LPR, CPL, 4, 5>, bags), kBagWarps * 32, 0, st>>>(p);
+            break;
+        case 2:
+            bag_kernel<TT, OT, LPR, CPL, 8, 4>
+                <<<persistent_grid(bag_kernel<TT, OT, LPR, CPL, 8, 4>, bags), kBagWarps * 32, 0, st>>>(p);
+            break;
+        default:
+            bag_kernel<TT, OT, LPR, CPL, 8, 3>
+                <<<persistent_grid(bag_kernel<TT, OT, LPR, CPL, 8, 3>, bags), kBagWarps * 32, 0, st>>>(p);
+    }
 }
 
 template <typename TT, typename OT>
 lattice_status launch_bag(const BagParams& p, int row_bytes, cudaStream_t st) {
-    const int64_t bags = (int64_t)p.F * p.B;
-    const unsigned grid = (unsigned)((bags + kBagWarps - 1) / kBagWarps);
-    const int threads = kBagWarps * 32;
     switch (row_bytes) {
-        case 128: bag_kernel<TT, OT, 8, 1><<<grid, threads, 0, st>>>(p); break;
-        case 256: bag_kernel<TT, OT, 16, 1><<<grid, threads, 0, st>>>(p); break;
-        case 512: bag_kernel<TT, OT, 32, 1><<<grid, threads, 0, st>>>(p); break;
-        case 1024: bag_kernel<TT, OT, 32, 2><<<grid, threads, 0, st>>>(p); break;
+        case 128: launch_one<TT, OT, 8, 1>(p, st, row_bytes); break;
+        case 256: launch_one<TT, OT, 16, 1>(p, st, row_bytes); break;
+        case 512: launch_one<TT, OT, 32, 1>(p, st, row_bytes); break;
+        case 1024: launch_one<TT, OT, 32, 2>(p, st, row_bytes); break;
         default:
             return set_error(LATTICE_USAGE,
                              "embedding_bag: D * sizeof(table dtype) must be 128, 256, 512 or 1024 bytes");
@@ -223,6 +285,11 @@ __global__ void synth_ids_kernel(int64_t bags, int max_len, int64_t rows, uint64
             ids[j] = (int32_t)(gen_u64(seed, kTagId, (uint64_t)bag * max_len + (j - s)) %
                                (uint64_t)rows);
     }
+}
+
+__global__ void widen_kernel(int64_t n, const int32_t* __restrict__ in, int64_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[i];
 }
 
 __global__ void synth_dom_kernel(int64_t n, int G, uint64_t seed, int32_t* dom) {
@@ -363,7 +430,8 @@ lattice_status lattice_embedding_bag(const lattice_bag_args* a, lattice_stream s
     LAT_CUDA(cudaMallocAsync(&err, sizeof(*err), stream));
     LAT_CUDA(cudaMemsetAsync(err, 0xff, sizeof(*err), stream));
     BagParams p{a->features, a->batch, a->dim, a->tables, a->rows, a->offsets, a->ids, a->out,
-                a->out_row_stride, a->out_feature_offset, a->sample_pos, a->normalize, err};
+                a->out_row_stride, a->out_feature_offset, a->sample_pos, a->normalize, err,
+                a->sources > 1 ? a->sources : 1};
     lattice_status st;
     if (a->table_dtype == LATTICE_F32)
         st = a->out_dtype == LATTICE_F32 ? launch_bag<float, float>(p, row_bytes, stream)
@@ -391,6 +459,26 @@ lattice_status lattice_embedding_bag(const lattice_bag_args* a, lattice_stream s
         return set_error(LATTICE_DATA,
                          "embedding_bag: id at position " + std::to_string(host) + " is outside its table",
                          (int64_t)host);
+    return LATTICE_OK;
+}
+
+lattice_status lattice_lengths_to_offsets(int64_t n, const int32_t* lengths, int64_t* offsets,
+                                          lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(n >= 0 && offsets, "lengths_to_offsets: bad args");
+    if (n == 0) {
+        LAT_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int64_t), stream));
+        return LATTICE_OK;
+    }
+    LAT_REQUIRE(lengths != nullptr, "lengths_to_offsets: null lengths");
+    LAT_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int64_t), stream));
+    widen_kernel<<<grid_for(n, 256), 256, 0, stream>>>(n, lengths, offsets + 1);  // int64 accumulation
+    size_t tmp_bytes = 0;
+    LAT_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, offsets + 1, offsets + 1, n, stream));
+    void* tmp = nullptr;
+    LAT_CUDA(cudaMallocAsync(&tmp, tmp_bytes, stream));
+    LAT_CUDA(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, offsets + 1, offsets + 1, n, stream));
+    cudaFreeAsync(tmp, stream);
     return LATTICE_OK;
 }
 

@@ -240,6 +240,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             //      drains M tile `half`
             tc::mbar_wait(&f_full[rg], rph);
             tc::fence_after();
+            // every MMA reading this X stage has completed and this thread's residual reads are
+            // done: hand the stage back to the producer before the F pass
+            tc::mbar_arrive(&x_empty[st]);
             {
                 const bool has_tile = half < m_tiles;
                 const int r = half * 128 + row;
@@ -279,7 +282,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            tc::mbar_arrive(&x_empty[st]);
         }
     }
     tc::fence_before();

@@ -72,6 +72,24 @@ __global__ void pooled_norm_kernel(int64_t B, int n, int d, const T* __restrict_
     }
 }
 
+// table-wise shards [S][B][n/S][d] bf16 (already normalised by their owners) -> X0 rows
+// pos[b]; one warp per (b, f), 16-byte vectors
+__global__ void shard_gather_kernel(int64_t B, int n, int d, int S, const __nv_bfloat16* __restrict__ in,
+                                    const int32_t* __restrict__ pos, __nv_bfloat16* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int nl = n / S;
+    const int vec = d / 8;  // uint4 per row
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < B * n;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t b = w / n;
+        const int f = (int)(w - b * n);
+        const int o = f / nl, fl = f - o * nl;
+        const uint4* src = reinterpret_cast<const uint4*>(in + (((int64_t)o * B + b) * nl + fl) * d);
+        uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)pos[b] * n + f) * d);
+        for (int i = lane; i < vec; i += 32) dst[i] = src[i];
+    }
+}
+
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 }  // namespace
@@ -395,7 +413,13 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
         LAT_REQUIRE(batch->pooled != nullptr, "lattice_net_forward: need tables or pooled input");
         const int64_t warps = B * c.n;
         const unsigned grid = (unsigned)((warps * 32 + 255) / 256 < 148 * 64 ? (warps * 32 + 255) / 256 : 148 * 64);
-        if (batch->table_dtype == LATTICE_F32)
+        if (batch->pooled_layout == 1) {
+            LAT_REQUIRE(batch->shards >= 1 && c.n % batch->shards == 0 && batch->table_dtype == LATTICE_BF16,
+                        "lattice_net_forward: sharded pooled input needs bf16 and shards dividing n");
+            shard_gather_kernel<<<grid, 256, 0, stream>>>(B, c.n, c.d, batch->shards,
+                                                          static_cast<const __nv_bfloat16*>(batch->pooled),
+                                                          net->pos, net->X[0]);
+        } else if (batch->table_dtype == LATTICE_F32)
             pooled_norm_kernel<float><<<grid, 256, 0, stream>>>(B, c.n, c.d, static_cast<const float*>(batch->pooled),
                                                                net->pos, net->X[0]);
         else
