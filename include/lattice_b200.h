@@ -105,7 +105,17 @@ typedef struct {
     int32_t sources;             /* R >= 1: bags laid out [R][F][B] (after an ids all-to-all,
                                     R = source ranks); bag (r, f, b) writes output row r*B + b.
                                     0 is treated as 1. */
+    int64_t slice_cap;           /* > 0: ids of source r live in the fixed slice
+                                    ids[r*slice_cap ..] (static exchange buffer); offsets stay
+                                    the global CSR over [R][F][B], rebased per slice. */
 } lattice_bag_args;
+
+/* Sender side of the static ids exchange: out[o][j] = ids[bounds[o] + j] for
+ * j < bounds[o+1] - bounds[o] (o < slices); slices longer than cap set *overflow = 1.
+ * All sizes are read on the device: no host synchronisation. */
+lattice_status lattice_pack_slices(int32_t slices, const int64_t* bounds, const int32_t* ids,
+                                   int64_t cap, int32_t* out, int32_t* overflow,
+                                   lattice_stream stream);
 
 /* Exclusive prefix sum of bag lengths into CSR offsets (n+1 entries): the owner side of the
  * ids all-to-all rebuilds its offsets with this. */

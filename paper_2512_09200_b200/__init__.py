@@ -61,7 +61,8 @@ class BagArgs(ctypes.Structure):
     _fields_ = [("features", _I32), ("batch", _I64), ("dim", _I32), ("table_dtype", _I32),
                 ("tables", _P), ("rows", _P), ("offsets", _P), ("ids", _P), ("out_dtype", _I32),
                 ("out", _P), ("out_row_stride", _I64), ("out_feature_offset", _I32),
-                ("sample_pos", _P), ("normalize", _I32), ("check", _I32), ("sources", _I32)]
+                ("sample_pos", _P), ("normalize", _I32), ("check", _I32), ("sources", _I32),
+                ("slice_cap", _I64)]
 
 
 class GemmArgs(ctypes.Structure):
@@ -104,6 +105,7 @@ _sig("lattice_synth_bags", ctypes.c_int, [_I32, _I64, _I32, _I64, _U64, _P, _P, 
 _sig("lattice_synth_domains", ctypes.c_int, [_I64, _I32, _U64, _P, _P])
 _sig("lattice_domain_bucket", ctypes.c_int, [_I64, _I32, _P, _P, _P, _P, _P])
 _sig("lattice_lengths_to_offsets", ctypes.c_int, [_I64, _P, _P, _P])
+_sig("lattice_pack_slices", ctypes.c_int, [_I32, _P, _P, _I64, _P, _P, _P])
 _sig("lattice_gemm", ctypes.c_int, [ctypes.POINTER(GemmArgs), _P])
 _sig("lattice_net_create", ctypes.c_int, [ctypes.POINTER(NetConfig), ctypes.POINTER(_P)])
 _sig("lattice_net_destroy", None, [_P])
@@ -117,7 +119,7 @@ EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_versio
            "lattice_stable_hash", "lattice_zipper_validate", "lattice_zipper_assign_labels",
            "lattice_embedding_bag", "lattice_rownorm", "lattice_fill_tables",
            "lattice_fill_weights", "lattice_synth_bags", "lattice_synth_domains",
-           "lattice_domain_bucket", "lattice_lengths_to_offsets", "lattice_gemm",
+           "lattice_domain_bucket", "lattice_lengths_to_offsets", "lattice_pack_slices", "lattice_gemm",
            "lattice_net_create", "lattice_net_destroy",
            "lattice_net_weight", "lattice_net_forward", "lattice_net_set_timing",
            "lattice_net_stage_times"]
@@ -187,7 +189,7 @@ def stable_hash(bytes_, off, seed, stream=None):
 
 def embedding_bag(tables, offsets, ids, batch, out=None, out_dtype=None, sample_pos=None,
                   normalize=False, out_row_stride=None, out_feature_offset=0, check_errors=True,
-                  stream=None, table_ptrs=None, rows=None, sources=1):
+                  stream=None, table_ptrs=None, rows=None, sources=1, slice_cap=0):
     """Sum-pooled embedding bags. tables: list of [rows_f, D] CUDA tensors (f32 or bf16).
     offsets int64 [R*F*B+1] CSR with bags laid out [R][F][B] (R = sources, 1 = plain
     feature-major), ids int32. Returns out [R*B, F, D]."""
@@ -207,7 +209,7 @@ def embedding_bag(tables, offsets, ids, batch, out=None, out_dtype=None, sample_
     a = BagArgs(F, batch, D, F32 if tdt == torch.float32 else BF16, _p(table_ptrs), _p(rows),
                 _p(offsets), _p(ids), F32 if odt == torch.float32 else BF16, _p(out), stride,
                 out_feature_offset, _p(sample_pos), 1 if normalize else 0, 1 if check_errors else 0,
-                sources)
+                sources, slice_cap)
     check(_lib.lattice_embedding_bag(ctypes.byref(a), _stream(stream)))
     return out
 
@@ -219,6 +221,13 @@ def lengths_to_offsets(lengths, out=None, stream=None):
     if out is None:
         out = torch.empty(n + 1, dtype=torch.int64, device=lengths.device)
     check(_lib.lattice_lengths_to_offsets(n, _p(lengths), _p(out), _stream(stream)))
+    return out
+
+
+def pack_slices(bounds, ids, cap, out, overflow, stream=None):
+    """out[o][j] = ids[bounds[o] + j] for the W = len(bounds)-1 slices; sizes read on device."""
+    check(_lib.lattice_pack_slices(bounds.numel() - 1, _p(bounds), _p(ids), cap, _p(out), _p(overflow),
+                                   _stream(stream)))
     return out
 
 

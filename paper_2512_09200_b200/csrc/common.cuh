@@ -127,8 +127,8 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 // numerics.hpp:29-33 in fp32. exp(-|z|) form keeps it stable for both signs.
 __device__ __forceinline__ float stable_sigmoid(float z) {
-    const float e = __expf(-fabsf(z));
-    const float s = 1.0f / (1.0f + e);
+    const float e = __expf(-fabsf(z));        // in (0, 1]: no overflow for any z
+    const float s = __fdividef(1.0f, 1.0f + e);  // MUFU reciprocal; ~2 ulp, far below bf16
     return z >= 0.0f ? s : 1.0f - s;
 }
 __device__ __forceinline__ float act_swish(float r, bool hard) {

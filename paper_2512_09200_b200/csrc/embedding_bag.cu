@@ -34,7 +34,21 @@ struct BagParams {
     int32_t normalize;
     unsigned long long* err;
     int32_t R;  // source ranks: bags laid out [R][F][B]
+    int64_t slice_cap;  // > 0: source r's ids start at r * slice_cap (static exchange buffer)
+    unsigned long long* counter;  // work-claim counter (zeroed per launch)
 };
+
+// [s, e) of bag `bag` in the ids array (CSR, or CSR rebased into fixed per-source slices)
+__device__ __forceinline__ void bag_range(const BagParams& p, int64_t bag, int64_t& s, int64_t& e) {
+    s = p.offsets[bag];
+    e = p.offsets[bag + 1];
+    if (p.slice_cap > 0) {
+        const int64_t r = bag / ((int64_t)p.F * p.B);
+        const int64_t shift = r * p.slice_cap - p.offsets[r * p.F * p.B];
+        s += shift;
+        e += shift;
+    }
+}
 
 __device__ __forceinline__ uint4 ld_stream(const void* p) {
     uint4 r;
@@ -95,29 +109,42 @@ __device__ __forceinline__ void store_out<__nv_bfloat16, 8>(__nv_bfloat16* dst, 
 
 constexpr int kBagWarps = 8;
 
-// Persistent: each warp walks bags bag0, bag0 + nwarps, ... While the current bag's rows are
-// in flight, the next bag's offsets and first 32 ids are already being fetched, so the
-// offsets -> ids -> rows dependency chain of one bag overlaps the row traffic of the previous.
+// Persistent warps with dynamic scheduling: a warp claims kChunk consecutive bags at a time
+// from a global counter, so all warps stay inside a narrow window of the bag sequence -- the
+// sequence is table-major, so the live working set is about one table and repeated rows hit
+// in L2 instead of re-reading HBM. While the current bag's rows are in flight, the next bag's
+// offsets and first 32 ids are already being fetched, so the offsets -> ids -> rows chain of
+// one bag overlaps the row traffic of the previous one.
+constexpr int kChunk = 4;
+
+__device__ __forceinline__ int64_t claim_chunk(unsigned long long* counter, int lane) {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(counter, 1ull);
+    return (int64_t)__shfl_sync(0xffffffffu, c, 0) * kChunk;
+}
+
 template <typename TT, typename OT, int LPR, int CPL, int U, int MINB>
 __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagParams p) {
     constexpr int EPC = Elem<TT>::kPerChunk;
     constexpr int RPP = 32 / LPR;  // rows per pass; U passes in flight
     const int lane = threadIdx.x & 31;
     const int64_t total = (int64_t)p.R * p.F * p.B;
-    const int64_t nwarps = (int64_t)gridDim.x * kBagWarps;
-    int64_t bag = (int64_t)blockIdx.x * kBagWarps + (threadIdx.x >> 5);
+    int64_t bag = claim_chunk(p.counter, lane);
     if (bag >= total) return;
+    int64_t chunk_end = bag + kChunk < total ? bag + kChunk : total;
     const int sub = lane / LPR, cl = lane % LPR;
-    int64_t s = p.offsets[bag], e = p.offsets[bag + 1];
+    int64_t s, e;
+    bag_range(p, bag, s, e);
     int first_id = lane < (e - s) ? __ldg(p.ids + s + lane) : 0;
 
     while (bag < total) {
-    const int64_t nbag = bag + nwarps;
-    int64_t ns = 0, ne = 0;
-    if (nbag < total) {
-        ns = p.offsets[nbag];
-        ne = p.offsets[nbag + 1];
+    int64_t nbag = bag + 1;
+    if (nbag >= chunk_end) {
+        nbag = claim_chunk(p.counter, lane);
+        chunk_end = nbag + kChunk < total ? nbag + kChunk : total;
     }
+    int64_t ns = 0, ne = 0;
+    if (nbag < total) bag_range(p, nbag, ns, ne);
     const int64_t rf = bag / p.B;  // r * F + f
     const int f = (int)(rf % p.F);
     const int64_t b = (rf / p.F) * p.B + (bag - rf * p.B);  // output sample r*B + b
@@ -203,8 +230,7 @@ int bag_variant(int row_bytes) {
         forced = e ? std::atoi(e) : -1;
     }
     if (forced >= 0 && forced <= 2) return forced;
-    (void)row_bytes;
-    return 1;  // measured best for fp32 and bf16 rows on B200 (scripts/bag_sweep.py)
+    return row_bytes >= 512 ? 0 : 2;  // measured on B200 (scripts/bag_sweep.py, profiles/r01)
 }
 
 template <typename TT, typename OT, int LPR, int CPL>
@@ -284,6 +310,23 @@ __global__ void synth_ids_kernel(int64_t bags, int max_len, int64_t rows, uint64
         for (int64_t j = s + lane; j < e; j += 32)
             ids[j] = (int32_t)(gen_u64(seed, kTagId, (uint64_t)bag * max_len + (j - s)) %
                                (uint64_t)rows);
+    }
+}
+
+__global__ void pack_slices_kernel(int S, const int64_t* __restrict__ bounds, const int32_t* __restrict__ ids,
+                                   int64_t cap, int32_t* __restrict__ out, int32_t* __restrict__ overflow) {
+    for (int o = blockIdx.y; o < S; o += gridDim.y) {
+        const int64_t b0 = bounds[o];
+        int64_t cnt = bounds[o + 1] - b0;
+        if (cnt > cap) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) *overflow = 1;
+            cnt = cap;
+        }
+        int32_t* dst = out + (int64_t)o * cap;
+        const int32_t* src = ids + b0;
+        for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cnt;
+             j += (int64_t)gridDim.x * blockDim.x)
+            dst[j] = src[j];
     }
 }
 
@@ -426,12 +469,13 @@ lattice_status lattice_embedding_bag(const lattice_bag_args* a, lattice_stream s
     LAT_REQUIRE(out_chunk == 8 || out_chunk == 16 || out_chunk == 32,
                 "embedding_bag: unsupported dtype combination");
 
-    unsigned long long* err = nullptr;
-    LAT_CUDA(cudaMallocAsync(&err, sizeof(*err), stream));
+    unsigned long long* err = nullptr;  // [0] first bad id (init ~0), [1] work-claim counter (init 0)
+    LAT_CUDA(cudaMallocAsync(&err, 2 * sizeof(*err), stream));
     LAT_CUDA(cudaMemsetAsync(err, 0xff, sizeof(*err), stream));
+    LAT_CUDA(cudaMemsetAsync(err + 1, 0, sizeof(*err), stream));
     BagParams p{a->features, a->batch, a->dim, a->tables, a->rows, a->offsets, a->ids, a->out,
                 a->out_row_stride, a->out_feature_offset, a->sample_pos, a->normalize, err,
-                a->sources > 1 ? a->sources : 1};
+                a->sources > 1 ? a->sources : 1, a->slice_cap > 0 ? a->slice_cap : 0, err + 1};
     lattice_status st;
     if (a->table_dtype == LATTICE_F32)
         st = a->out_dtype == LATTICE_F32 ? launch_bag<float, float>(p, row_bytes, stream)
@@ -459,6 +503,16 @@ lattice_status lattice_embedding_bag(const lattice_bag_args* a, lattice_stream s
         return set_error(LATTICE_DATA,
                          "embedding_bag: id at position " + std::to_string(host) + " is outside its table",
                          (int64_t)host);
+    return LATTICE_OK;
+}
+
+lattice_status lattice_pack_slices(int32_t slices, const int64_t* bounds, const int32_t* ids, int64_t cap,
+                                   int32_t* out, int32_t* overflow, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(slices > 0 && cap > 0 && bounds && ids && out && overflow, "pack_slices: bad args");
+    dim3 grid((unsigned)(num_sms() * 4 / slices > 0 ? num_sms() * 4 / slices : 1), (unsigned)slices);
+    pack_slices_kernel<<<grid, 256, 0, stream>>>(slices, bounds, ids, cap, out, overflow);
+    LAT_CUDA(cudaGetLastError());
     return LATTICE_OK;
 }
 

@@ -51,22 +51,27 @@ __device__ __forceinline__ void store_row32(const Params& p, int64_t m, int n, c
     }
 }
 
-// Sum a per-row partial across the cluster (rank order) through DSMEM. Every epilogue thread
-// of every CTA in the cluster calls this once per tile with its own row; `slot` alternates
-// with the tile so a fast CTA can run one tile ahead without clobbering a slow one.
-__device__ __forceinline__ float cluster_row_sum(float part, int row, int C, float* xbuf,
+// Sum a per-row partial across the cluster (rank order) through DSMEM, pull model: each CTA
+// writes its partials to its own slot, every warp then announces "my 32 rows are ready" with
+// ONE release arrive per peer CTA (4 warps x C peers per barrier phase), waits on its own
+// barrier (CTA-scope spin, one cluster acquire fence after), and reads the C peers' partials
+// with ld.shared::cluster. `xbuf` alternates with the tile so a fast CTA can run one tile
+// ahead: it only rewrites a slot after every peer arrived for the tile in between, i.e.
+// after they finished reading that slot.
+__device__ __forceinline__ float cluster_row_sum(float part, int row, int lane, int C, float* xbuf,
                                                  uint64_t* xbar, uint32_t phase) {
     if (C == 1) return part;
-    const uint32_t my = tc::cluster_rank();
-    const uint32_t local = tc::smem_u32(&xbuf[my * BM + row]);
-    const uint32_t bar = tc::smem_u32(xbar);
-    for (int r = 0; r < C; ++r) {
-        tc::st_cluster_f32(tc::mapa(local, r), part);
-        tc::mbar_arrive_remote(tc::mapa(bar, r));
+    xbuf[row] = part;
+    __syncwarp();
+    if (lane == 0) {
+        const uint32_t bar = tc::smem_u32(xbar);
+        for (int r = 0; r < C; ++r) tc::mbar_arrive_remote(tc::mapa(bar, r));
     }
-    tc::mbar_wait_cluster(xbar, phase);
+    tc::mbar_wait(xbar, phase);
+    tc::fence_acq_rel_cluster();
+    const uint32_t local = tc::smem_u32(&xbuf[row]);
     float s = 0.0f;
-    for (int r = 0; r < C; ++r) s += xbuf[r * BM + row];
+    for (int r = 0; r < C; ++r) s += tc::ld_cluster_f32(tc::mapa(local, r));
     return s;
 }
 
@@ -186,8 +191,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&tfull[i], 1);
             tc::mbar_init(&tempty[i], BM);
-            tc::mbar_init(&xbar[i], BM * C);
-            tc::mbar_init(&hbar[i], BM * C);
+            tc::mbar_init(&xbar[i], 4 * C);  // one arrive per epilogue warp per CTA
+            tc::mbar_init(&hbar[i], 4 * C);  // one arrive per epilogue warp per CTA
         }
         tc::fence_mbar_init();
     }
@@ -289,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) ss += (n0 + c + j < p.N) ? v[j] * v[j] : 0.0f;
                 }
-                const float total = cluster_row_sum(ss, row, C, xbuf + acc * kMaxCluster * BM, &xbar[acc], ph);
+                const float total = cluster_row_sum(ss, row, lane, C, xbuf + acc * BM, &xbar[acc], ph);
                 const float inv = 1.0f / sqrtf(total / (float)p.N_full + 1e-6f);
                 if (epi == kSwish || epi == kSwishHard) {
 #pragma unroll 1
@@ -336,24 +341,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     tc::fence_before();
                     tc::mbar_arrive(&tempty[acc]);
-                    // reduce head partials into cluster rank 0 (rank order), then write
-                    float* hb = hbuf + (size_t)acc * C * p.heads * BM;
+                    // reduce head partials into cluster rank 0 (rank order), pull model: every
+                    // CTA parks its partials in its own slot, each warp signals rank 0 once,
+                    // rank 0 reads the peers' slots through DSMEM
+                    float* hb = hbuf + (size_t)acc * p.heads * BM;
                     if (C > 1) {
 #pragma unroll
                         for (int h = 0; h < kMaxHeads; ++h)
-                            if (h < p.heads)
-                                tc::st_cluster_f32(tc::mapa(tc::smem_u32(&hb[(rank * p.heads + h) * BM + row]), 0),
-                                                   part[h]);
-                        tc::mbar_arrive_remote(tc::mapa(tc::smem_u32(&hbar[acc]), 0));
+                            if (h < p.heads) hb[h * BM + row] = part[h];
+                        __syncwarp();
+                        if (lane == 0) tc::mbar_arrive_remote(tc::mapa(tc::smem_u32(&hbar[acc]), 0));
                     }
                     if (rank == 0) {
                         if (C > 1) {
-                            tc::mbar_wait_cluster(&hbar[acc], ph);
+                            tc::mbar_wait(&hbar[acc], ph);
+                            tc::fence_acq_rel_cluster();
 #pragma unroll
                             for (int h = 0; h < kMaxHeads; ++h) {
                                 if (h < p.heads) {
+                                    const uint32_t la = tc::smem_u32(&hb[h * BM + row]);
                                     float sum = 0.0f;
-                                    for (int r = 0; r < C; ++r) sum += hb[(r * p.heads + h) * BM + row];
+                                    for (int r = 0; r < C; ++r) sum += tc::ld_cluster_f32(tc::mapa(la, r));
                                     part[h] = sum;
                                 }
                             }
@@ -405,11 +413,7 @@ lattice_status launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Para
     }
     if (smem > 227 * 1024) return set_error(LATTICE_USAGE, "gemm: shared memory budget exceeded");
     const int C = p.cluster;
-    int clusters = num_sms() / C;
-    if (clusters > units) clusters = units;
-    if (clusters < 1) clusters = 1;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(clusters * C, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -420,6 +424,20 @@ lattice_status launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Para
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    // persistent grid = the clusters that can be co-resident (GPC sizes limit clusters of 8 to
+    // 16 per B200); a larger grid would serialise whole clusters behind the first wave
+    static int max_clusters[kMaxCluster + 1] = {0};
+    if (!max_clusters[C]) {
+        cfg.gridDim = dim3(C * (num_sms() / C), 1, 1);
+        int mc = 0;
+        if (cudaOccupancyMaxActiveClusters(&mc, gemm_kernel<STAGES>, &cfg) != cudaSuccess || mc < 1)
+            mc = num_sms() / C;
+        max_clusters[C] = mc;
+    }
+    int clusters = max_clusters[C];
+    if (clusters > units) clusters = units;
+    if (clusters < 1) clusters = 1;
+    cfg.gridDim = dim3(clusters * C, 1, 1);
     LAT_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<STAGES>, ta, tb, p));
     return LATTICE_OK;
 }

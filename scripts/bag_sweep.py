@@ -3,7 +3,7 @@ import os, subprocess, sys, json
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-def one(F, R, D, B, dt, variant):
+def one(F, R, D, B, dt, variant, net_like=False):
     code = f"""
 import os, sys, torch, json
 sys.path.insert(0, {ROOT!r})
@@ -15,11 +15,12 @@ ptrs = torch.tensor([t.data_ptr() for t in tables], dtype=torch.int64, device='c
 rows = torch.full(({F},), {R}, dtype=torch.int64, device='cuda')
 off, ids = L.synth_bags({F}, {B}, 40, {R}, 0x1A78)
 out = torch.empty(({B}, {F}, {D}), dtype=dt, device='cuda')
-for _ in range(3): L.embedding_bag(tables, off, ids, {B}, out=out, check_errors=False, table_ptrs=ptrs, rows=rows)
+pos = torch.randperm({B}, device='cuda').to(torch.int32) if {net_like} else None
+for _ in range(3): L.embedding_bag(tables, off, ids, {B}, out=out, check_errors=False, table_ptrs=ptrs, rows=rows, sample_pos=pos, normalize={net_like})
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-for _ in range(20): L.embedding_bag(tables, off, ids, {B}, out=out, check_errors=False, table_ptrs=ptrs, rows=rows)
+for _ in range(20): L.embedding_bag(tables, off, ids, {B}, out=out, check_errors=False, table_ptrs=ptrs, rows=rows, sample_pos=pos, normalize={net_like})
 e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 20
 n = int(off[-1]); s = tab.element_size()
@@ -35,3 +36,5 @@ for name, cfg in [("micro_f32", (64, 1000000, 128, 16384, "float32")),
                   ("mid_bf16", (256, 100000, 128, 32768, "bfloat16"))]:
     for v in (0, 1, 2):
         print(name, "variant", v, one(*cfg, v), flush=True)
+for v in (0, 1, 2):
+    print("mid_bf16 normalize+pos variant", v, one(256, 100000, 128, 32768, "bfloat16", v, True), flush=True)

@@ -28,15 +28,16 @@ def _free_port():
 
 def _oracle_pool(Fl, owned0, W, B):
     """pool_fn stand-in: [src][f_local][b] bags -> [W*B][Fl][D] normalised (fp32 here)."""
-    def fn(recv_off, recv_ids):
+    def fn(recv_off, recv_ids, slice_cap):
         off = recv_off.numpy()
         ids = recv_ids.numpy()
         out = np.zeros((W * B, Fl, D), np.float32)
         for r in range(W):
+            shift = r * slice_cap - off[r * Fl * B] if slice_cap else 0
             for fl in range(Fl):
                 for b in range(B):
                     bag = (r * Fl + fl) * B + b
-                    for j in range(off[bag], off[bag + 1]):
+                    for j in range(off[bag] + shift, off[bag + 1] + shift):
                         for c in range(D):
                             out[r * B + b, fl, c] += oracle.load_oracle().lo_table_value(
                                 SEED_T, owned0 + fl, int(ids[j]), D, ROWS, c)
@@ -54,10 +55,18 @@ def _worker(rank, world, port, q, capacity):
         from paper_2512_09200_b200.sharded import ShardedBags  # noqa: E402  (no CUDA needed)
         sb = ShardedBags(F, B, D, world, rank, capacity=capacity)
         off, ids = oracle.synth_bags(F, B, MAXLEN, ROWS, 0x1A78 + rank)
-        recv_off, recv_ids = sb.exchange_ids(torch.from_numpy(off), torch.from_numpy(ids.astype(np.int32)),
-                                             scan_fn=lambda l: torch.cat([torch.zeros(1, dtype=torch.int64),
-                                                                          torch.cumsum(l.to(torch.int64), 0)]))
-        send = sb.pool(recv_off, recv_ids, pool_fn=_oracle_pool(sb.Fl, sb.owned()[0], world, B))
+        def pack(bounds, ids_, cap, out, overflow):  # CPU stand-in for lattice_pack_slices
+            for o in range(world):
+                n = int(bounds[o + 1] - bounds[o])
+                overflow |= int(n > cap)
+                out[o, :min(n, cap)] = ids_[int(bounds[o]): int(bounds[o]) + min(n, cap)]
+
+        recv_off, recv_ids, cap = sb.exchange_ids(
+            torch.from_numpy(off), torch.from_numpy(ids.astype(np.int32)),
+            scan_fn=lambda l: torch.cat([torch.zeros(1, dtype=torch.int64), torch.cumsum(l.to(torch.int64), 0)]),
+            pack_fn=pack)
+        send = sb.pool(recv_off, recv_ids, cap, pool_fn=_oracle_pool(sb.Fl, sb.owned()[0], world, B))
+        sb.check_overflow()
         recv = sb.exchange_pooled(send)
         # expected: oracle pooling of this rank's own batch over all F features, normalised
         full, _ = oracle.embedding_bag_synth(SEED_T, F, ROWS, D, B, off, ids)
