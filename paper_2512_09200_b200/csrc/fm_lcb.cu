@@ -13,9 +13,10 @@
 // W_L and Y stay resident in shared memory for the whole persistent CTA. P goes TMEM ->
 // registers -> bf16 -> swizzled shared memory to become F's B operand.
 //
-// Warp roles: 0 TMA producer, 1 MMA issuer, 2-9 epilogue. Each TMEM lane quarter is
-// drained by two epilogue warps that split the columns (P, L) or the M tiles (F), so every
-// SM sub-partition runs two epilogue warps. TMEM holds two accumulator regions
+// Warp roles: 0 TMA producer, 1 MMA issuer, 2-5 LCB group (thread = L row: residual +
+// rms_norm_d, no cross-warp reduction), 6-9 FM group (P -> Pbuf, then the n*k-wide norm of
+// F with one 4-warp named barrier). The two groups run independently, so every SM
+// sub-partition has two epilogue warps in flight. TMEM holds two accumulator regions
 // {P | L | F}: the MMAs of sample s+1 run while sample s's epilogue drains the other region,
 // and X stages are double-buffered so loads run two samples ahead. The epilogue is the
 // critical path; values stay in registers between the sum-of-squares and the normalise pass.
@@ -44,11 +45,13 @@ __device__ __forceinline__ int region_cols(const Params& p) {
     return 64 + p.d + ((p.n_pad + 127) / 128) * p.k_pad;
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __maxnreg__(200)  // 320 threads, 1 CTA/SM: up to 200 registers per thread
     fm_lcb_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWL,
                   const __grid_constant__ CUtensorMap tmYT, const Params p) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align to 1024 B (SW128) by offsetting the __shared__ pointer itself, so the compiler keeps
+    // the shared address space (LDS/STS rather than generic loads)
+    uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int npad = p.n_pad, kpad = p.k_pad, d = p.d;
     const int panels_d = d / 64, panels_n = (npad + 63) / 64;
     // An X stage always spans 2 panels of >= 128 rows so that every M=128 operand view
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_init(&tmem_empty[i], kEpiThreads);
         }
         tc::mbar_init(w_full, 1);
-        tc::mbar_init(pbuf_full, kEpiThreads);
+        tc::mbar_init(pbuf_full, 128);  // the FM group
         tc::fence_mbar_init();
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, tcols);
@@ -163,31 +166,90 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::mma_commit(&f_full[rg]);
             }
         }
-    } else {  // ---- epilogue warps 2..9
-        const int e = warp - 2;
-        const int q = warp & 3;        // TMEM lane quarter this warp may access
-        const int half = e >> 2;       // which column half / M tile
-        const int row = q * 32 + lane; // TMEM lane
+    } else if (warp < 6) {  // ---- LCB group, warps 2..5: thread = L row, all d columns
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        const float inv_nk = 1.0f / (float)(p.n * p.k), inv_d = 1.0f / (float)d;
+        const float inv_d = 1.0f / (float)d;
+        const int xr = p.nF + row;
+        const bool live = row < p.nL;
         int it = 0;
         for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
             const int st = it & 1;
             const int rg = nreg == 2 ? (it & 1) : 0;
             const uint32_t rph = nreg == 2 ? ((it >> 1) & 1) : (it & 1);
-            const uint32_t t_P = tmem + rg * 256 + lane_off, t_L = t_P + 64, t_F = t_L + d;
+            const uint32_t t_L = tmem + rg * 256 + lane_off + 64;
             const uint8_t* xs = sX + st * xstage;
+            // pick up the residual row X[nF+row] as soon as the stage lands, so the stage can
+            // be recycled right after the MMAs (the producer runs two samples ahead)
+            tc::mbar_wait(&x_full[st], (it >> 1) & 1);
+            uint4 res[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                res[j] = (live && j * 8 < d) ? *reinterpret_cast<const uint4*>(xs + (j / 8) * xpanel + swz(xr, (j * 8) & 63))
+                                             : make_uint4(0, 0, 0, 0);
+            tc::mbar_arrive(&x_empty[st]);
             tc::mbar_wait(&pl_full[rg], rph);
             tc::fence_after();
-            // ---- P row `row` (= d index), 16-column chunks split across the two halves,
-            //      -> bf16 -> Pbuf[j][row] (K-major B operand of F). One Pbuf suffices: this
-            //      sample's writes start after the previous sample's F MMAs completed.
-            uint8_t* pbuf = sP;
-            for (int c0 = 16 * half; c0 < kpad; c0 += 32) {
+            // X'[nF+row] = rms_norm_d(L[row] + X[nF+row])
+            float v[128];
+            tc::tmem_ld32(t_L, v);
+            tc::tmem_ld32(t_L + 32, v + 32);
+            if (d == 128) {
+                tc::tmem_ld32(t_L + 64, v + 64);
+                tc::tmem_ld32(t_L + 96, v + 96);
+            }
+            tc::fence_before();
+            tc::mbar_arrive(&tmem_empty[rg]);
+            float ss = 0.0f;
+            if (live) {
+#pragma unroll
+                for (int j = 0; j < 128; j += 8) {
+                    if (j < d) {
+                        const uint4 r = res[j / 8];
+                        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            v[j + 2 * i] += bf16_lo(w[i]);
+                            v[j + 2 * i + 1] += bf16_hi(w[i]);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) ss += v[j + i] * v[j + i];
+                    }
+                }
+            }
+            if (live) {
+                const float inv = 1.0f / sqrtf(ss * inv_d + 1e-6f);
+                __nv_bfloat16* dst = p.Xout + (b * p.n + xr) * (int64_t)d;
+#pragma unroll
+                for (int j = 0; j < 128; j += 8)
+                    if (j < d)
+                        *reinterpret_cast<uint4*>(dst + j) =
+                            make_uint4(pack_bf16x2(v[j] * inv, v[j + 1] * inv), pack_bf16x2(v[j + 2] * inv, v[j + 3] * inv),
+                                       pack_bf16x2(v[j + 4] * inv, v[j + 5] * inv), pack_bf16x2(v[j + 6] * inv, v[j + 7] * inv));
+            }
+        }
+    } else {  // ---- FM group, warps 6..9: P -> Pbuf, then Fin = rms_norm(flatten(X P))
+        const int q = warp & 3;
+        const int e = warp - 6;
+        const int row = q * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const float inv_nk = 1.0f / (float)(p.n * p.k);
+        int it = 0;
+        for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
+            const int st = it & 1;
+            const int rg = nreg == 2 ? (it & 1) : 0;
+            const uint32_t rph = nreg == 2 ? ((it >> 1) & 1) : (it & 1);
+            const uint32_t t_P = tmem + rg * 256 + lane_off, t_F = t_P + 64 + d;
+            tc::mbar_wait(&pl_full[rg], rph);
+            tc::fence_after();
+            // P row `row` (= d index) -> bf16 -> Pbuf[j][row], the K-major B operand of F. One
+            // Pbuf suffices: this sample's writes start after the previous F MMAs completed.
+            for (int c0 = 0; c0 < kpad; c0 += 16) {
                 float v[16];
                 tc::tmem_ld16(t_P + c0, v);
                 if (row < d) {
-                    uint8_t* pan = pbuf + (row / 64) * ppanel;
+                    uint8_t* pan = sP + (row / 64) * ppanel;
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
                         *reinterpret_cast<__nv_bfloat16*>(pan + swz(c0 + j, row & 63)) = __float2bfloat16_rn(v[j]);
@@ -195,90 +257,46 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tc::fence_async_shared();
             tc::mbar_arrive(pbuf_full);
-            // ---- LCB half: X'[nF+row] = rms_norm_d(L[row] + X[nF+row]); this warp owns
-            //      columns [half*d/2, (half+1)*d/2)
-            {
-                const int xr = p.nF + row;
-                const bool live = row < p.nL;
-                const int cbase = half * (d / 2);
-                float v[64];
-                tc::tmem_ld32(t_L + cbase, v);
-                if (d == 128) tc::tmem_ld32(t_L + cbase + 32, v + 32);
-                float ss = 0.0f;
-                if (live) {
-#pragma unroll
-                    for (int j = 0; j < 64; j += 8) {
-                        if (j < d / 2) {
-                            const int c = cbase + j;
-                            const uint4 r = *reinterpret_cast<const uint4*>(xs + (c / 64) * xpanel + swz(xr, c & 63));
-                            const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                v[j + 2 * i] += bf16_lo(w[i]);
-                                v[j + 2 * i + 1] += bf16_hi(w[i]);
-                            }
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) ss += v[j + i] * v[j + i];
-                        }
-                    }
-                }
-                red_l[half * 128 + row] = ss;
-                tc::named_bar(1, kEpiThreads);
-                const float total = red_l[row] + red_l[128 + row];
-                const float inv = 1.0f / sqrtf(total * inv_d + 1e-6f);
-                if (live) {
-                    __nv_bfloat16* dst = p.Xout + (b * p.n + xr) * (int64_t)d + cbase;
-#pragma unroll
-                    for (int j = 0; j < 64; j += 8)
-                        if (j < d / 2)
-                            *reinterpret_cast<uint4*>(dst + j) =
-                                make_uint4(pack_bf16x2(v[j] * inv, v[j + 1] * inv), pack_bf16x2(v[j + 2] * inv, v[j + 3] * inv),
-                                           pack_bf16x2(v[j + 4] * inv, v[j + 5] * inv), pack_bf16x2(v[j + 6] * inv, v[j + 7] * inv));
-                }
-            }
-            // ---- FM: Fin = rms_norm(flatten(X P)) over the n*k real entries; this warp
-            //      drains M tile `half`
             tc::mbar_wait(&f_full[rg], rph);
             tc::fence_after();
-            // every MMA reading this X stage has completed and this thread's residual reads are
-            // done: hand the stage back to the producer before the F pass
-            tc::mbar_arrive(&x_empty[st]);
-            {
-                const bool has_tile = half < m_tiles;
-                const int r = half * 128 + row;
-                float v[64];
-                float ss = 0.0f;
-                if (has_tile) {
-                    tc::tmem_ld32(t_F + half * kpad, v);
-                    if (kpad > 32) tc::tmem_ld32(t_F + half * kpad + 32, v + 32);
-                    if (r < p.n) {
+            tc::mbar_arrive(&x_empty[st]);  // every MMA reading this X stage has completed
+            float v[2][64];
+            float ss = 0.0f;
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                if (mt < m_tiles) {
+                    tc::tmem_ld32(t_F + mt * kpad, v[mt]);
+                    if (kpad > 32) tc::tmem_ld32(t_F + mt * kpad + 32, v[mt] + 32);
+                    if (mt * 128 + row < p.n) {
 #pragma unroll
                         for (int j = 0; j < 64; ++j)
-                            if (j < p.k) ss += v[j] * v[j];
+                            if (j < p.k) ss += v[mt][j] * v[mt][j];
                     }
                 }
-                tc::fence_before();
-                tc::mbar_arrive(&tmem_empty[rg]);  // this thread's TMEM reads of the region are done
-                ss = warp_sum(ss);
-                if (lane == 0) red_f[e] = ss;
-                tc::named_bar(1, kEpiThreads);
-                float total = 0.0f;
+            }
+            tc::fence_before();
+            tc::mbar_arrive(&tmem_empty[rg]);
+            ss = warp_sum(ss);
+            float* red = red_f + (it & 1) * 4;  // parity-buffered: no reuse race across samples
+            if (lane == 0) red[e] = ss;
+            tc::named_bar(2, 128);
+            const float inv = 1.0f / sqrtf((red[0] + red[1] + red[2] + red[3]) * inv_nk + 1e-6f);
 #pragma unroll
-                for (int i = 0; i < kEpiWarps; ++i) total += red_f[i];
-                const float inv = 1.0f / sqrtf(total * inv_nk + 1e-6f);
-                if (has_tile && r < p.n) {
+            for (int mt = 0; mt < 2; ++mt) {
+                const int r = mt * 128 + row;
+                if (mt < m_tiles && r < p.n) {
                     __nv_bfloat16* dst = p.Fout + b * (int64_t)p.n * p.k + (int64_t)r * p.k;
                     if ((p.k & 7) == 0) {
 #pragma unroll
                         for (int j = 0; j < 64; j += 8)
                             if (j < p.k)
                                 *reinterpret_cast<uint4*>(dst + j) = make_uint4(
-                                    pack_bf16x2(v[j] * inv, v[j + 1] * inv), pack_bf16x2(v[j + 2] * inv, v[j + 3] * inv),
-                                    pack_bf16x2(v[j + 4] * inv, v[j + 5] * inv), pack_bf16x2(v[j + 6] * inv, v[j + 7] * inv));
+                                    pack_bf16x2(v[mt][j] * inv, v[mt][j + 1] * inv), pack_bf16x2(v[mt][j + 2] * inv, v[mt][j + 3] * inv),
+                                    pack_bf16x2(v[mt][j + 4] * inv, v[mt][j + 5] * inv), pack_bf16x2(v[mt][j + 6] * inv, v[mt][j + 7] * inv));
                     } else {
 #pragma unroll
                         for (int j = 0; j < 64; ++j)
-                            if (j < p.k) dst[j] = __float2bfloat16_rn(v[j] * inv);
+                            if (j < p.k) dst[j] = __float2bfloat16_rn(v[mt][j] * inv);
                     }
                 }
             }

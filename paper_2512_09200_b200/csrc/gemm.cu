@@ -148,7 +148,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const Params p) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align to 1024 B (SW128) by offsetting the __shared__ pointer itself, so the compiler keeps
+    // the shared address space (LDS/STS rather than generic loads)
+    uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr int A_BYTES = BM * BK * 2;
     constexpr int B_BYTES = BN * BK * 2;
     uint8_t* sA = smem;
@@ -379,6 +381,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc::fence_before();
     __syncthreads();
+    // peers read this CTA's exchange slots through DSMEM (pull model): nobody leaves the
+    // cluster before everyone is done
+    if (C > 1) tc::cluster_sync();
     if (warp == 1) tc::tmem_dealloc(tmem, 2 * BN);
 }
 
