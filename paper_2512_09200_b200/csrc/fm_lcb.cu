@@ -45,7 +45,8 @@ __device__ __forceinline__ int region_cols(const Params& p) {
     return 64 + p.d + ((p.n_pad + 127) / 128) * p.k_pad;
 }
 
-__global__ void __maxnreg__(200)  // 320 threads, 1 CTA/SM: up to 200 registers per thread
+// 10 warps: some SM sub-partitions hold 3 of them, so 168 registers is the ceiling
+__global__ void __launch_bounds__(kThreads, 1)
     fm_lcb_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWL,
                   const __grid_constant__ CUtensorMap tmYT, const Params p) {
     extern __shared__ uint8_t smem_raw[];
@@ -191,43 +192,47 @@ __global__ void __maxnreg__(200)  // 320 threads, 1 CTA/SM: up to 200 registers 
             tc::mbar_arrive(&x_empty[st]);
             tc::mbar_wait(&pl_full[rg], rph);
             tc::fence_after();
-            // X'[nF+row] = rms_norm_d(L[row] + X[nF+row])
-            float v[128];
-            tc::tmem_ld32(t_L, v);
-            tc::tmem_ld32(t_L + 32, v + 32);
-            if (d == 128) {
-                tc::tmem_ld32(t_L + 64, v + 64);
-                tc::tmem_ld32(t_L + 96, v + 96);
-            }
-            tc::fence_before();
-            tc::mbar_arrive(&tmem_empty[rg]);
+            // X'[nF+row] = rms_norm_d(L[row] + X[nF+row]): two passes over TMEM (sum of squares,
+            // then normalise + store) so only the packed residual stays live in registers
             float ss = 0.0f;
-            if (live) {
 #pragma unroll
-                for (int j = 0; j < 128; j += 8) {
-                    if (j < d) {
-                        const uint4 r = res[j / 8];
+            for (int c = 0; c < 128; c += 32) {
+                if (c < d) {
+                    float v[32];
+                    tc::tmem_ld32(t_L + c, v);
+#pragma unroll
+                    for (int j = 0; j < 32; j += 8) {
+                        const uint4 r = res[(c + j) / 8];
                         const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
-                            v[j + 2 * i] += bf16_lo(w[i]);
-                            v[j + 2 * i + 1] += bf16_hi(w[i]);
+                            const float a = v[j + 2 * i] + bf16_lo(w[i]), bb = v[j + 2 * i + 1] + bf16_hi(w[i]);
+                            ss += a * a + bb * bb;
                         }
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) ss += v[j + i] * v[j + i];
                     }
                 }
             }
-            if (live) {
-                const float inv = 1.0f / sqrtf(ss * inv_d + 1e-6f);
-                __nv_bfloat16* dst = p.Xout + (b * p.n + xr) * (int64_t)d;
+            const float inv = 1.0f / sqrtf(ss * inv_d + 1e-6f);
+            __nv_bfloat16* dst = p.Xout + (b * p.n + xr) * (int64_t)d;
 #pragma unroll
-                for (int j = 0; j < 128; j += 8)
-                    if (j < d)
-                        *reinterpret_cast<uint4*>(dst + j) =
-                            make_uint4(pack_bf16x2(v[j] * inv, v[j + 1] * inv), pack_bf16x2(v[j + 2] * inv, v[j + 3] * inv),
-                                       pack_bf16x2(v[j + 4] * inv, v[j + 5] * inv), pack_bf16x2(v[j + 6] * inv, v[j + 7] * inv));
+            for (int c = 0; c < 128; c += 32) {
+                if (c < d) {
+                    float v[32];
+                    tc::tmem_ld32(t_L + c, v);
+#pragma unroll
+                    for (int j = 0; j < 32; j += 8) {
+                        const uint4 r = res[(c + j) / 8];
+                        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+                        uint32_t o[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            o[i] = pack_bf16x2((v[j + 2 * i] + bf16_lo(w[i])) * inv, (v[j + 2 * i + 1] + bf16_hi(w[i])) * inv);
+                        if (live) *reinterpret_cast<uint4*>(dst + c + j) = make_uint4(o[0], o[1], o[2], o[3]);
+                    }
+                }
             }
+            tc::fence_before();
+            tc::mbar_arrive(&tmem_empty[rg]);
         }
     } else {  // ---- FM group, warps 6..9: P -> Pbuf, then Fin = rms_norm(flatten(X P))
         const int q = warp & 3;
