@@ -331,7 +331,7 @@ def run_mid(args, rank, world, local):
     # per-stage device times (separate pass, events between stages)
     net.set_timing(True)
     stages, emb_ms = [], []
-    for _ in range(3):
+    for _ in range(5):
         if sharded:  # ids a2a + owner pooling + pooled a2a, timed on the stream
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record(stream)
@@ -344,9 +344,9 @@ def run_mid(args, rank, world, local):
             step()
         stages.append(net.stage_times())
     net.set_timing(False)
-    st = [statistics.median(s[i] for s in stages) for i in range(len(stages[0]))]
+    st = [min(s[i] for s in stages) for i in range(len(stages[0]))]  # min: robust to host hiccups
     # stages: [bucket, bag (or shard gather), (fm_lcb, mlp) x blocks, tower]
-    t_bag = st[1] + (statistics.median(emb_ms) if sharded else 0.0)
+    t_bag = st[1] + (min(emb_ms) if sharded else 0.0)
     t_fm = [st[2 + 2 * b] for b in range(c["blocks"])]
     t_mlp = [st[3 + 2 * b] for b in range(c["blocks"])]
     t_tower = st[2 + 2 * c["blocks"]]

@@ -177,6 +177,8 @@ typedef struct {
     const void* resid;  /* bf16 [M][ldr] for epilogue 3 */
     int64_t ldr;
     int32_t group;      /* epilogue 3 group width (128 or 64) */
+    int32_t in_dtype;   /* A/B dtype: LATTICE_BF16 (kind::f16) or LATTICE_F32 (kind::tf32);
+                           resid has the output dtype */
 } lattice_gemm_args;
 
 lattice_status lattice_gemm(const lattice_gemm_args* args, lattice_stream stream);

@@ -68,7 +68,7 @@ class BagArgs(ctypes.Structure):
 class GemmArgs(ctypes.Structure):
     _fields_ = [("M", _I64), ("N", _I64), ("K", _I64), ("A", _P), ("lda", _I64), ("B", _P),
                 ("ldb", _I64), ("C", _P), ("ldc", _I64), ("out_dtype", _I32), ("epilogue", _I32),
-                ("resid", _P), ("ldr", _I64), ("group", _I32)]
+                ("resid", _P), ("ldr", _I64), ("group", _I32), ("in_dtype", _I32)]
 
 
 class NetConfig(ctypes.Structure):
@@ -291,16 +291,18 @@ EPI_STORE, EPI_SWISH, EPI_SWISH_HARD, EPI_RESID_NORM = 0, 1, 2, 3
 
 
 def gemm(A, B, epilogue=EPI_STORE, out_dtype=None, resid=None, group=128, out=None, stream=None):
-    """C = A @ B^T with A [M,K] bf16, B [N,K] bf16 on tcgen05; fused epilogue."""
+    """C = A @ B^T with A [M,K], B [N,K] both bf16 (kind::f16) or both fp32 (kind::tf32) on
+    tcgen05; fused epilogue. resid (epilogue 3) has the output dtype."""
     import torch
     M, K = A.shape
     N = B.shape[0]
-    odt = out_dtype or torch.bfloat16
+    f32_in = A.dtype == torch.float32
+    odt = out_dtype or (torch.float32 if f32_in else torch.bfloat16)
     if out is None:
         out = torch.empty((M, N), dtype=odt, device=A.device)
     a = GemmArgs(M, N, K, _p(A), A.stride(0), _p(B), B.stride(0), _p(out), out.stride(0),
                  F32 if odt == torch.float32 else BF16, epilogue, _p(resid),
-                 resid.stride(0) if resid is not None else 0, group)
+                 resid.stride(0) if resid is not None else 0, group, F32 if f32_in else BF16)
     check(_lib.lattice_gemm(ctypes.byref(a), _stream(stream)))
     return out
 

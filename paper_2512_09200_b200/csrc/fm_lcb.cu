@@ -13,9 +13,10 @@
 // W_L and Y stay resident in shared memory for the whole persistent CTA. P goes TMEM ->
 // registers -> bf16 -> swizzled shared memory to become F's B operand.
 //
-// Warp roles: 0 TMA producer, 1 MMA issuer, 2-5 LCB group (thread = L row: residual +
-// rms_norm_d, no cross-warp reduction), 6-9 FM group (P -> Pbuf, then the n*k-wide norm of
-// F with one 4-warp named barrier). The two groups run independently, so every SM
+// Warp roles: 0 TMA producer, 1 MMA issuer, 2-5 LCB group (thread = TMEM lane: P row ->
+// bf16 Pbuf for F's MMA, then L row + residual + rms_norm_d, no cross-warp reduction), 6-9 FM
+// group (the n*k-wide norm of F with one 4-warp named barrier). The two groups run
+// independently and the F MMAs of a sample overlap its LCB epilogue, so every SM
 // sub-partition has two epilogue warps in flight. TMEM holds two accumulator regions
 // {P | L | F}: the MMAs of sample s+1 run while sample s's epilogue drains the other region,
 // and X stages are double-buffered so loads run two samples ahead. The epilogue is the
@@ -192,6 +193,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_arrive(&x_empty[st]);
             tc::mbar_wait(&pl_full[rg], rph);
             tc::fence_after();
+            // P row `row` (= d index, same TMEM lane as this thread's L row) -> bf16 ->
+            // Pbuf[j][row], the K-major B operand of F. One Pbuf suffices: pl_full of this
+            // sample completes after the previous sample's F MMAs (same issuing thread).
+            {
+                const uint32_t t_P = tmem + rg * 256 + lane_off;
+                for (int c0 = 0; c0 < kpad; c0 += 16) {
+                    float pv[16];
+                    tc::tmem_ld16(t_P + c0, pv);
+                    if (row < d) {
+                        uint8_t* pan = sP + (row / 64) * ppanel;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            *reinterpret_cast<__nv_bfloat16*>(pan + swz(c0 + j, row & 63)) = __float2bfloat16_rn(pv[j]);
+                    }
+                }
+                tc::fence_async_shared();
+                tc::mbar_arrive(pbuf_full);
+            }
             // X'[nF+row] = rms_norm_d(L[row] + X[nF+row]): two passes over TMEM (sum of squares,
             // then normalise + store) so only the packed residual stays live in registers
             float ss = 0.0f;
@@ -245,23 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int st = it & 1;
             const int rg = nreg == 2 ? (it & 1) : 0;
             const uint32_t rph = nreg == 2 ? ((it >> 1) & 1) : (it & 1);
-            const uint32_t t_P = tmem + rg * 256 + lane_off, t_F = t_P + 64 + d;
-            tc::mbar_wait(&pl_full[rg], rph);
-            tc::fence_after();
-            // P row `row` (= d index) -> bf16 -> Pbuf[j][row], the K-major B operand of F. One
-            // Pbuf suffices: this sample's writes start after the previous F MMAs completed.
-            for (int c0 = 0; c0 < kpad; c0 += 16) {
-                float v[16];
-                tc::tmem_ld16(t_P + c0, v);
-                if (row < d) {
-                    uint8_t* pan = sP + (row / 64) * ppanel;
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        *reinterpret_cast<__nv_bfloat16*>(pan + swz(c0 + j, row & 63)) = __float2bfloat16_rn(v[j]);
-                }
-            }
-            tc::fence_async_shared();
-            tc::mbar_arrive(pbuf_full);
+            const uint32_t t_F = tmem + rg * 256 + lane_off + 64 + d;
             tc::mbar_wait(&f_full[rg], rph);
             tc::fence_after();
             tc::mbar_arrive(&x_empty[st]);  // every MMA reading this X stage has completed

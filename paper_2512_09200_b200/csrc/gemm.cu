@@ -82,15 +82,27 @@ __device__ __forceinline__ void resid_norm_group(const Params& p, uint32_t taddr
 #pragma unroll
     for (int c = 0; c < GROUP; c += 32) tc::tmem_ld32(taddr + c, v + c);
     if (!valid) return;
-    const __nv_bfloat16* r = p.resid + m * p.ldr + n;
+    if (p.out_bf16) {
+        const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(p.resid) + m * p.ldr + n;
 #pragma unroll
-    for (int c = 0; c < GROUP; c += 8) {
-        const uint4 q = *reinterpret_cast<const uint4*>(r + c);
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        for (int c = 0; c < GROUP; c += 8) {
+            const uint4 q = *reinterpret_cast<const uint4*>(r + c);
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            v[c + 2 * i] += bf16_lo(w[i]);
-            v[c + 2 * i + 1] += bf16_hi(w[i]);
+            for (int i = 0; i < 4; ++i) {
+                v[c + 2 * i] += bf16_lo(w[i]);
+                v[c + 2 * i + 1] += bf16_hi(w[i]);
+            }
+        }
+    } else {
+        const float* r = static_cast<const float*>(p.resid) + m * p.ldr + n;
+#pragma unroll
+        for (int c = 0; c < GROUP; c += 4) {
+            const float4 q = *reinterpret_cast<const float4*>(r + c);
+            v[c] += q.x;
+            v[c + 1] += q.y;
+            v[c + 2] += q.z;
+            v[c + 3] += q.w;
         }
     }
     float ss = 0.0f;
@@ -143,7 +155,7 @@ __device__ __forceinline__ void decode(const Params& p, const Sched& s, int u, i
 // ---------------------------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------------------------
-template <int STAGES>
+template <int STAGES, typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const Params p) {
@@ -151,8 +163,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // align to 1024 B (SW128) by offsetting the __shared__ pointer itself, so the compiler keeps
     // the shared address space (LDS/STS rather than generic loads)
     uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-    constexpr int A_BYTES = BM * BK * 2;
-    constexpr int B_BYTES = BN * BK * 2;
+    using Op = tc::Operand<T>;
+    constexpr int BKE = Op::kRow;         // elements per 128-byte k-block row
+    constexpr int A_BYTES = BM * 128;
+    constexpr int B_BYTES = BN * 128;
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
@@ -181,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         s.first = blockIdx.x;
         s.stride = gridDim.x;
     }
-    const int nk = (p.K + BK - 1) / BK;
+    const int nk = (p.K + BKE - 1) / BKE;
 
     if (warp == 0 && lane == 0) {
         tc::tma_prefetch(&tmA);
@@ -217,14 +231,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t ph = (g / STAGES) & 1;
                     tc::mbar_wait(&empty[st], ph ^ 1);
                     tc::mbar_expect_tx(&full[st], A_BYTES + B_BYTES);
-                    tc::tma_load_2d(sA + st * A_BYTES, &tmA, &full[st], kb * BK, m0);
-                    tc::tma_load_2d(sB + st * B_BYTES, &tmB, &full[st], kb * BK, b_row0);
+                    tc::tma_load_2d(sA + st * A_BYTES, &tmA, &full[st], kb * BKE, m0);
+                    tc::tma_load_2d(sB + st * B_BYTES, &tmB, &full[st], kb * BKE, b_row0);
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---- MMA issuer
-            constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
+            constexpr uint32_t idesc = tc::idesc_fmt(Op::kFormat, BM, BN, 0, 0);
             int g = 0, i = 0;
             for (int u = s.first; u < s.units; u += s.stride, ++i) {
                 const int acc = i & 1;
@@ -239,10 +253,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t a_base = tc::smem_u32(sA + st * A_BYTES);
                     const uint32_t b_base = tc::smem_u32(sB + st * B_BYTES);
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {
+                    for (int k = 0; k < 4; ++k) {  // 4 x 32-byte K slices per k-block
                         const uint64_t ad = tc::sdesc(a_base + k * 32, 16, 1024, 2);
                         const uint64_t bd = tc::sdesc(b_base + k * 32, 16, 1024, 2);
-                        tc::mma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                        Op::mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
                     }
                     tc::mma_commit(&empty[st]);
                 }
@@ -404,16 +418,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <int STAGES>
+template <int STAGES, typename T>
 lattice_status launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int units,
                         cudaStream_t st) {
     const size_t smem = smem_bytes(BN, STAGES, p.cluster, p.heads) + kMaxCluster * BM * 4 +
                         (size_t)p.cluster * p.heads * BM * 4;  // double-buffered exchange slots
     static bool attr_done = false;
     if (!attr_done) {
-        LAT_CUDA(cudaFuncSetAttribute(gemm_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        LAT_CUDA(cudaFuncSetAttribute(gemm_kernel<STAGES, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       227 * 1024));
-        LAT_CUDA(cudaFuncSetAttribute(gemm_kernel<STAGES>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        LAT_CUDA(cudaFuncSetAttribute(gemm_kernel<STAGES, T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         attr_done = true;
     }
     if (smem > 227 * 1024) return set_error(LATTICE_USAGE, "gemm: shared memory budget exceeded");
@@ -435,7 +449,7 @@ lattice_status launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Para
     if (!max_clusters[C]) {
         cfg.gridDim = dim3(C * (num_sms() / C), 1, 1);
         int mc = 0;
-        if (cudaOccupancyMaxActiveClusters(&mc, gemm_kernel<STAGES>, &cfg) != cudaSuccess || mc < 1)
+        if (cudaOccupancyMaxActiveClusters(&mc, gemm_kernel<STAGES, T>, &cfg) != cudaSuccess || mc < 1)
             mc = num_sms() / C;
         max_clusters[C] = mc;
     }
@@ -443,13 +457,13 @@ lattice_status launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Para
     if (clusters > units) clusters = units;
     if (clusters < 1) clusters = 1;
     cfg.gridDim = dim3(clusters * C, 1, 1);
-    LAT_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<STAGES>, ta, tb, p));
+    LAT_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<STAGES, T>, ta, tb, p));
     return LATTICE_OK;
 }
 }  // namespace
 
 lattice_status make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
-                           uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+                           uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, bool f32) {
     auto fn = encode_fn();
     if (!fn) return set_error(LATTICE_CUDA, "cuTensorMapEncodeTiled unavailable");
     if ((reinterpret_cast<uintptr_t>(base) & 15) || (row_stride_bytes & 15))
@@ -458,7 +472,8 @@ lattice_status make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uin
     cuuint64_t strides[1] = {row_stride_bytes};
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+    CUresult r = fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                    const_cast<void*>(base), dims, strides,
                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
@@ -470,18 +485,22 @@ lattice_status launch(const GemmPlan& g, cudaStream_t st) {
     // grid_y carries the number of M units (dense M-tiles, or the tile-table capacity)
     const int nt = (g.p.N + BN - 1) / BN;
     const int units = g.p.cluster > 1 ? g.grid_y : g.grid_y * nt;
-    return launch_t<4>(g.ta, g.tb, g.p, units, st);
+    if (g.f32) return launch_t<4, float>(g.ta, g.tb, g.p, units, st);
+    return launch_t<4, __nv_bfloat16>(g.ta, g.tb, g.p, units, st);
 }
 
 lattice_status plan(GemmPlan* g, const void* A, int64_t lda, int64_t a_rows, const void* B,
-                    int64_t ldb, int64_t b_rows, const Params& p, int grid_y) {
-    lattice_status s = make_map_2d(&g->ta, A, (uint64_t)p.K, (uint64_t)a_rows, (uint64_t)lda * 2, BK, BM);
+                    int64_t ldb, int64_t b_rows, const Params& p, int grid_y, bool f32) {
+    const uint64_t es = f32 ? 4 : 2;
+    const uint32_t bke = f32 ? 32 : 64;
+    lattice_status s = make_map_2d(&g->ta, A, (uint64_t)p.K, (uint64_t)a_rows, (uint64_t)lda * es, bke, BM, f32);
     if (s != LATTICE_OK) return s;
-    s = make_map_2d(&g->tb, B, (uint64_t)p.K, (uint64_t)b_rows, (uint64_t)ldb * 2, BK, BN);
+    s = make_map_2d(&g->tb, B, (uint64_t)p.K, (uint64_t)b_rows, (uint64_t)ldb * es, bke, BN, f32);
     if (s != LATTICE_OK) return s;
     g->p = p;
     g->grid_y = grid_y;
     g->stages = 4;
+    g->f32 = f32;
     return LATTICE_OK;
 }
 
@@ -506,7 +525,7 @@ extern "C" lattice_status lattice_gemm(const lattice_gemm_args* a, lattice_strea
     p.ldc = a->ldc;
     p.out_bf16 = a->out_dtype == LATTICE_BF16;
     p.epi = a->epilogue;
-    p.resid = static_cast<const __nv_bfloat16*>(a->resid);
+    p.resid = a->resid;
     p.ldr = a->ldr;
     p.group = a->group;
     p.N_full = p.N;
@@ -517,12 +536,14 @@ extern "C" lattice_status lattice_gemm(const lattice_gemm_args* a, lattice_strea
         LAT_REQUIRE(p.cluster <= kMaxCluster, "lattice_gemm: swish_rn rows wider than 2048 are not supported");
     }
     if (p.epi == kResidNorm) {
-        LAT_REQUIRE(a->resid && (a->group == 128 || a->group == 64) && p.N % a->group == 0 &&
-                        a->ldr % 8 == 0 && p.out_bf16,
-                    "lattice_gemm: residual-norm epilogue needs bf16 out, group 64/128 dividing N");
+        LAT_REQUIRE(a->resid && (a->group == 128 || a->group == 64) && p.N % a->group == 0 && a->ldr % 8 == 0,
+                    "lattice_gemm: residual-norm epilogue needs a residual, group 64/128 dividing N");
     }
     GemmPlan g;
-    lattice_status s = plan(&g, a->A, a->lda, a->M, a->B, a->ldb, a->N, p, (int)((a->M + BM - 1) / BM));
+    LAT_REQUIRE(a->in_dtype == LATTICE_BF16 || a->in_dtype == LATTICE_F32, "lattice_gemm: in_dtype must be bf16 or f32");
+    const bool f32 = a->in_dtype == LATTICE_F32;
+    LAT_REQUIRE(!f32 || (a->K % 4 == 0 && a->lda % 4 == 0 && a->ldb % 4 == 0), "lattice_gemm: fp32 strides");
+    lattice_status s = plan(&g, a->A, a->lda, a->M, a->B, a->ldb, a->N, p, (int)((a->M + BM - 1) / BM), f32);
     if (s != LATTICE_OK) return s;
     return launch(g, stream);
 }

@@ -42,7 +42,7 @@ struct Params {
     int64_t ldc;
     int out_bf16;
     int epi;
-    const __nv_bfloat16* resid;
+    const void* resid;   // same dtype as the output (bf16 or fp32)
     int64_t ldr;
     int group;
     int cluster;         // CTAs along N sharing a row (row-norm epilogues)

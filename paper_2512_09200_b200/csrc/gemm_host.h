@@ -13,13 +13,15 @@ struct GemmPlan {
     Params p;
     int grid_y;
     int stages;
+    bool f32;  // fp32 operands on the TF32 tensor path
 };
 
 lattice_status make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
-                           uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+                           uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer,
+                           bool f32 = false);
 // A: [a_rows][K] (row stride lda elements), B: [b_rows][K]; tiles of 128 x 256.
 lattice_status plan(GemmPlan* g, const void* A, int64_t lda, int64_t a_rows, const void* B,
-                    int64_t ldb, int64_t b_rows, const Params& p, int grid_y);
+                    int64_t ldb, int64_t b_rows, const Params& p, int grid_y, bool f32 = false);
 lattice_status launch(const GemmPlan& g, cudaStream_t st);
 
 }  // namespace gemm

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 namespace lat {
@@ -147,6 +148,41 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// D[tmem] (+)= A . B, kind::tf32 (fp32 operands in smem, TF32 multiply, fp32 accumulate).
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Operand-type traits: bytes per element, elements per 128-byte swizzle row, K per MMA.
+template <typename T>
+struct Operand;
+template <>
+struct Operand<__nv_bfloat16> {
+    static constexpr int kBytes = 2, kRow = 64, kK = 16, kFormat = 1;
+    __device__ static void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+        mma_f16(d, a, b, id, acc);
+    }
+};
+template <>
+struct Operand<float> {
+    static constexpr int kBytes = 4, kRow = 32, kK = 8, kFormat = 2;  // TF32
+    __device__ static void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+        mma_tf32(d, a, b, id, acc);
+    }
+};
+
+// Instruction descriptor for kind::f16 / kind::tf32 with an fp32 accumulator.
+__host__ __device__ constexpr uint32_t idesc_fmt(int fmt, int M, int N, int a_mn, int b_mn) {
+    return (1u << 4) | (uint32_t(fmt) << 7) | (uint32_t(fmt) << 10) | (uint32_t(a_mn) << 15) |
+           (uint32_t(b_mn) << 16) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
 // Arrive on an mbarrier once every previously issued tcgen05.mma of this thread completed.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile(
