@@ -21,6 +21,7 @@ struct NetworkConfig {
     bool hard_gate = false;             // swish_rn_hard activations
     std::int64_t max_batch = 512;
     Seed weight_seed{0x1A79};
+    lattice_dtype dtype = LATTICE_F32;  // configs[0] is fp32 (TF32 tensor cores); bf16 otherwise
 };
 
 // Jagged sparse batch, feature-major CSR: bag (f, b) = ids[offsets[f*B+b] .. offsets[f*B+b+1]).
@@ -57,6 +58,7 @@ public:
         nc.hard = c.hard_gate ? 1 : 0;
         nc.max_batch = c.max_batch;
         nc.weight_seed = c.weight_seed.value;
+        nc.dtype = c.dtype;
         device::throw_status(lattice_net_create(&nc, &net_));
     }
     Network(const Network&) = delete;

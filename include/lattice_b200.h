@@ -200,6 +200,8 @@ typedef struct {
     int32_t hard;          /* 1: swish_rn_hard */
     int64_t max_batch;
     uint64_t weight_seed;
+    int32_t dtype;         /* storage/compute dtype: LATTICE_BF16 (kind::f16 tensor cores) or
+                              LATTICE_F32 (kind::tf32; d = 64 only) */
 } lattice_net_config;
 
 typedef struct lattice_net lattice_net;

@@ -75,7 +75,7 @@ class NetConfig(ctypes.Structure):
     _fields_ = [("n", _I32), ("d", _I32), ("blocks", _I32), ("nF", _I32), ("nL", _I32),
                 ("k", _I32), ("n_mlp", _I32), ("mlp", _I32 * 6), ("domains", _I32),
                 ("heads", _I32), ("tower_hidden", _I32), ("hard", _I32), ("max_batch", _I64),
-                ("weight_seed", _U64)]
+                ("weight_seed", _U64), ("dtype", _I32)]
 
 
 class Batch(ctypes.Structure):
@@ -332,10 +332,11 @@ class Network:
     """lattice::Network over the C ABI (lattice_net_*). Weights live on the current device."""
 
     def __init__(self, n, d, blocks, nF, nL, k, mlp, domains, heads, tower_hidden, hard=False,
-                 max_batch=32768, weight_seed=0x1A78):
+                 max_batch=32768, weight_seed=0x1A78, dtype="bf16"):
+        """dtype "bf16" (kind::f16 tensor cores) or "f32" (fp32 storage, kind::tf32; d=64)."""
         self.cfg = dict(n=n, d=d, blocks=blocks, nF=nF, nL=nL, k=k, mlp=list(mlp), domains=domains,
                         heads=heads, tower_hidden=tower_hidden, hard=hard, max_batch=max_batch,
-                        weight_seed=weight_seed)
+                        weight_seed=weight_seed, dtype=dtype)
         c = NetConfig()
         c.n, c.d, c.blocks, c.nF, c.nL, c.k = n, d, blocks, nF, nL, k
         c.n_mlp = len(mlp) - 1
@@ -343,6 +344,7 @@ class Network:
             c.mlp[i] = w
         c.domains, c.heads, c.tower_hidden, c.hard = domains, heads, tower_hidden, int(hard)
         c.max_batch, c.weight_seed = max_batch, weight_seed
+        c.dtype = F32 if dtype in ("f32", "fp32", "float32") else BF16
         h = ctypes.c_void_p()
         check(_lib.lattice_net_create(ctypes.byref(c), ctypes.byref(h)))
         self._h = h
@@ -394,19 +396,20 @@ class Network:
         import torch
         c = self.cfg
         n, d, k, nL = c["n"], c["d"], c["k"], c["nL"]
+        wdt = torch.float32 if c["dtype"] in ("f32", "fp32", "float32") else torch.bfloat16
         out = {"YT": [], "WL": [], "mlp": []}
         for blk in range(c["blocks"]):
-            yt = _view(_lib.lattice_net_weight(self._h, blk, 1, 0), (_pad16(k), _pad16(n)), torch.bfloat16)
-            wl = _view(_lib.lattice_net_weight(self._h, blk, 2, 0), (128, _pad16(n)), torch.bfloat16)
+            yt = _view(_lib.lattice_net_weight(self._h, blk, 1, 0), (_pad16(k), _pad16(n)), wdt)
+            wl = _view(_lib.lattice_net_weight(self._h, blk, 2, 0), (128, _pad16(n)), wdt)
             out["YT"].append(yt[:k, :n].float().cpu().numpy().copy())
             out["WL"].append(wl[:nL, :n].float().cpu().numpy().copy())
             for li in range(len(c["mlp"]) - 1):
                 w = _view(_lib.lattice_net_weight(self._h, blk, 3, li),
-                          (c["mlp"][li + 1], c["mlp"][li]), torch.bfloat16)
+                          (c["mlp"][li + 1], c["mlp"][li]), wdt)
                 out["mlp"].append(w.float().cpu().numpy().copy())
         G, th, H = c["domains"], c["tower_hidden"], c["heads"]
         out["T1"] = _view(_lib.lattice_net_weight(self._h, 0, 4, 0), (G, th, n * d),
-                          torch.bfloat16).float().cpu().numpy().copy()
+                          wdt).float().cpu().numpy().copy()
         out["T2"] = _view(_lib.lattice_net_weight(self._h, 0, 5, 0), (G, H, th),
                           torch.float32).cpu().numpy().copy()
         return out

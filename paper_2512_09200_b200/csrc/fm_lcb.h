@@ -13,9 +13,10 @@ struct Params {
     int64_t B;
     int n, d, k, nF, nL;
     int n_pad, k_pad;       // multiples of 16
-    int tmem_cols;          // 256 or 512
-    __nv_bfloat16* Fout;    // [B][n*k]
-    __nv_bfloat16* Xout;    // [B][n][d], rows nF .. n-1 written
+    int tmem_cols;          // informational (the kernel sizes its own allocation)
+    int f32;                // 1: fp32 storage, kind::tf32 MMAs; 0: bf16, kind::f16
+    void* Fout;             // [B][n*k]
+    void* Xout;             // [B][n][d], rows nF .. n-1 written
 };
 
 struct Plan {
@@ -23,7 +24,7 @@ struct Plan {
     Params p;
 };
 
-// X: [B][n][d] bf16. WLpad: [128][n_pad] bf16 (rows >= nL zero). YTpad: [k_pad][n_pad] bf16.
+// X: [B][n][d]. WLpad: [128][n_pad] (rows >= nL zero). YTpad: [k_pad][n_pad]. Same dtype.
 lattice_status check(const Params& p);
 lattice_status make_maps(Plan* pl, const void* X, const void* WLpad, const void* YTpad);
 lattice_status launch(const Plan& pl, cudaStream_t st);

@@ -7,8 +7,10 @@
 //                         swish_rn  ->  K3 last GEMM with fused residual + rms_norm_d (FMB half)
 //   K4 towers             one grouped GEMM over the G domain segments, swish_rn + heads fused,
 //                         logits written back in the caller's sample order
-// All weights are bf16 (tower heads fp32), generated on device from weight_seed with the
-// counter-based scheme shared with oracle/lattice_oracle.c.
+// Storage dtype (cfg.dtype): bf16 (kind::f16 MMAs) or fp32 (kind::tf32 MMAs) for weights and
+// activations; tower heads and logits are fp32. Weights are generated on device from
+// weight_seed with the counter-based scheme shared with oracle/lattice_oracle.c (the values
+// are exact in both dtypes).
 #include <cuda_bf16.h>
 
 #include <string>
@@ -43,16 +45,19 @@ __global__ void tiles_kernel(const int32_t* __restrict__ seg, int G, int4* __res
     }
 }
 
-// pooled sums (caller order, [B][n][d] f32 or bf16) -> rms_norm_d -> bf16 row pos[b] of X0
-template <typename T>
-__global__ void pooled_norm_kernel(int64_t B, int n, int d, const T* __restrict__ in,
-                                   const int32_t* __restrict__ pos, __nv_bfloat16* __restrict__ out) {
+__device__ __forceinline__ void put(float* p, float v) { *p = v; }
+__device__ __forceinline__ void put(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
+// pooled sums (caller order, [B][n][d] f32 or bf16) -> rms_norm_d -> row pos[b] of X0
+template <typename TI, typename TO>
+__global__ void pooled_norm_kernel(int64_t B, int n, int d, const TI* __restrict__ in,
+                                   const int32_t* __restrict__ pos, TO* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < B * n;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t b = w / n;
         const int f = (int)(w - b * n);
-        const T* src = in + w * d;
+        const TI* src = in + w * d;
         float v[4];
         float ss = 0.0f;
 #pragma unroll
@@ -63,29 +68,30 @@ __global__ void pooled_norm_kernel(int64_t B, int n, int d, const T* __restrict_
         }
         ss = warp_sum(ss);
         const float denom = sqrtf(ss / (float)d + 1e-6f);
-        __nv_bfloat16* dst = out + ((int64_t)pos[b] * n + f) * d;
+        TO* dst = out + ((int64_t)pos[b] * n + f) * d;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int c = lane + 32 * i;
-            if (c < d) dst[c] = __float2bfloat16_rn(v[i] / denom);
+            if (c < d) put(dst + c, v[i] / denom);
         }
     }
 }
 
-// table-wise shards [S][B][n/S][d] bf16 (already normalised by their owners) -> X0 rows
-// pos[b]; one warp per (b, f), 16-byte vectors
-__global__ void shard_gather_kernel(int64_t B, int n, int d, int S, const __nv_bfloat16* __restrict__ in,
-                                    const int32_t* __restrict__ pos, __nv_bfloat16* __restrict__ out) {
+// table-wise shards [S][B][n/S][d] (already normalised by their owners) -> X0 rows pos[b];
+// one warp per (b, f), 16-byte vectors; dtype-agnostic (vec = d * es / 16)
+__global__ void shard_gather_kernel(int64_t B, int n, int d, int es, int S, const uint8_t* __restrict__ in,
+                                    const int32_t* __restrict__ pos, uint8_t* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     const int nl = n / S;
-    const int vec = d / 8;  // uint4 per row
+    const int row = d * es;      // bytes per embedding
+    const int vec = row / 16;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < B * n;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t b = w / n;
         const int f = (int)(w - b * n);
         const int o = f / nl, fl = f - o * nl;
-        const uint4* src = reinterpret_cast<const uint4*>(in + (((int64_t)o * B + b) * nl + fl) * d);
-        uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)pos[b] * n + f) * d);
+        const uint4* src = reinterpret_cast<const uint4*>(in + (((int64_t)o * B + b) * nl + fl) * row);
+        uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)pos[b] * n + f) * row);
         for (int i = lane; i < vec; i += 32) dst[i] = src[i];
     }
 }
@@ -99,18 +105,20 @@ struct lattice_net {
     lattice_net_config cfg;
     int n_pad, k_pad;
     int device;
-    // weights
-    std::vector<__nv_bfloat16*> YT, WL;  // padded [k_pad][n_pad], [128][n_pad]
-    std::vector<__nv_bfloat16*> mlp;     // [blocks * n_mlp] -> [out][in]
-    __nv_bfloat16* T1 = nullptr;         // [G * th][n*d]
-    float* T2 = nullptr;                 // [G][heads][th]
+    bool f32;
+    size_t es;  // bytes per stored element
+    // weights (storage dtype unless noted)
+    std::vector<void*> YT, WL;   // padded [k_pad][n_pad], [128][n_pad]
+    std::vector<void*> mlp;      // [blocks * n_mlp] -> [out][in]
+    void* T1 = nullptr;          // [G * th][n*d]
+    float* T2 = nullptr;         // [G][heads][th] fp32
     // workspace
     int32_t *pos = nullptr, *order = nullptr, *seg = nullptr;
     int4* tiles = nullptr;
     int* n_tiles = nullptr;
-    __nv_bfloat16* X[2] = {nullptr, nullptr};
-    __nv_bfloat16* Fbuf = nullptr;
-    __nv_bfloat16* H[2] = {nullptr, nullptr};
+    void* X[2] = {nullptr, nullptr};
+    void* Fbuf = nullptr;
+    void* H[2] = {nullptr, nullptr};
     // plans (tensor maps built once for max_batch)
     std::vector<lat::fm::Plan> fm_plans;              // [blocks]
     std::vector<lat::gemm::GemmPlan> mlp_plans;       // [blocks * n_mlp]
@@ -118,30 +126,37 @@ struct lattice_net {
     // timing
     bool timing = false;
     std::vector<cudaEvent_t> ev;
-    std::vector<float> stage_ms;
     std::vector<void*> allocs;
 };
 
 namespace {
 
-template <typename T>
-lattice_status dalloc(lattice_net* net, T** p, size_t count) {
+lattice_status dalloc_bytes(lattice_net* net, void** p, size_t bytes) {
     void* q = nullptr;
-    LAT_CUDA(cudaMalloc(&q, count * sizeof(T) > 0 ? count * sizeof(T) : 16));
+    LAT_CUDA(cudaMalloc(&q, bytes > 0 ? bytes : 16));
     net->allocs.push_back(q);
-    *p = static_cast<T*>(q);
+    *p = q;
     return LATTICE_OK;
 }
 
-lattice_status fill_padded(lattice_net* net, __nv_bfloat16* dst, int rows, int cols, int rows_pad,
-                           int cols_pad, uint64_t tag) {
-    LAT_CUDA(cudaMemset(dst, 0, sizeof(__nv_bfloat16) * (size_t)rows_pad * cols_pad));
-    __nv_bfloat16* tmp = nullptr;
-    LAT_CUDA(cudaMalloc(&tmp, sizeof(__nv_bfloat16) * (size_t)rows * cols));
-    lattice_status s = lattice_fill_weights(tmp, LATTICE_BF16, rows, cols, net->cfg.weight_seed, tag, nullptr);
+template <typename T>
+lattice_status dalloc(lattice_net* net, T** p, size_t count) {
+    void* q = nullptr;
+    lattice_status s = dalloc_bytes(net, &q, count * sizeof(T));
+    *p = static_cast<T*>(q);
+    return s;
+}
+
+lattice_status fill_padded(lattice_net* net, void* dst, int rows, int cols, int rows_pad, int cols_pad,
+                           uint64_t tag) {
+    const size_t es = net->es;
+    LAT_CUDA(cudaMemset(dst, 0, es * (size_t)rows_pad * cols_pad));
+    void* tmp = nullptr;
+    LAT_CUDA(cudaMalloc(&tmp, es * (size_t)rows * cols));
+    lattice_status s = lattice_fill_weights(tmp, net->f32 ? LATTICE_F32 : LATTICE_BF16, rows, cols,
+                                            net->cfg.weight_seed, tag, nullptr);
     if (s == LATTICE_OK) {
-        cudaError_t e = cudaMemcpy2D(dst, sizeof(__nv_bfloat16) * cols_pad, tmp, sizeof(__nv_bfloat16) * cols,
-                                     sizeof(__nv_bfloat16) * cols, rows, cudaMemcpyDeviceToDevice);
+        cudaError_t e = cudaMemcpy2D(dst, es * cols_pad, tmp, es * cols, es * cols, rows, cudaMemcpyDeviceToDevice);
         if (e != cudaSuccess) s = lat::check_cuda(e, "weight pad copy");
     }
     cudaFree(tmp);
@@ -151,8 +166,11 @@ lattice_status fill_padded(lattice_net* net, __nv_bfloat16* dst, int rows, int c
 lattice_status validate(const lattice_net_config* c) {
     using lat::set_error;
     if (!c) return set_error(LATTICE_USAGE, "lattice_net_create: null config");
+    if (c->dtype != LATTICE_BF16 && c->dtype != LATTICE_F32)
+        return set_error(LATTICE_USAGE, "network: dtype must be bf16 or f32");
     if (c->n < 1 || c->n > 256) return set_error(LATTICE_USAGE, "network: n must be in [1, 256]");
     if (c->d != 64 && c->d != 128) return set_error(LATTICE_USAGE, "network: d must be 64 or 128");
+    if (c->dtype == LATTICE_F32 && c->d != 64) return set_error(LATTICE_USAGE, "network: fp32 needs d = 64");
     if (c->blocks < 1) return set_error(LATTICE_USAGE, "network: need at least one block");
     if (c->nF < 1 || c->nL < 0 || c->nF + c->nL != c->n || c->nL > 128)
         return set_error(LATTICE_USAGE, "network: need nF >= 1, nL <= 128 and nF + nL == n");
@@ -180,8 +198,8 @@ lattice_status build_plans(lattice_net* net) {
     net->fm_plans.resize(c.blocks);
     net->mlp_plans.resize((size_t)c.blocks * c.n_mlp);
     for (int blk = 0; blk < c.blocks; ++blk) {
-        __nv_bfloat16* Xc = net->X[blk & 1];
-        __nv_bfloat16* Xn = net->X[(blk + 1) & 1];
+        void* Xc = net->X[blk & 1];
+        void* Xn = net->X[(blk + 1) & 1];
         fm::Plan& fp = net->fm_plans[blk];
         fp.p.B = Bm;
         fp.p.n = c.n;
@@ -191,7 +209,8 @@ lattice_status build_plans(lattice_net* net) {
         fp.p.nL = c.nL;
         fp.p.n_pad = net->n_pad;
         fp.p.k_pad = net->k_pad;
-        fp.p.tmem_cols = (64 + c.d + ((net->n_pad + 127) / 128) * net->k_pad) <= 256 ? 256 : 512;
+        fp.p.tmem_cols = 512;
+        fp.p.f32 = net->f32 ? 1 : 0;
         fp.p.Fout = net->Fbuf;
         fp.p.Xout = Xn;
         lattice_status s = fm::check(fp.p);
@@ -201,12 +220,12 @@ lattice_status build_plans(lattice_net* net) {
         for (int li = 0; li < c.n_mlp; ++li) {
             const int in = c.mlp[li], out = c.mlp[li + 1];
             const bool last = li + 1 == c.n_mlp;
-            const __nv_bfloat16* A = li == 0 ? net->Fbuf : net->H[(li - 1) & 1];
+            const void* A = li == 0 ? net->Fbuf : net->H[(li - 1) & 1];
             gemm::Params p = {};
             p.M = (int)Bm;
             p.N = out;
             p.K = in;
-            p.out_bf16 = 1;
+            p.out_bf16 = net->f32 ? 0 : 1;
             p.N_full = out;
             p.cluster = 1;
             if (!last) {
@@ -223,7 +242,7 @@ lattice_status build_plans(lattice_net* net) {
                 p.group = c.d;
             }
             s = gemm::plan(&net->mlp_plans[(size_t)blk * c.n_mlp + li], A, in, Bm, net->mlp[(size_t)blk * c.n_mlp + li],
-                           in, out, p, (int)((Bm + 127) / 128));
+                           in, out, p, (int)((Bm + 127) / 128), net->f32);
             if (s != LATTICE_OK) return s;
         }
     }
@@ -242,7 +261,7 @@ lattice_status build_plans(lattice_net* net) {
     p.heads = c.heads;
     p.order = net->order;
     return gemm::plan(&net->tower_plan, net->X[c.blocks & 1], nd, Bm, net->T1, nd,
-                      (int64_t)c.domains * c.tower_hidden, p, (int)((Bm + 127) / 128) + c.domains);
+                      (int64_t)c.domains * c.tower_hidden, p, (int)((Bm + 127) / 128) + c.domains, net->f32);
 }
 
 }  // namespace
@@ -259,10 +278,14 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
     net->cfg = *cfg;
     cudaGetDevice(&net->device);
     const lattice_net_config& c = net->cfg;
+    net->f32 = c.dtype == LATTICE_F32;
+    net->es = net->f32 ? 4 : 2;
+    const int wdt = net->f32 ? LATTICE_F32 : LATTICE_BF16;
     net->n_pad = round_up(c.n, 16);
     net->k_pad = round_up(c.k, 16);
     const int nd = c.n * c.d;
     const int64_t Bm = c.max_batch;
+    const size_t es = net->es;
     auto fail = [&](lattice_status st) {
         lattice_net_destroy(net);
         return st;
@@ -274,26 +297,26 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
     } while (0)
     const uint64_t seed = c.weight_seed;
     for (int blk = 0; blk < c.blocks; ++blk) {
-        __nv_bfloat16 *yt, *wl;
-        NET_TRY(dalloc(net, &yt, (size_t)net->k_pad * net->n_pad));
-        NET_TRY(dalloc(net, &wl, (size_t)128 * net->n_pad));
+        void *yt = nullptr, *wl = nullptr;
+        NET_TRY(dalloc_bytes(net, &yt, es * (size_t)net->k_pad * net->n_pad));
+        NET_TRY(dalloc_bytes(net, &wl, es * (size_t)128 * net->n_pad));
         NET_TRY(fill_padded(net, yt, c.k, c.n, net->k_pad, net->n_pad, weight_tag(blk, 1, 0)));
         NET_TRY(fill_padded(net, wl, c.nL > 0 ? c.nL : 1, c.n, 128, net->n_pad, weight_tag(blk, 2, 0)));
-        if (c.nL == 0) LAT_CUDA(cudaMemset(wl, 0, sizeof(__nv_bfloat16) * 128 * net->n_pad));
+        if (c.nL == 0) LAT_CUDA(cudaMemset(wl, 0, es * 128 * net->n_pad));
         net->YT.push_back(yt);
         net->WL.push_back(wl);
         for (int li = 0; li < c.n_mlp; ++li) {
-            __nv_bfloat16* w;
-            NET_TRY(dalloc(net, &w, (size_t)c.mlp[li + 1] * c.mlp[li]));
-            NET_TRY(lattice_fill_weights(w, LATTICE_BF16, c.mlp[li + 1], c.mlp[li], seed, weight_tag(blk, 3, li), nullptr));
+            void* w = nullptr;
+            NET_TRY(dalloc_bytes(net, &w, es * (size_t)c.mlp[li + 1] * c.mlp[li]));
+            NET_TRY(lattice_fill_weights(w, wdt, c.mlp[li + 1], c.mlp[li], seed, weight_tag(blk, 3, li), nullptr));
             net->mlp.push_back(w);
         }
     }
-    NET_TRY(dalloc(net, &net->T1, (size_t)c.domains * c.tower_hidden * nd));
+    NET_TRY(dalloc_bytes(net, &net->T1, es * (size_t)c.domains * c.tower_hidden * nd));
     NET_TRY(dalloc(net, &net->T2, (size_t)c.domains * c.heads * c.tower_hidden));
     for (int g = 0; g < c.domains; ++g) {
-        NET_TRY(lattice_fill_weights(net->T1 + (size_t)g * c.tower_hidden * nd, LATTICE_BF16, c.tower_hidden, nd,
-                                     seed, weight_tag(g, 4, 0), nullptr));
+        NET_TRY(lattice_fill_weights(static_cast<uint8_t*>(net->T1) + es * (size_t)g * c.tower_hidden * nd, wdt,
+                                     c.tower_hidden, nd, seed, weight_tag(g, 4, 0), nullptr));
         NET_TRY(lattice_fill_weights(net->T2 + (size_t)g * c.heads * c.tower_hidden, LATTICE_F32, c.heads,
                                      c.tower_hidden, seed, weight_tag(g, 5, 0), nullptr));
     }
@@ -304,11 +327,11 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
     NET_TRY(dalloc(net, &net->seg, (size_t)c.domains + 1));
     NET_TRY(dalloc(net, &net->tiles, (size_t)((Bm + 127) / 128 + c.domains)));
     NET_TRY(dalloc(net, &net->n_tiles, 1));
-    NET_TRY(dalloc(net, &net->X[0], (size_t)Bm * nd));
-    NET_TRY(dalloc(net, &net->X[1], (size_t)Bm * nd));
-    NET_TRY(dalloc(net, &net->Fbuf, (size_t)Bm * c.n * c.k));
-    NET_TRY(dalloc(net, &net->H[0], (size_t)Bm * max_hidden));
-    NET_TRY(dalloc(net, &net->H[1], (size_t)Bm * max_hidden));
+    NET_TRY(dalloc_bytes(net, &net->X[0], es * (size_t)Bm * nd));
+    NET_TRY(dalloc_bytes(net, &net->X[1], es * (size_t)Bm * nd));
+    NET_TRY(dalloc_bytes(net, &net->Fbuf, es * (size_t)Bm * c.n * c.k));
+    NET_TRY(dalloc_bytes(net, &net->H[0], es * (size_t)Bm * max_hidden));
+    NET_TRY(dalloc_bytes(net, &net->H[1], es * (size_t)Bm * max_hidden));
     NET_TRY(build_plans(net));
     LAT_CUDA(cudaDeviceSynchronize());
 #undef NET_TRY
@@ -401,30 +424,44 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
         a.rows = batch->rows;
         a.offsets = batch->offsets;
         a.ids = batch->ids;
-        a.out_dtype = LATTICE_BF16;
+        a.out_dtype = net->f32 ? LATTICE_F32 : LATTICE_BF16;
         a.out = net->X[0];
         a.out_row_stride = nd;
         a.out_feature_offset = 0;
         a.sample_pos = net->pos;
         a.normalize = 1;
         a.check = 0;
+        a.sources = 1;
         FWD_TRY(lattice_embedding_bag(&a, stream));
     } else {
         LAT_REQUIRE(batch->pooled != nullptr, "lattice_net_forward: need tables or pooled input");
         const int64_t warps = B * c.n;
         const unsigned grid = (unsigned)((warps * 32 + 255) / 256 < 148 * 64 ? (warps * 32 + 255) / 256 : 148 * 64);
         if (batch->pooled_layout == 1) {
-            LAT_REQUIRE(batch->shards >= 1 && c.n % batch->shards == 0 && batch->table_dtype == LATTICE_BF16,
-                        "lattice_net_forward: sharded pooled input needs bf16 and shards dividing n");
-            shard_gather_kernel<<<grid, 256, 0, stream>>>(B, c.n, c.d, batch->shards,
-                                                          static_cast<const __nv_bfloat16*>(batch->pooled),
-                                                          net->pos, net->X[0]);
-        } else if (batch->table_dtype == LATTICE_F32)
-            pooled_norm_kernel<float><<<grid, 256, 0, stream>>>(B, c.n, c.d, static_cast<const float*>(batch->pooled),
-                                                               net->pos, net->X[0]);
-        else
-            pooled_norm_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>(
-                B, c.n, c.d, static_cast<const __nv_bfloat16*>(batch->pooled), net->pos, net->X[0]);
+            LAT_REQUIRE(batch->shards >= 1 && c.n % batch->shards == 0 &&
+                            batch->table_dtype == (net->f32 ? LATTICE_F32 : LATTICE_BF16),
+                        "lattice_net_forward: sharded pooled input needs the net dtype and shards dividing n");
+            shard_gather_kernel<<<grid, 256, 0, stream>>>(B, c.n, c.d, (int)net->es, batch->shards,
+                                                          static_cast<const uint8_t*>(batch->pooled), net->pos,
+                                                          static_cast<uint8_t*>(net->X[0]));
+        } else if (batch->table_dtype == LATTICE_F32) {
+            if (net->f32)
+                pooled_norm_kernel<float, float><<<grid, 256, 0, stream>>>(
+                    B, c.n, c.d, static_cast<const float*>(batch->pooled), net->pos, static_cast<float*>(net->X[0]));
+            else
+                pooled_norm_kernel<float, __nv_bfloat16><<<grid, 256, 0, stream>>>(
+                    B, c.n, c.d, static_cast<const float*>(batch->pooled), net->pos,
+                    static_cast<__nv_bfloat16*>(net->X[0]));
+        } else {
+            if (net->f32)
+                pooled_norm_kernel<__nv_bfloat16, float><<<grid, 256, 0, stream>>>(
+                    B, c.n, c.d, static_cast<const __nv_bfloat16*>(batch->pooled), net->pos,
+                    static_cast<float*>(net->X[0]));
+            else
+                pooled_norm_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, stream>>>(
+                    B, c.n, c.d, static_cast<const __nv_bfloat16*>(batch->pooled), net->pos,
+                    static_cast<__nv_bfloat16*>(net->X[0]));
+        }
         LAT_CUDA(cudaGetLastError());
     }
     FWD_TRY(mark());

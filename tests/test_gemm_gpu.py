@@ -31,6 +31,30 @@ def test_store_fp32(M, N, K):
     torch.testing.assert_close(C, ref, rtol=1e-4, atol=1e-4)
 
 
+@pytest.mark.parametrize("M,N,K,epi", [(300, 512, 256, 0), (257, 512, 520, 1), (130, 256, 64, 3)])
+def test_tf32_path(M, N, K, epi):
+    """fp32 operands on kind::tf32: compare against fp32 math on TF32-rounded inputs."""
+    import torch
+    import paper_2512_09200_b200 as L
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    A = torch.randn((M, K), generator=g, device="cuda")
+    B = torch.randn((N, K), generator=g, device="cuda") / K ** 0.5
+    tf = lambda x: (x.view(torch.int32) & ~0x1FFF).view(torch.float32)  # truncation bound
+    ref = tf(A).double() @ tf(B).double().t()
+    if epi == 0:
+        C = L.gemm(A, B, out_dtype=torch.float32)
+        torch.testing.assert_close(C.double(), ref, rtol=2e-3, atol=2e-3)
+    elif epi == 1:
+        C = L.gemm(A, B, epilogue=L.EPI_SWISH, out_dtype=torch.float32)
+        torch.testing.assert_close(C.double(), ref_swish(ref.float()).double(), rtol=5e-3, atol=5e-3)
+    else:
+        R = torch.randn((M, N), device="cuda")
+        C = L.gemm(A, B, epilogue=L.EPI_RESID_NORM, resid=R, group=128, out_dtype=torch.float32)
+        z = (ref.float() + R).view(M, N // 128, 128)
+        want = (z / torch.sqrt((z * z).mean(-1, keepdim=True) + 1e-6)).view(M, N)
+        torch.testing.assert_close(C, want, rtol=5e-3, atol=5e-3)
+
+
 def test_store_bf16():
     import torch
     import paper_2512_09200_b200 as L

@@ -20,12 +20,12 @@ SMALL = dict(n=64, d=128, blocks=2, nF=32, nL=32, k=16, mlp=[1024, 512, 4096], d
              heads=4, tower_hidden=256)
 
 
-def build(cfg, B, rows, max_len=40, hard=False):
+def build(cfg, B, rows, max_len=40, hard=False, dtype="bf16"):
     import torch
     import paper_2512_09200_b200 as L
-    net = L.Network(**cfg, hard=hard, max_batch=B, weight_seed=SEED_W)
+    net = L.Network(**cfg, hard=hard, max_batch=B, weight_seed=SEED_W, dtype=dtype)
     n, d = cfg["n"], cfg["d"]
-    tab = torch.empty((n, rows, d), dtype=torch.bfloat16, device="cuda")
+    tab = torch.empty((n, rows, d), dtype=torch.float32 if dtype == "f32" else torch.bfloat16, device="cuda")
     L.fill_tables(tab, SEED_T)
     ptrs = torch.tensor([t.data_ptr() for t in tab.unbind(0)], dtype=torch.int64, device="cuda")
     rws = torch.full((n,), rows, dtype=torch.int64, device="cuda")
@@ -34,7 +34,7 @@ def build(cfg, B, rows, max_len=40, hard=False):
     return net, tab, ptrs, rws, offsets, ids, dom
 
 
-def oracle_logits(net, cfg, rows, offsets, ids, dom, samples, hard=False):
+def oracle_logits(net, cfg, rows, offsets, ids, dom, samples, hard=False, bf16=True):
     n, d = cfg["n"], cfg["d"]
     B = dom.shape[0]
     o_cpu = offsets.cpu().numpy()
@@ -48,7 +48,8 @@ def oracle_logits(net, cfg, rows, offsets, ids, dom, samples, hard=False):
     c.n_mlp = len(cfg["mlp"]) - 1
     for i, v in enumerate(cfg["mlp"]):
         c.mlp[i] = v
-    c.G, c.heads, c.tower_hidden, c.hard, c.bf16 = cfg["domains"], cfg["heads"], cfg["tower_hidden"], int(hard), 1
+    c.G, c.heads, c.tower_hidden, c.hard = cfg["domains"], cfg["heads"], cfg["tower_hidden"], int(hard)
+    c.bf16 = 1 if bf16 else 0
     keep = [np.ascontiguousarray(a, dtype=np.float32) for a in w["YT"] + w["WL"] + w["mlp"]]
     nb = cfg["blocks"]
     P = oracle.ctypes.c_void_p
@@ -101,6 +102,24 @@ def test_forward_matches_oracle(name, cfg, B, rows, hard):
     got = logits.cpu().numpy()[samples]
     assert np.isfinite(got).all()
     assert_logits_close(got, want)
+
+
+def test_tiny_config_fp32_tf32_matches_oracle():
+    """BASELINE configs[0] in its stated dtype: fp32 storage, kind::tf32 tensor cores, against
+    the fp64 oracle with fp32 storage rounding. Tolerance (TF32, 10-bit mantissa products):
+    |gpu - oracle| <= 5e-3 + 5e-3 * |oracle|."""
+    import torch
+    B, rows = 512, 10000
+    net, tab, ptrs, rws, offsets, ids, dom = build(TINY, B, rows, dtype="f32")
+    logits = net.forward(dom, offsets, ids, ptrs, rws, torch.float32)
+    torch.cuda.synchronize()
+    samples = list(range(0, B, 16)) + [B - 1]
+    want, w = oracle_logits(net, TINY, rows, offsets, ids, dom, samples, bf16=False)
+    check_weights_against_generator(w, TINY)
+    got = logits.cpu().numpy()[samples]
+    err = np.abs(got - want)
+    bound = 5e-3 + 5e-3 * np.abs(want)
+    assert (err <= bound).all(), f"max err {err.max():.4g}; rms logit {np.sqrt((want ** 2).mean()):.3g}"
 
 
 def test_mid_config_matches_oracle():
