@@ -266,10 +266,27 @@ def mlp_flops_per_sample(c):
     return 2 * sum(mlp[i] * mlp[i + 1] for i in range(len(mlp) - 1))
 
 
+FULL_TASKS, FULL_WINDOWS = 4, [5400000, 86400000, 604800000]  # O = 4 objectives, {90min, 1d, 7d}
+
+
+LARGE = dict(n=512, d=128, blocks=4, nF=256, nL=256, k=32, mlp=[16384, 2048, 2048, 32768],
+             domains=4, heads=6, tower_hidden=512)
+LARGE_ROWS, LARGE_B = 1_500_000, 65536  # 512 x 1.5M x 128 bf16 = 196.6 GB: needs >= 2 GPUs
+
+
 def run_mid(args, rank, world, local):
     import torch
     import paper_2512_09200_b200 as L
-    c = MID
+    full = args.workload == "full"
+    large = args.workload == "large"
+    global MID_ROWS, MID_B
+    if large:  # configs[3]: table-wise sharded over >= 2 GPUs, B = 64k per GPU
+        if world < 2:
+            raise SystemExit("--workload large needs >= 2 GPUs (196 GB of tables)")
+        MID_ROWS, MID_B = LARGE_ROWS, LARGE_B
+    # full consolidated portfolio: 16 domains, heads = 4 objectives x 3 attribution windows,
+    # Zipper window assignment + window-routed heads in every step (mid-width backbone)
+    c = dict(MID, domains=16, heads=FULL_TASKS * len(FULL_WINDOWS)) if full else (LARGE if large else MID)
     n, d, B = c["n"], c["d"], MID_B
     net = L.Network(**c, max_batch=B, weight_seed=SEED_W)
     sharded = world > 1
@@ -300,12 +317,22 @@ def run_mid(args, rank, world, local):
     logits = torch.empty((B, c["heads"]), dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
 
-    def forward(dm, off, ii, out):
+    if full:
+        imp = L.synth_impressions(B, FULL_TASKS, 7 + rank)
+        routed = torch.empty((B, FULL_TASKS), dtype=torch.float32, device="cuda")
+        wp = [1.0 / len(FULL_WINDOWS)] * len(FULL_WINDOWS)
+
+    def forward(dm, off, ii, out, imp_cols=None):
+        if full:  # K5: window assignment + per-window labels of this batch's impressions
+            win, _, _ = L.zipper_assign_labels(*(imp_cols or imp), FULL_WINDOWS, wp, 7, routed=True,
+                                               check_errors=False)
         if sharded:
             pooled = sb.forward_embeddings(off, ii, tables, ptrs, rows, send=send, recv=recv)
             net.forward(dm, pooled=pooled, shards=world, logits=out)
         else:
             net.forward(dm, off, ii, ptrs, rows, torch.bfloat16, logits=out)
+        if full:  # the window mask applied to the heads (training routes each sample's loss)
+            L.route_heads(out, win, FULL_TASKS, len(FULL_WINDOWS), out=routed)
 
     def step():
         forward(dom, offsets, ids, logits)
@@ -367,6 +394,9 @@ def run_mid(args, rank, world, local):
     h_out = torch.empty((B, c["heads"]), dtype=torch.float32, pin_memory=True)
     bufs = [(torch.empty_like(offsets), torch.empty(n_ids, dtype=torch.int32, device="cuda"),
              torch.empty_like(dom)) for _ in range(2)]
+    if full:  # the impression log columns travel with the batch too
+        h_imp = [t.cpu().pin_memory() for t in imp]
+        d_imp = [[torch.empty_like(t) for t in imp] for _ in range(2)]
     cstream = torch.cuda.Stream()
     copied = [torch.cuda.Event() for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
@@ -378,6 +408,9 @@ def run_mid(args, rank, world, local):
             o.copy_(h_off, non_blocking=True)
             ii.copy_(h_ids, non_blocking=True)
             dm.copy_(h_dom, non_blocking=True)
+            if full:
+                for dst, src in zip(d_imp[i % 2], h_imp):
+                    dst.copy_(src, non_blocking=True)
             copied[i % 2].record(cstream)
 
     def e2e_run(k):
@@ -389,7 +422,7 @@ def run_mid(args, rank, world, local):
                 h2d(i + 1)
             stream.wait_event(copied[i % 2])
             o, ii, dm = bufs[i % 2]
-            forward(dm, o, ii, logits)
+            forward(dm, o, ii, logits, d_imp[i % 2] if full else None)
             consumed[i % 2].record(stream)
             h_out.copy_(logits, non_blocking=True)
 
@@ -407,20 +440,36 @@ def run_mid(args, rank, world, local):
     if sharded:
         sb.check_overflow()
         launches += 2  # owner bag kernel + offsets scan (the bag slot above is the shard gather)
+    if full:
+        launches += 2  # zipper_kernel + route_heads_kernel
+    if full:
+        metric = "Lattice Network samples/sec (full consolidated portfolio, forward step)"
+        wl = ("full consolidated portfolio: 16 domains x (4 objectives x 3 windows {90min,1d,7d}) "
+              "heads, per-sample Zipper window assignment (seed 7, p=1/3) + window-routed heads each step; "
+              "mid-width backbone (256 sparse feats x 100k rows x 128, l=4, MLP 8192-2048-2048-16384, "
+              "tower 32768-512-12), B=32768/GPU")
+    elif large:
+        metric = "Lattice Network samples/sec (large config, forward step)"
+        wl = ("large Lattice Network: 512 tables x 1.5M rows x 128 bf16 (196.6 GB) table-wise sharded, "
+              "l=4 DWFB blocks (n=512, nF=nL=256, k=32, MLP 16384-2048-2048-32768), 4 domains x 6 heads, "
+              "tower 65536-512-6, B=65536/GPU")
+    else:
+        metric = "Lattice Network samples/sec (mid config, forward step)"
+        wl = ("mid Lattice Network: 256 sparse feats x 100k rows x 128, l=4 DWFB blocks (nF=nL=128, k=32, "
+              "MLP 8192-2048-2048-16384), 4 domains x 6 heads, tower 32768-512-6, B=32768/GPU")
     res = {
-        "metric": "Lattice Network samples/sec (mid config, forward step)",
+        "metric": metric,
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (counter-based tables/bags/weights)",
-        "config": {"workload": "mid Lattice Network: 256 sparse feats x 100k rows x 128, l=4 DWFB "
-                               "blocks (nF=nL=128, k=32, MLP 8192-2048-2048-16384), 4 domains x 6 "
-                               "heads, tower 32768-512-6, B=32768/GPU",
+        "config": {"workload": wl,
                    "global_batch": world * B, "ids_per_step": n_ids,
                    "l2": "embedding rows drawn uniformly from 6.6 GB of tables; activations 2.1 GB/buffer (> L2)",
                    "parallelism": (f"table-wise sharded embeddings over {world} GPUs (ids + pooled "
                                    f"all-to-all, NCCL/NVLink) + dense replicas") if sharded else "1 GPU"},
         "e2e": {"value": world * B / (e2e_ms / 1e3), "unit": "samples/s",
-                "h2d_bytes_per_step": (n * B + 1) * 8 + n_ids * 4 + B * 4,
+                "h2d_bytes_per_step": (n * B + 1) * 8 + n_ids * 4 + B * 4 +
+                                      (sum(t.numel() * t.element_size() for t in imp) if full else 0),
                 "d2h_bytes_per_step": B * c["heads"] * 4},
         "roofline": {"bound": "tensor", "achieved": mlp_achieved, "peak": tf_sust, "unit": "TFLOP/s",
                      "frac": mlp_achieved / tf_sust, "traffic": None,
@@ -533,7 +582,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="mid", choices=["mid", "micro"])
+    ap.add_argument("--workload", default="mid", choices=["mid", "full", "large", "micro"])
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"], help="micro table dtype")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -545,12 +594,12 @@ def main():
         if rank != 0:
             return
         per_step = max(0.5, min(3.0, 60.0 / (args.warmup + args.steps)))
-        base = cpu_baseline_mid if args.workload == "mid" else cpu_baseline_micro
+        base = cpu_baseline_mid if args.workload in ("mid", "full") else cpu_baseline_micro
         steps = [base(seconds=per_step) for _ in range(args.warmup + args.steps)]
         v = statistics.median([s["value"] for s in steps[args.warmup:]])
         cb = dict(steps[-1])
         cb["value"] = v
-        if args.workload == "mid":
+        if args.workload in ("mid", "full"):
             metric = "Lattice Network samples/sec (mid config, forward step)"
             wl = ("mid Lattice Network (CPU oracle port, fp64 with bf16 rounding emulation): "
                   "256 sparse feats x 100k rows x 128, l=4, B=32768")
@@ -568,14 +617,14 @@ def main():
         return
 
     rank, world, local = dist_setup(args.gpus)
-    if args.workload == "mid":
+    if args.workload in ("mid", "full", "large"):
         res = run_mid(args, rank, world, local)
         base = cpu_baseline_mid
     else:
         res, _ = run_micro(args, rank, world, local)
         base = cpu_baseline_micro
     if rank == 0:
-        if world == 1:
+        if world == 1 and args.workload != "large":
             res["cpu_baseline"] = base(args.cpu_seconds)
         print(json.dumps(res))
     if world > 1:

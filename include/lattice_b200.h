@@ -147,6 +147,18 @@ lattice_status lattice_fill_weights(void* w, int32_t dtype, int64_t out_features
 lattice_status lattice_synth_bags(int32_t features, int64_t batch, int32_t max_len, int64_t rows,
                                   uint64_t seed, int64_t* offsets, int32_t* ids,
                                   lattice_stream stream);
+/* Impression log columns for the Zipper: user i = "u%08d" of H mod 1e8
+ * (9 bytes), ad i = "a%06d" of H mod 1e6 (7 bytes), ts = 1.7e12 + 37 i, task t converts with
+ * probability 0.3 after a delay H mod 8 days. user_bytes [9n], ad_bytes [7n], offsets [n+1],
+ * ts [n], conv/present [n][tasks]. */
+lattice_status lattice_synth_impressions(int64_t n, int32_t tasks, uint64_t seed, uint8_t* user_bytes,
+                                         int64_t* user_off, uint8_t* ad_bytes, int64_t* ad_off,
+                                         int64_t* ts, int64_t* conv, uint8_t* present,
+                                         lattice_stream stream);
+/* Per-sample attribution-window routing of the heads:
+ * out[b][t] = logits[b][t*windows + window[b]]. */
+lattice_status lattice_route_heads(int64_t batch, int32_t tasks, int32_t windows, const float* logits,
+                                   const uint8_t* window, float* out, lattice_stream stream);
 lattice_status lattice_synth_domains(int64_t batch, int32_t domains, uint64_t seed,
                                      int32_t* domain, lattice_stream stream);
 

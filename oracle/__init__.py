@@ -83,6 +83,8 @@ def load_oracle():
         lib.lo_synth_domains.argtypes = [_I64, ctypes.c_int, _U64, _P]
         lib.lo_fill_weights.restype = None
         lib.lo_fill_weights.argtypes = [_P, _I64, _I64, _U64, _U64]
+        lib.lo_synth_impressions.restype = None
+        lib.lo_synth_impressions.argtypes = [_I64, ctypes.c_int, _U64, _P, _P, _P, _P, _P, _P, _P]
         lib.lo_bf16_round.restype = ctypes.c_float
         lib.lo_bf16_round.argtypes = [ctypes.c_float]
         _oracle = lib
@@ -214,3 +216,19 @@ def bf16_round(x):
     u = x.view(np.uint32).astype(np.uint64)
     r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
     return r.view(np.float32)
+
+
+def synth_impressions(n, T, seed):
+    """Host copy of lattice_synth_impressions: (users list[bytes], ads list[bytes], ts, conv, present)."""
+    ub = np.zeros(9 * n, np.uint8)
+    ab = np.zeros(7 * n, np.uint8)
+    uo = np.zeros(n + 1, np.int64)
+    ao = np.zeros(n + 1, np.int64)
+    ts = np.zeros(n, np.int64)
+    conv = np.zeros((n, T), np.int64)
+    pres = np.zeros((n, T), np.uint8)
+    load_oracle().lo_synth_impressions(n, T, seed, ptr(ub), ptr(uo), ptr(ab), ptr(ao), ptr(ts),
+                                       ptr(conv), ptr(pres))
+    users = [ub[9 * i: 9 * i + 9].tobytes() for i in range(n)]
+    ads = [ab[7 * i: 7 * i + 7].tobytes() for i in range(n)]
+    return users, ads, ts, conv, pres

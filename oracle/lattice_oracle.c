@@ -444,3 +444,27 @@ void lo_fill_weights(float* out, int64_t out_features, int64_t fan_in, uint64_t 
     for (int64_t i = 0; i < n; ++i)
         out[i] = ldexpf((float)(int8_t)(lo_gen(seed, tag, (uint64_t)i) >> 56), -shift);
 }
+
+/* Impression columns exactly as lattice_synth_impressions (fixed-width decimal ids). */
+void lo_synth_impressions(int64_t n, int T, uint64_t seed, uint8_t* ub, int64_t* uo, uint8_t* ab, int64_t* ao,
+                          int64_t* ts, int64_t* conv, uint8_t* pres) {
+    const uint64_t tag_user = 0x55534552ull, tag_ad = 0x41442020ull, tag_p = 0x43565020ull, tag_d = 0x43564420ull;
+    for (int64_t i = 0; i < n; ++i) {
+        uint64_t u = lo_gen(seed, tag_user, (uint64_t)i) % 100000000ull;
+        uint64_t a = lo_gen(seed, tag_ad, (uint64_t)i) % 1000000ull;
+        ub[9 * i] = 'u';
+        for (int k = 8; k >= 1; --k, u /= 10) ub[9 * i + k] = (uint8_t)('0' + u % 10);
+        ab[7 * i] = 'a';
+        for (int k = 6; k >= 1; --k, a /= 10) ab[7 * i + k] = (uint8_t)('0' + a % 10);
+        uo[i] = 9 * i;
+        ao[i] = 7 * i;
+        ts[i] = 1700000000000ll + 37 * i;
+        for (int t = 0; t < T; ++t) {
+            const uint64_t k = (uint64_t)i * T + t;
+            pres[k] = (uint8_t)(lo_gen(seed, tag_p, k) % 10 < 3);
+            conv[k] = ts[i] + (int64_t)(lo_gen(seed, tag_d, k) % (8ull * 86400000ull));
+        }
+    }
+    uo[n] = 9 * n;
+    ao[n] = 7 * n;
+}

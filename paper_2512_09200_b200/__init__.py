@@ -106,6 +106,8 @@ _sig("lattice_synth_domains", ctypes.c_int, [_I64, _I32, _U64, _P, _P])
 _sig("lattice_domain_bucket", ctypes.c_int, [_I64, _I32, _P, _P, _P, _P, _P])
 _sig("lattice_lengths_to_offsets", ctypes.c_int, [_I64, _P, _P, _P])
 _sig("lattice_pack_slices", ctypes.c_int, [_I32, _P, _P, _I64, _P, _P, _P])
+_sig("lattice_synth_impressions", ctypes.c_int, [_I64, _I32, _U64, _P, _P, _P, _P, _P, _P, _P, _P])
+_sig("lattice_route_heads", ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _P])
 _sig("lattice_gemm", ctypes.c_int, [ctypes.POINTER(GemmArgs), _P])
 _sig("lattice_net_create", ctypes.c_int, [ctypes.POINTER(NetConfig), ctypes.POINTER(_P)])
 _sig("lattice_net_destroy", None, [_P])
@@ -119,7 +121,8 @@ EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_versio
            "lattice_stable_hash", "lattice_zipper_validate", "lattice_zipper_assign_labels",
            "lattice_embedding_bag", "lattice_rownorm", "lattice_fill_tables",
            "lattice_fill_weights", "lattice_synth_bags", "lattice_synth_domains",
-           "lattice_domain_bucket", "lattice_lengths_to_offsets", "lattice_pack_slices", "lattice_gemm",
+           "lattice_domain_bucket", "lattice_lengths_to_offsets", "lattice_pack_slices",
+           "lattice_synth_impressions", "lattice_route_heads", "lattice_gemm",
            "lattice_net_create", "lattice_net_destroy",
            "lattice_net_weight", "lattice_net_forward", "lattice_net_set_timing",
            "lattice_net_stage_times"]
@@ -175,6 +178,33 @@ def zipper_assign_labels(user_bytes, user_off, ad_bytes, ad_off, ts, conv, conv_
                 1 if check_errors else 0)
     check(_lib.lattice_zipper_assign_labels(ctypes.byref(a), _stream(stream)))
     return win, lab, rt
+
+
+def synth_impressions(n, tasks, seed, device="cuda", stream=None):
+    """Synthetic impression log columns (device): (user_bytes, user_off, ad_bytes, ad_off, ts,
+    conv [n,T], present [n,T])."""
+    import torch
+    kw = dict(device=device)
+    ub = torch.empty(9 * n, dtype=torch.uint8, **kw)
+    uo = torch.empty(n + 1, dtype=torch.int64, **kw)
+    ab = torch.empty(7 * n, dtype=torch.uint8, **kw)
+    ao = torch.empty(n + 1, dtype=torch.int64, **kw)
+    ts = torch.empty(n, dtype=torch.int64, **kw)
+    conv = torch.empty((n, tasks), dtype=torch.int64, **kw)
+    pres = torch.empty((n, tasks), dtype=torch.uint8, **kw)
+    check(_lib.lattice_synth_impressions(n, tasks, seed, _p(ub), _p(uo), _p(ab), _p(ao), _p(ts),
+                                         _p(conv), _p(pres), _stream(stream)))
+    return ub, uo, ab, ao, ts, conv, pres
+
+
+def route_heads(logits, window, tasks, windows, out=None, stream=None):
+    """out[b][t] = logits[b][t*windows + window[b]] (the Zipper window mask applied to heads)."""
+    import torch
+    B = logits.shape[0]
+    if out is None:
+        out = torch.empty((B, tasks), dtype=torch.float32, device=logits.device)
+    check(_lib.lattice_route_heads(B, tasks, windows, _p(logits), _p(window), _p(out), _stream(stream)))
+    return out
 
 
 def stable_hash(bytes_, off, seed, stream=None):
@@ -399,8 +429,9 @@ class Network:
         wdt = torch.float32 if c["dtype"] in ("f32", "fp32", "float32") else torch.bfloat16
         out = {"YT": [], "WL": [], "mlp": []}
         for blk in range(c["blocks"]):
-            yt = _view(_lib.lattice_net_weight(self._h, blk, 1, 0), (_pad16(k), _pad16(n)), wdt)
-            wl = _view(_lib.lattice_net_weight(self._h, blk, 2, 0), (128, _pad16(n)), wdt)
+            n_pad = (n + 255) // 256 * 256 if n > 256 else _pad16(n)
+            yt = _view(_lib.lattice_net_weight(self._h, blk, 1, 0), (_pad16(k), n_pad), wdt)
+            wl = _view(_lib.lattice_net_weight(self._h, blk, 2, 0), (256 if nL > 128 else 128, n_pad), wdt)
             out["YT"].append(yt[:k, :n].float().cpu().numpy().copy())
             out["WL"].append(wl[:nL, :n].float().cpu().numpy().copy())
             for li in range(len(c["mlp"]) - 1):

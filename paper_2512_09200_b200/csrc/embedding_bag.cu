@@ -36,6 +36,7 @@ struct BagParams {
     int32_t R;  // source ranks: bags laid out [R][F][B]
     int64_t slice_cap;  // > 0: source r's ids start at r * slice_cap (static exchange buffer)
     unsigned long long* counter;  // work-claim counter (zeroed per launch)
+    int32_t l2keep;  // 1: table rows loaded with an L2 evict_last policy
 };
 
 // [s, e) of bag `bag` in the ids array (CSR, or CSR rebased into fixed per-source slices)
@@ -56,6 +57,20 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
     return r;
+}
+// Table rows with an L2 evict_last policy: rows of the table being pooled are re-read by
+// other bags a few microseconds later, while ids/offsets/outputs stream through once.
+__device__ __forceinline__ uint4 ld_row_keep(const void* p, uint64_t pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 
 template <typename T>
@@ -133,6 +148,8 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
     if (bag >= total) return;
     int64_t chunk_end = bag + kChunk < total ? bag + kChunk : total;
     const int sub = lane / LPR, cl = lane % LPR;
+    const bool keep = p.l2keep != 0;
+    const uint64_t pol = policy_evict_last();
     int64_t s, e;
     bag_range(p, bag, s, e);
     int first_id = lane < (e - s) ? __ldg(p.ids + s + lane) : 0;
@@ -171,7 +188,9 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
                 const TT* row = table + (int64_t)(ok[u] ? id : 0) * p.D;
 #pragma unroll
                 for (int c = 0; c < CPL; ++c)
-                    v[u][c] = ok[u] ? ld_stream(row + (c * LPR + cl) * EPC) : make_uint4(0, 0, 0, 0);
+                    v[u][c] = !ok[u] ? make_uint4(0, 0, 0, 0)
+                              : keep   ? ld_row_keep(row + (c * LPR + cl) * EPC, pol)
+                                       : ld_stream(row + (c * LPR + cl) * EPC);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u)
@@ -249,6 +268,15 @@ void launch_one(const BagParams& p, cudaStream_t st, int row_bytes) {
             bag_kernel<TT, OT, LPR, CPL, 8, 3>
                 <<<persistent_grid(bag_kernel<TT, OT, LPR, CPL, 8, 3>, bags), kBagWarps * 32, 0, st>>>(p);
     }
+}
+
+int bag_l2keep() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("LATTICE_BAG_L2KEEP");
+        v = e ? std::atoi(e) : 0;
+    }
+    return v;
 }
 
 template <typename TT, typename OT>
@@ -475,7 +503,8 @@ lattice_status lattice_embedding_bag(const lattice_bag_args* a, lattice_stream s
     LAT_CUDA(cudaMemsetAsync(err + 1, 0, sizeof(*err), stream));
     BagParams p{a->features, a->batch, a->dim, a->tables, a->rows, a->offsets, a->ids, a->out,
                 a->out_row_stride, a->out_feature_offset, a->sample_pos, a->normalize, err,
-                a->sources > 1 ? a->sources : 1, a->slice_cap > 0 ? a->slice_cap : 0, err + 1};
+                a->sources > 1 ? a->sources : 1, a->slice_cap > 0 ? a->slice_cap : 0, err + 1,
+                bag_l2keep()};
     lattice_status st;
     if (a->table_dtype == LATTICE_F32)
         st = a->out_dtype == LATTICE_F32 ? launch_bag<float, float>(p, row_bytes, stream)

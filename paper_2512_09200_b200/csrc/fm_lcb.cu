@@ -398,7 +398,286 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) tc::tmem_dealloc(tmem, tcols);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Large-n variant (256 < n <= 512, nL <= 256, d = 128, bf16): X_b (128 KB) fits only once, and
+// W_L (nL x n, up to 256 KB) cannot stay resident, so W_L streams from L2 through a TMA ring of
+// [128 x 64] panels (shared by every CTA, it stays L2-resident). Accumulators: P | L (2 M-tiles)
+// | F (4 M-tiles) in one TMEM region. Same warp roles as the resident variant.
+// ---------------------------------------------------------------------------------------------
+constexpr int kWlStages = 3;
+
+struct GeoL {
+    int panels_n, ml, mf;
+    uint32_t xpanel, ytpanel, ppanel, wlpanel;
+    __host__ __device__ GeoL(const Params& p) {
+        panels_n = p.n_pad / 64;
+        ml = (p.nL + 127) / 128;
+        mf = p.n_pad / 128;
+        xpanel = (uint32_t)p.n_pad * 128u;
+        ytpanel = (uint32_t)p.k_pad * 128u;
+        ppanel = (uint32_t)p.k_pad * 128u;
+        wlpanel = 128u * 128u;
+    }
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    fm_lcb_large_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWL,
+                        const __grid_constant__ CUtensorMap tmYT, const Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int npad = p.n_pad, kpad = p.k_pad;
+    constexpr int d = 128;
+    const GeoL g(p);
+    uint8_t* sX = smem;                                   // [2 panels][n_pad][64]
+    uint8_t* sWL = sX + 2 * g.xpanel;                     // ring [kWlStages][128][64]
+    uint8_t* sYT = sWL + kWlStages * g.wlpanel;           // [panels_n][k_pad][64]
+    uint8_t* sP = sYT + g.ytpanel * g.panels_n;           // [2 panels][k_pad][64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + ((2 * g.ppanel + 1023u) & ~1023u));
+    uint64_t* x_full = bars;
+    uint64_t* x_empty = bars + 1;
+    uint64_t* pl_full = bars + 2;
+    uint64_t* f_full = bars + 3;
+    uint64_t* tmem_empty = bars + 4;
+    uint64_t* w_full = bars + 5;
+    uint64_t* pbuf_full = bars + 6;
+    uint64_t* wl_full = bars + 7;               // [kWlStages]
+    uint64_t* wl_empty = wl_full + kWlStages;   // [kWlStages]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wl_empty + kWlStages);
+    float* red_f = reinterpret_cast<float*>(wl_empty + kWlStages + 1);  // [2][4]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        tc::tma_prefetch(&tmX);
+        tc::tma_prefetch(&tmWL);
+        tc::tma_prefetch(&tmYT);
+        tc::mbar_init(x_full, 1);
+        tc::mbar_init(x_empty, kEpiThreads);
+        tc::mbar_init(pl_full, 1);
+        tc::mbar_init(f_full, 1);
+        tc::mbar_init(tmem_empty, kEpiThreads);
+        tc::mbar_init(w_full, 1);
+        tc::mbar_init(pbuf_full, 128);
+        for (int i = 0; i < kWlStages; ++i) {
+            tc::mbar_init(&wl_full[i], 1);
+            tc::mbar_init(&wl_empty[i], 1);
+        }
+        tc::fence_mbar_init();
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t t_Pb = tmem, t_Lb = tmem + 64, t_Fb = tmem + 64 + 128 * 2;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer: X (4 boxes), then the W_L panel stream
+            tc::mbar_expect_tx(w_full, g.ytpanel * g.panels_n);
+            for (int pn = 0; pn < g.panels_n; ++pn) tc::tma_load_2d(sYT + pn * g.ytpanel, &tmYT, w_full, pn * 64, 0);
+            int it = 0, gw = 0;
+            for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
+                tc::mbar_wait(x_empty, (it & 1) ^ 1);
+                tc::mbar_expect_tx(x_full, (uint32_t)npad * 128u * 2u);
+                for (int pd = 0; pd < 2; ++pd)
+                    for (int h = 0; h < npad / 256; ++h)
+                        tc::tma_load_3d(sX + pd * g.xpanel + h * 256 * 128, &tmX, x_full, pd * 64, h * 256, (int)b);
+                for (int mt = 0; mt < g.ml; ++mt)
+                    for (int kp = 0; kp < g.panels_n; ++kp, ++gw) {
+                        const int s = gw % kWlStages;
+                        tc::mbar_wait(&wl_empty[s], ((gw / kWlStages) & 1) ^ 1);
+                        tc::mbar_expect_tx(&wl_full[s], g.wlpanel);
+                        tc::tma_load_2d(sWL + s * g.wlpanel, &tmWL, &wl_full[s], kp * 64, mt * 128);
+                    }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            const uint32_t id_P = tc::idesc_bf16(128, kpad, 1, 0);
+            const uint32_t id_L = tc::idesc_bf16(128, d, 0, 1);
+            const uint32_t id_F = tc::idesc_bf16(128, kpad, 0, 0);
+            tc::mbar_wait(w_full, 0);
+            const uint32_t yt = tc::smem_u32(sYT), pb = tc::smem_u32(sP), xs = tc::smem_u32(sX);
+            const uint32_t wl0 = tc::smem_u32(sWL);
+            int it = 0, gw = 0;
+            for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
+                tc::mbar_wait(x_full, it & 1);
+                tc::mbar_wait(tmem_empty, (it & 1) ^ 1);
+                tc::fence_after();
+                for (int kk = 0; kk < npad / 16; ++kk) {  // P = X^T Y
+                    const int k0 = kk * 16;
+                    const uint64_t a_xt = tc::sdesc(xs + k0 * 128, g.xpanel, 1024, 2);
+                    const uint64_t b_y = tc::sdesc(yt + (k0 / 64) * g.ytpanel + (k0 % 64) * 2, 16, 1024, 2);
+                    tc::mma_f16(t_Pb, a_xt, b_y, id_P, kk != 0);
+                }
+                for (int mt = 0; mt < g.ml; ++mt)  // L = W_L X, W_L streamed
+                    for (int kp = 0; kp < g.panels_n; ++kp, ++gw) {
+                        const int s = gw % kWlStages;
+                        tc::mbar_wait(&wl_full[s], (gw / kWlStages) & 1);
+                        tc::fence_after();
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int k0 = kp * 64 + j * 16;
+                            const uint64_t a_wl = tc::sdesc(wl0 + s * g.wlpanel + j * 32, 16, 1024, 2);
+                            const uint64_t b_x = tc::sdesc(xs + k0 * 128, g.xpanel, 1024, 2);
+                            tc::mma_f16(t_Lb + mt * 128, a_wl, b_x, id_L, (kp | j) != 0);
+                        }
+                        tc::mma_commit(&wl_empty[s]);
+                    }
+                tc::mma_commit(pl_full);
+                tc::mbar_wait(pbuf_full, it & 1);
+                tc::fence_after();
+                for (int mt = 0; mt < g.mf; ++mt)  // F = X P
+                    for (int kk = 0; kk < d / 16; ++kk) {
+                        const int k0 = kk * 16;
+                        const uint32_t pan = (uint32_t)(k0 / 64), kin = (uint32_t)(k0 % 64) * 2;
+                        const uint64_t a_x = tc::sdesc(xs + pan * g.xpanel + mt * 16384 + kin, 16, 1024, 2);
+                        const uint64_t b_p = tc::sdesc(pb + pan * g.ppanel + kin, 16, 1024, 2);
+                        tc::mma_f16(t_Fb + mt * kpad, a_x, b_p, id_F, kk != 0);
+                    }
+                tc::mma_commit(f_full);
+            }
+        }
+    } else if (warp < 6) {  // ---- LCB group: P -> Pbuf, then the L rows (2 M-tiles)
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const float inv_d = 1.0f / (float)d;
+        int it = 0;
+        for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
+            tc::mbar_wait(pl_full, it & 1);
+            tc::fence_after();
+            for (int c0 = 0; c0 < kpad; c0 += 16) {
+                float pv[16];
+                tc::tmem_ld16(t_Pb + lane_off + c0, pv);
+                uint8_t* pan = sP + (row / 64) * g.ppanel;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    *reinterpret_cast<__nv_bfloat16*>(pan + swz<2>(c0 + j, row & 63)) = __float2bfloat16_rn(pv[j]);
+            }
+            tc::fence_async_shared();
+            tc::mbar_arrive(pbuf_full);
+            for (int mt = 0; mt < g.ml; ++mt) {
+                const int i = mt * 128 + row;
+                const bool live = i < p.nL;
+                const int xr = p.nF + i;
+                const uint32_t t_L = t_Lb + lane_off + mt * 128;
+                float ss = 0.0f;
+#pragma unroll
+                for (int c = 0; c < d; c += 32) {
+                    float v[32];
+                    tc::tmem_ld32(t_L + c, v);
+                    if (live) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 8) {
+                            const uint4 r = *reinterpret_cast<const uint4*>(sX + ((c + j) / 64) * g.xpanel +
+                                                                            swz<2>(xr, (c + j) & 63));
+                            const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const float a = v[j + 2 * k] + bf16_lo(w[k]), bb = v[j + 2 * k + 1] + bf16_hi(w[k]);
+                                ss += a * a + bb * bb;
+                            }
+                        }
+                    }
+                }
+                const float inv = 1.0f / sqrtf(ss * inv_d + 1e-6f);
+                __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.Xout) + (b * p.n + xr) * (int64_t)d;
+#pragma unroll
+                for (int c = 0; c < d; c += 32) {
+                    float v[32];
+                    tc::tmem_ld32(t_L + c, v);
+                    if (live) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 8) {
+                            const uint4 r = *reinterpret_cast<const uint4*>(sX + ((c + j) / 64) * g.xpanel +
+                                                                            swz<2>(xr, (c + j) & 63));
+                            const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+                            uint32_t o[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                o[k] = pack_bf16x2((v[j + 2 * k] + bf16_lo(w[k])) * inv,
+                                                   (v[j + 2 * k + 1] + bf16_hi(w[k])) * inv);
+                            *reinterpret_cast<uint4*>(dst + c + j) = make_uint4(o[0], o[1], o[2], o[3]);
+                        }
+                    }
+                }
+            }
+            tc::mbar_arrive(x_empty);  // residual reads done
+            tc::fence_before();
+            tc::mbar_arrive(tmem_empty);
+        }
+    } else {  // ---- FM group: Fin = rms_norm(flatten(X P)) over 4 M-tiles, two TMEM passes
+        const int q = warp & 3;
+        const int e = warp - 6;
+        const int row = q * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const float inv_nk = 1.0f / (float)(p.n * p.k);
+        int it = 0;
+        for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
+            tc::mbar_wait(f_full, it & 1);
+            tc::fence_after();
+            tc::mbar_arrive(x_empty);  // every MMA reading X has completed
+            float ss = 0.0f;
+            for (int mt = 0; mt < g.mf; ++mt) {
+                const int r = mt * 128 + row;
+                for (int c0 = 0; c0 < kpad; c0 += 16) {
+                    float v[16];
+                    tc::tmem_ld16(t_Fb + lane_off + mt * kpad + c0, v);
+                    if (r < p.n) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (c0 + j < p.k) ss += v[j] * v[j];
+                    }
+                }
+            }
+            ss = warp_sum(ss);
+            float* red = red_f + (it & 1) * 4;
+            if (lane == 0) red[e] = ss;
+            tc::named_bar(2, 128);
+            const float inv = 1.0f / sqrtf((red[0] + red[1] + red[2] + red[3]) * inv_nk + 1e-6f);
+            for (int mt = 0; mt < g.mf; ++mt) {
+                const int r = mt * 128 + row;
+                for (int c0 = 0; c0 < kpad; c0 += 16) {
+                    float v[16];
+                    tc::tmem_ld16(t_Fb + lane_off + mt * kpad + c0, v);
+                    if (r < p.n) {
+                        __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.Fout) + b * (int64_t)p.n * p.k +
+                                             (int64_t)r * p.k + c0;
+                        if ((p.k & 15) == 0) {
+                            float o[8];
+#pragma unroll
+                            for (int j = 0; j < 16; j += 8) {
+#pragma unroll
+                                for (int k = 0; k < 8; ++k) o[k] = v[j + k] * inv;
+                                Store<__nv_bfloat16>::row8(dst + j, o);
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                if (c0 + j < p.k) dst[j] = __float2bfloat16_rn(v[j] * inv);
+                        }
+                    }
+                }
+            }
+            tc::fence_before();
+            tc::mbar_arrive(tmem_empty);
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+size_t smem_bytes_large(const Params& p) {
+    const GeoL g(p);
+    return 1024 + 2 * (size_t)g.xpanel + kWlStages * (size_t)g.wlpanel + (size_t)g.ytpanel * g.panels_n +
+           ((2 * (size_t)g.ppanel + 1023) & ~size_t(1023)) + 256;
+}
+
+bool is_large(const Params& p) { return p.n_pad > 256; }
+
 size_t smem_bytes(const Params& p) {
+    if (is_large(p)) return smem_bytes_large(p);
     const Geo g(p, p.f32 ? 4 : 2);
     size_t s = 1024;
     s += (size_t)g.wlpanel * g.panels_n;   // W_L
@@ -414,10 +693,19 @@ lattice_status check(const Params& p) {
     if (p.f32 ? p.d != 64 : !(p.d == 64 || p.d == 128))
         return set_error(LATTICE_USAGE, "fm_lcb: d must be 64 or 128 (bf16), 64 (fp32)");
     if (p.f32 && p.n_pad > 64) return set_error(LATTICE_USAGE, "fm_lcb: fp32 supports n <= 64");
-    if (p.n < 1 || p.n_pad > 256 || p.n_pad % 16 || p.n_pad < p.n)
-        return set_error(LATTICE_USAGE, "fm_lcb: n must be <= 256");
     if (p.k < 1 || p.k_pad > 64 || p.k_pad % 16 || p.k_pad < p.k)
         return set_error(LATTICE_USAGE, "fm_lcb: k must be <= 64");
+    if (is_large(p)) {  // streamed-W_L variant
+        if (p.f32 || p.d != 128 || p.n_pad > 512 || p.n_pad % 256 || p.n_pad < p.n)
+            return set_error(LATTICE_USAGE, "fm_lcb: n in (256, 512] needs bf16, d = 128 and n_pad = 512");
+        if (p.nL < 0 || p.nL > 256 || p.nF + p.nL != p.n)
+            return set_error(LATTICE_USAGE, "fm_lcb: nL must be <= 256 and nF + nL == n");
+        if (64 + 256 + (p.n_pad / 128) * p.k_pad > 512)
+            return set_error(LATTICE_USAGE, "fm_lcb: n = 512 needs k <= 48 (TMEM)");
+        if (smem_bytes(p) > 227 * 1024) return set_error(LATTICE_USAGE, "fm_lcb: shared memory budget exceeded");
+        return LATTICE_OK;
+    }
+    if (p.n < 1 || p.n_pad % 16 || p.n_pad < p.n) return set_error(LATTICE_USAGE, "fm_lcb: bad n");
     if (p.nL < 0 || p.nL > 128 || p.nF + p.nL != p.n)
         return set_error(LATTICE_USAGE, "fm_lcb: nL must be <= 128 and nF + nL == n");
     if (region_cols(p) > 512) return set_error(LATTICE_USAGE, "fm_lcb: accumulators exceed TMEM");
@@ -439,14 +727,15 @@ lattice_status make_maps(Plan* pl, const void* X, const void* WLpad, const void*
     }
     cuuint64_t dims[3] = {(cuuint64_t)p.d, (cuuint64_t)p.n, (cuuint64_t)p.B};
     cuuint64_t strides[2] = {(cuuint64_t)p.d * es, (cuuint64_t)p.n * p.d * es};
-    cuuint32_t box[3] = {(cuuint32_t)ep, (cuuint32_t)p.n_pad, 1};
+    // TMA boxes hold at most 256 rows: the large variant loads X in two row halves
+    cuuint32_t box[3] = {(cuuint32_t)ep, (cuuint32_t)(p.n_pad > 256 ? 256 : p.n_pad), 1};
     cuuint32_t el[3] = {1, 1, 1};
     CUresult r = fn(&pl->tmX, p.f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                     const_cast<void*>(X), dims, strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_error(LATTICE_CUDA, "fm_lcb: X tensor map (" + std::to_string((int)r) + ")");
-    lattice_status s = gemm::make_map_2d(&pl->tmWL, WLpad, (uint64_t)p.n_pad, 128, (uint64_t)p.n_pad * es, ep, 128,
-                                         p.f32);
+    lattice_status s = gemm::make_map_2d(&pl->tmWL, WLpad, (uint64_t)p.n_pad, (uint64_t)wl_rows(p),
+                                         (uint64_t)p.n_pad * es, ep, 128, p.f32);
     if (s != LATTICE_OK) return s;
     return gemm::make_map_2d(&pl->tmYT, YTpad, (uint64_t)p.n_pad, (uint64_t)p.k_pad, (uint64_t)p.n_pad * es, ep,
                              (uint32_t)p.k_pad, p.f32);
@@ -467,8 +756,22 @@ lattice_status launch_t(const Plan& pl, cudaStream_t st) {
 }
 
 lattice_status launch(const Plan& pl, cudaStream_t st) {
+    if (is_large(pl.p)) {
+        static bool attr = false;
+        if (!attr) {
+            LAT_CUDA(cudaFuncSetAttribute(fm_lcb_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            attr = true;
+        }
+        const int grid = (int)(pl.p.B < num_sms() ? pl.p.B : num_sms());
+        if (grid <= 0) return LATTICE_OK;
+        fm_lcb_large_kernel<<<grid, kThreads, smem_bytes(pl.p), st>>>(pl.tmX, pl.tmWL, pl.tmYT, pl.p);
+        LAT_CUDA(cudaGetLastError());
+        return LATTICE_OK;
+    }
     return pl.p.f32 ? launch_t<float>(pl, st) : launch_t<__nv_bfloat16>(pl, st);
 }
+
+int wl_rows(const Params& p) { return p.nL > 128 ? 256 : 128; }
 
 }  // namespace fm
 }  // namespace lat

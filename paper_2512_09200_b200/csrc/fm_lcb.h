@@ -24,11 +24,13 @@ struct Plan {
     Params p;
 };
 
-// X: [B][n][d]. WLpad: [128][n_pad] (rows >= nL zero). YTpad: [k_pad][n_pad]. Same dtype.
+// X: [B][n][d]. WLpad: [wl_rows][n_pad] (rows >= nL zero). YTpad: [k_pad][n_pad]. Same dtype.
 lattice_status check(const Params& p);
 lattice_status make_maps(Plan* pl, const void* X, const void* WLpad, const void* YTpad);
 lattice_status launch(const Plan& pl, cudaStream_t st);
 size_t smem_bytes(const Params& p);
+// rows of the padded W_L buffer the plan expects: 128 (nL <= 128) or 256
+int wl_rows(const Params& p);
 
 }  // namespace fm
 }  // namespace lat

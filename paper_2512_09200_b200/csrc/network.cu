@@ -168,12 +168,14 @@ lattice_status validate(const lattice_net_config* c) {
     if (!c) return set_error(LATTICE_USAGE, "lattice_net_create: null config");
     if (c->dtype != LATTICE_BF16 && c->dtype != LATTICE_F32)
         return set_error(LATTICE_USAGE, "network: dtype must be bf16 or f32");
-    if (c->n < 1 || c->n > 256) return set_error(LATTICE_USAGE, "network: n must be in [1, 256]");
+    if (c->n < 1 || c->n > 512) return set_error(LATTICE_USAGE, "network: n must be in [1, 512]");
+    if (c->n > 256 && (c->dtype != LATTICE_BF16 || c->d != 128))
+        return set_error(LATTICE_USAGE, "network: n > 256 needs bf16 and d = 128");
     if (c->d != 64 && c->d != 128) return set_error(LATTICE_USAGE, "network: d must be 64 or 128");
     if (c->dtype == LATTICE_F32 && c->d != 64) return set_error(LATTICE_USAGE, "network: fp32 needs d = 64");
     if (c->blocks < 1) return set_error(LATTICE_USAGE, "network: need at least one block");
-    if (c->nF < 1 || c->nL < 0 || c->nF + c->nL != c->n || c->nL > 128)
-        return set_error(LATTICE_USAGE, "network: need nF >= 1, nL <= 128 and nF + nL == n");
+    if (c->nF < 1 || c->nL < 0 || c->nF + c->nL != c->n || c->nL > (c->n > 256 ? 256 : 128))
+        return set_error(LATTICE_USAGE, "network: need nF >= 1, nF + nL == n, nL <= 128 (<= 256 when n > 256)");
     if (c->k < 1 || c->k > 64) return set_error(LATTICE_USAGE, "network: k must be in [1, 64]");
     if (c->n_mlp < 1 || c->n_mlp > 5) return set_error(LATTICE_USAGE, "network: n_mlp must be in [1, 5]");
     if (c->mlp[0] != c->n * c->k) return set_error(LATTICE_USAGE, "network: mlp[0] must equal n*k");
@@ -281,7 +283,7 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
     net->f32 = c.dtype == LATTICE_F32;
     net->es = net->f32 ? 4 : 2;
     const int wdt = net->f32 ? LATTICE_F32 : LATTICE_BF16;
-    net->n_pad = round_up(c.n, 16);
+    net->n_pad = c.n > 256 ? round_up(c.n, 256) : round_up(c.n, 16);  // large variant: 512
     net->k_pad = round_up(c.k, 16);
     const int nd = c.n * c.d;
     const int64_t Bm = c.max_batch;
@@ -298,11 +300,12 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
     const uint64_t seed = c.weight_seed;
     for (int blk = 0; blk < c.blocks; ++blk) {
         void *yt = nullptr, *wl = nullptr;
+        const int wlr = c.nL > 128 ? 256 : 128;  // padded W_L rows (fm::wl_rows)
         NET_TRY(dalloc_bytes(net, &yt, es * (size_t)net->k_pad * net->n_pad));
-        NET_TRY(dalloc_bytes(net, &wl, es * (size_t)128 * net->n_pad));
+        NET_TRY(dalloc_bytes(net, &wl, es * (size_t)wlr * net->n_pad));
         NET_TRY(fill_padded(net, yt, c.k, c.n, net->k_pad, net->n_pad, weight_tag(blk, 1, 0)));
-        NET_TRY(fill_padded(net, wl, c.nL > 0 ? c.nL : 1, c.n, 128, net->n_pad, weight_tag(blk, 2, 0)));
-        if (c.nL == 0) LAT_CUDA(cudaMemset(wl, 0, es * 128 * net->n_pad));
+        NET_TRY(fill_padded(net, wl, c.nL > 0 ? c.nL : 1, c.n, wlr, net->n_pad, weight_tag(blk, 2, 0)));
+        if (c.nL == 0) LAT_CUDA(cudaMemset(wl, 0, es * wlr * net->n_pad));
         net->YT.push_back(yt);
         net->WL.push_back(wl);
         for (int li = 0; li < c.n_mlp; ++li) {

@@ -92,10 +92,76 @@ __global__ void __launch_bounds__(256) zipper_kernel(
     }
 }
 
+constexpr uint64_t kTagUser = 0x55534552ull, kTagAd = 0x41442020ull, kTagConvP = 0x43565020ull,
+                   kTagConvD = 0x43564420ull;
+
+__device__ __forceinline__ void put_dec(uint8_t* dst, uint64_t v, int digits) {
+    for (int i = digits - 1; i >= 0; --i) {
+        dst[i] = (uint8_t)('0' + v % 10);
+        v /= 10;
+    }
+}
+
+__global__ void synth_impressions_kernel(int64_t n, int T, uint64_t seed, uint8_t* ub, int64_t* uo, uint8_t* ab,
+                                         int64_t* ao, int64_t* ts, int64_t* conv, uint8_t* pres) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        ub[9 * i] = 'u';
+        put_dec(ub + 9 * i + 1, gen_u64(seed, kTagUser, (uint64_t)i) % 100000000ull, 8);
+        ab[7 * i] = 'a';
+        put_dec(ab + 7 * i + 1, gen_u64(seed, kTagAd, (uint64_t)i) % 1000000ull, 6);
+        uo[i] = 9 * i;
+        ao[i] = 7 * i;
+        if (i == n - 1) {
+            uo[n] = 9 * n;
+            ao[n] = 7 * n;
+        }
+        const int64_t t0 = 1700000000000ll + 37 * i;
+        ts[i] = t0;
+        for (int t = 0; t < T; ++t) {
+            const uint64_t k = (uint64_t)i * T + t;
+            pres[k] = (uint8_t)(gen_u64(seed, kTagConvP, k) % 10 < 3);
+            conv[k] = t0 + (int64_t)(gen_u64(seed, kTagConvD, k) % (8ull * 86400000ull));
+        }
+    }
+}
+
+__global__ void route_heads_kernel(int64_t B, int T, int W, const float* __restrict__ logits,
+                                   const uint8_t* __restrict__ window, float* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B * T; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / T;
+        const int t = (int)(i - b * T);
+        out[i] = logits[b * (int64_t)T * W + (int64_t)t * W + window[b]];
+    }
+}
+
 }  // namespace
 }  // namespace lat
 
 extern "C" {
+
+lattice_status lattice_synth_impressions(int64_t n, int32_t T, uint64_t seed, uint8_t* ub, int64_t* uo, uint8_t* ab,
+                                         int64_t* ao, int64_t* ts, int64_t* conv, uint8_t* pres,
+                                         lattice_stream stream) {
+    LAT_REQUIRE(n > 0 && T >= 0 && ub && uo && ab && ao && ts && (T == 0 || (conv && pres)),
+                "synth_impressions: bad args");
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    lat::synth_impressions_kernel<<<(unsigned)blocks, 256, 0, stream>>>(n, T, seed, ub, uo, ab, ao, ts, conv, pres);
+    LAT_CUDA(cudaGetLastError());
+    return LATTICE_OK;
+}
+
+lattice_status lattice_route_heads(int64_t B, int32_t T, int32_t W, const float* logits, const uint8_t* window,
+                                   float* out, lattice_stream stream) {
+    LAT_REQUIRE(B >= 0 && T > 0 && W > 0 && W <= 255, "route_heads: bad sizes");
+    if (B == 0) return LATTICE_OK;
+    LAT_REQUIRE(logits && window && out, "route_heads: null pointer");
+    int64_t blocks = (B * T + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    lat::route_heads_kernel<<<(unsigned)blocks, 256, 0, stream>>>(B, T, W, logits, window, out);
+    LAT_CUDA(cudaGetLastError());
+    return LATTICE_OK;
+}
 
 lattice_status lattice_zipper_validate(int32_t W, const int64_t* dur, const double* p) {
     // datasets.hpp:60-84 (name checks live in the C++ shim)

@@ -122,6 +122,24 @@ def test_tiny_config_fp32_tf32_matches_oracle():
     assert (err <= bound).all(), f"max err {err.max():.4g}; rms logit {np.sqrt((want ** 2).mean()):.3g}"
 
 
+LARGE_N = dict(n=512, d=128, blocks=1, nF=256, nL=256, k=32, mlp=[16384, 256, 32768], domains=2,
+               heads=3, tower_hidden=256)
+
+
+def test_large_n_streamed_wl_matches_oracle():
+    """n = 512 / nL = 256 (the large config's backbone width) runs the streamed-W_L FM/LCB
+    variant; widths of the MLP/tower shrunk so the fp64 oracle stays fast."""
+    import torch
+    B, rows = 300, 4000
+    net, tab, ptrs, rws, offsets, ids, dom = build(LARGE_N, B, rows)
+    logits = net.forward(dom, offsets, ids, ptrs, rws, torch.bfloat16)
+    torch.cuda.synchronize()
+    samples = [0, 1, 150, 299]
+    want, w = oracle_logits(net, LARGE_N, rows, offsets, ids, dom, samples)
+    check_weights_against_generator(w, LARGE_N)
+    assert_logits_close(logits.cpu().numpy()[samples], want)
+
+
 def test_mid_config_matches_oracle():
     import torch
     B, rows = 2048, 20000

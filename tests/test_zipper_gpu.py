@@ -144,3 +144,25 @@ def test_empty_and_degenerate():
     empty = np.zeros((1000, 0), np.int64)
     w, _, _ = run_gpu(users, users, ts, empty, empty, [10, 20], [1.0, 0.0], 5)
     assert (w == 0).all()
+
+
+def test_synth_impressions_and_head_routing():
+    """Device impression generator == oracle generator; Zipper on it == oracle; the window
+    mask applied to heads picks logits[b][t*W + window[b]]."""
+    import torch
+    import paper_2512_09200_b200 as L
+    n, T, W = 20000, 4, 3
+    cols = L.synth_impressions(n, T, 7)
+    users, ads, ts, conv, pres = oracle.synth_impressions(n, T, 7)
+    assert cols[0].cpu().numpy().tobytes() == b"".join(users)
+    assert cols[2].cpu().numpy().tobytes() == b"".join(ads)
+    assert (cols[4].cpu().numpy() == ts).all() and (cols[5].cpu().numpy() == conv).all()
+    assert (cols[6].cpu().numpy() == pres).all()
+    dur, pr = [5400000, 86400000, 604800000], [1 / 3, 1 / 3, 1 / 3]
+    w, lab, rt = L.zipper_assign_labels(*cols, dur, pr, 7, routed=True)
+    ow, ol, err, _ = oracle.zip_columns(users, ads, ts, conv, pres, dur, pr, 7)
+    assert err == -1 and (w.cpu().numpy() == ow).all() and (lab.cpu().numpy() == ol).all()
+    logits = torch.randn((n, T * W), device="cuda")
+    routed = L.route_heads(logits, w, T, W)
+    idx = torch.arange(T, device="cuda")[None, :] * W + w.long()[:, None]
+    assert torch.equal(routed, torch.gather(logits, 1, idx))
