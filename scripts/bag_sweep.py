@@ -3,7 +3,7 @@ import os, subprocess, sys, json
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-def one(F, R, D, B, dt, variant, net_like=False):
+def one(F, R, D, B, dt, variant, net_like=False, keep=0):
     code = f"""
 import os, sys, torch, json
 sys.path.insert(0, {ROOT!r})
@@ -27,10 +27,16 @@ n = int(off[-1]); s = tab.element_size()
 by = n*{D}*s + n*4 + ({F}*{B}+1)*8 + {F}*{B}*{D}*s
 print(json.dumps(dict(ms=ms, GBs=by/ms/1e6)))
 """
-    env = dict(os.environ, LATTICE_BAG_VARIANT=str(variant))
+    env = dict(os.environ, LATTICE_BAG_VARIANT=str(variant), LATTICE_BAG_L2KEEP=str(keep))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     return r.stdout.strip() or r.stderr[-300:]
 
+if len(sys.argv) > 1 and sys.argv[1] == "l2":
+    for rows in (100000, 20000):
+        for keep in (0, 1):
+            print("mid_bf16 rows", rows, "keep", keep,
+                  one(256, rows, 128, 32768, "bfloat16", 2, True, keep), flush=True)
+    sys.exit(0)
 for name, cfg in [("micro_f32", (64, 1000000, 128, 16384, "float32")),
                   ("micro_bf16", (64, 1000000, 128, 16384, "bfloat16")),
                   ("mid_bf16", (256, 100000, 128, 32768, "bfloat16"))]:
