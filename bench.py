@@ -289,15 +289,20 @@ def run_mid(args, rank, world, local):
     c = dict(MID, domains=16, heads=FULL_TASKS * len(FULL_WINDOWS)) if full else (LARGE if large else MID)
     n, d, B = c["n"], c["d"], MID_B
     net = L.Network(**c, max_batch=B, weight_seed=SEED_W)
-    sharded = world > 1
+    sharded = world > 1 or args.exchange == "peer1"  # peer1: the peer path at N=1 (experiments)
+    peer = sharded and args.exchange in ("peer", "peer1")
     if sharded:  # table-wise: this rank owns features [rank*n/W, (rank+1)*n/W)
         from paper_2512_09200_b200.sharded import ShardedBags
         sb = ShardedBags(n, B, d, world, rank)
         n_tab = sb.Fl
         tab = torch.empty((n_tab, MID_ROWS, d), dtype=torch.bfloat16, device="cuda")
         L.fill_tables(tab, SEED_T, feature_base=sb.owned()[0], rows_total=MID_ROWS)
-        send = torch.empty((world * B, sb.Fl, d), dtype=torch.bfloat16, device="cuda")
-        recv = torch.empty_like(send)
+        if peer:  # owners write pooled rows straight into every rank's X0 over NVLink
+            from paper_2512_09200_b200.peer import PeerBags
+            pb = PeerBags(net, n, B, d, world, rank)
+        else:
+            send = torch.empty((world * B, sb.Fl, d), dtype=torch.bfloat16, device="cuda")
+            recv = torch.empty_like(send)
     else:
         n_tab = n
         tab = torch.empty((n, MID_ROWS, d), dtype=torch.bfloat16, device="cuda")
@@ -308,7 +313,9 @@ def run_mid(args, rank, world, local):
     offsets, ids = L.synth_bags(n, B, MID_MAXLEN, MID_ROWS, SEED_D + rank)
     dom = L.synth_domains(B, c["domains"], SEED_D + rank)
     n_ids = int(offsets[-1].item())
-    if sharded:  # static exchange capacity (setup, outside the timed region): max slice over ranks
+    if peer:
+        pb.register("main", offsets, ids)
+    elif sharded:  # static exchange capacity (setup, outside the timed region): max slice over ranks
         import torch.distributed as dist
         cnt, _ = sb.slice_counts(offsets)
         cap = cnt.max().reshape(1)
@@ -316,6 +323,7 @@ def run_mid(args, rank, world, local):
         sb.capacity = int(cap.item())
     logits = torch.empty((B, c["heads"]), dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
+    key_of = {id(offsets): "main"}  # peer exchange: input buffer pair -> registered key
 
     if full:
         imp = L.synth_impressions(B, FULL_TASKS, 7 + rank)
@@ -326,7 +334,9 @@ def run_mid(args, rank, world, local):
         if full:  # K5: window assignment + per-window labels of this batch's impressions
             win, _, _ = L.zipper_assign_labels(*(imp_cols or imp), FULL_WINDOWS, wp, 7, routed=True,
                                                check_errors=False)
-        if sharded:
+        if peer:
+            pb.forward(key_of[id(off)], dm, tables, ptrs, rows, logits=out)
+        elif sharded:
             pooled = sb.forward_embeddings(off, ii, tables, ptrs, rows, send=send, recv=recv)
             net.forward(dm, pooled=pooled, shards=world, logits=out)
         else:
@@ -357,9 +367,19 @@ def run_mid(args, rank, world, local):
 
     # per-stage device times (separate pass, events between stages)
     net.set_timing(True)
-    stages, emb_ms = [], []
+    stages, emb_ms, peer_split = [], [], []
     for _ in range(5):
-        if sharded:  # ids a2a + owner pooling + pooled a2a, timed on the stream
+        if peer:  # bucket + barrier + owner kernel (NVLink reads/stores) + barrier
+            barrier(world)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            pb.forward_embeddings("main", dom, tables, ptrs, rows, timed=True)
+            a1.record(stream)
+            net.forward_in_place(dom, logits=logits)
+            torch.cuda.synchronize()
+            emb_ms.append(a0.elapsed_time(a1))
+            peer_split.append(pb.stage_ms())
+        elif sharded:  # ids a2a + owner pooling + pooled a2a, timed on the stream
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record(stream)
             pooled = sb.forward_embeddings(offsets, ids, tables, ptrs, rows, send=send, recv=recv)
@@ -394,6 +414,10 @@ def run_mid(args, rank, world, local):
     h_out = torch.empty((B, c["heads"]), dtype=torch.float32, pin_memory=True)
     bufs = [(torch.empty_like(offsets), torch.empty(n_ids, dtype=torch.int32, device="cuda"),
              torch.empty_like(dom)) for _ in range(2)]
+    if peer:  # the double-buffered H2D destinations are published to the owners once
+        for i, (o, ii, _) in enumerate(bufs):
+            pb.register(i, o, ii)
+            key_of[id(o)] = i
     if full:  # the impression log columns travel with the batch too
         h_imp = [t.cpu().pin_memory() for t in imp]
         d_imp = [[torch.empty_like(t) for t in imp] for _ in range(2)]
@@ -437,7 +461,10 @@ def run_mid(args, rank, world, local):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
 
     launches = 3 + c["blocks"] * (1 + len(c["mlp"]) - 1) + 1
-    if sharded:
+    if peer:
+        pb.check()
+        launches += 2  # two barrier kernels (the bag slot above is the owner kernel)
+    elif sharded:
         sb.check_overflow()
         launches += 2  # owner bag kernel + offsets scan (the bag slot above is the shard gather)
     if full:
@@ -465,8 +492,12 @@ def run_mid(args, rank, world, local):
         "config": {"workload": wl,
                    "global_batch": world * B, "ids_per_step": n_ids,
                    "l2": "embedding rows drawn uniformly from 6.6 GB of tables; activations 2.1 GB/buffer (> L2)",
-                   "parallelism": (f"table-wise sharded embeddings over {world} GPUs (ids + pooled "
-                                   f"all-to-all, NCCL/NVLink) + dense replicas") if sharded else "1 GPU"},
+                   "parallelism": ((f"table-wise sharded embeddings over {world} GPUs (owner kernel reads "
+                                    f"peers' ids and stores pooled rows into their X0 over NVLink via CUDA "
+                                    f"IPC, in-kernel barriers, no NCCL on the data path) + dense replicas")
+                                   if peer else
+                                   (f"table-wise sharded embeddings over {world} GPUs (ids + pooled "
+                                    f"all-to-all, NCCL/NVLink) + dense replicas")) if sharded else "1 GPU"},
         "e2e": {"value": world * B / (e2e_ms / 1e3), "unit": "samples/s",
                 "h2d_bytes_per_step": (n * B + 1) * 8 + n_ids * 4 + B * 4 +
                                       (sum(t.numel() * t.element_size() for t in imp) if full else 0),
@@ -492,6 +523,8 @@ def run_mid(args, rank, world, local):
         "gpu_launches": launches * args.steps,
         "clocks": clk.summary(),
     }
+    if peer:  # embedding stage split on rank 0: [bucket, barrier 1, owner kernel, barrier 2] ms
+        res["stages"]["embedding"]["peer_split_ms"] = [min(x[i] for x in peer_split) for i in range(4)]
     return res
 
 
@@ -586,6 +619,8 @@ def main():
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"], help="micro table dtype")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl", "peer1"],
+                    help="N>1 sharded embedding exchange: peer memory (default) or NCCL all-to-alls")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

@@ -110,6 +110,57 @@ typedef struct {
                                     the global CSR over [R][F][B], rebased per slice. */
 } lattice_bag_args;
 
+/* ======================================================================================
+ * Peer-memory sharded embedding bag (NVLink/NVSwitch; SURVEY.md 8e "K1 writes pooled rows
+ * straight into peers' receive buffers"). Replaces the three-step ids all-to-all -> owner
+ * pooling -> pooled all-to-all of lattice_embedding_bag(sources = R) with ONE kernel per
+ * owner: this rank owns global features [feature_base, feature_base + features_local); for
+ * every source rank r it reads r's CSR offsets / ids / sample_pos over NVLink (peer-mapped
+ * pointers from lattice_ipc_open), gathers its own table rows from local HBM, and stores the
+ * pooled (optionally rms-normalised) row at out[r][sample_pos[r][b]*out_row_stride +
+ * (feature_base + f)*dim] -- i.e. straight into source r's network X0. Must be bracketed by
+ * lattice_peer_barrier calls (see paper_2512_09200_b200/peer.py).
+ * ==================================================================================== */
+typedef struct {
+    int32_t rank, world;
+    int32_t features_local;      /* tables owned by this rank */
+    int32_t feature_base;        /* their first global feature index */
+    int64_t batch;               /* B per source rank */
+    int32_t dim;
+    int32_t table_dtype;
+    const void* const* tables;   /* DEVICE [features_local] local table pointers */
+    const int64_t* rows;         /* DEVICE [features_local] */
+    const int64_t* const* offsets;   /* DEVICE [world]: rank r's CSR offsets over all features
+                                        (feature-major, [F_total*B + 1]) */
+    const int32_t* const* ids;       /* DEVICE [world]: rank r's ids */
+    const int32_t* const* sample_pos;/* DEVICE [world]: output row of rank r's sample b */
+    void* const* out;                /* DEVICE [world]: rank r's output base */
+    int32_t out_dtype;
+    int64_t out_row_stride;      /* elements between output rows (>= F_total*dim) */
+    int32_t normalize;
+    int32_t check;               /* 1: synchronise; DATA error index = position in the
+                                    source's ids array */
+} lattice_peer_bag_args;
+
+lattice_status lattice_peer_embedding_bag(const lattice_peer_bag_args* args, lattice_stream stream);
+
+/* CUDA IPC between the one-process-per-GPU ranks. lattice_ipc_handle exports the allocation
+ * that contains dptr (any pointer inside a cudaMalloc'd block) as a 64-byte handle plus the
+ * byte offset of dptr in it; lattice_ipc_open maps a peer's handle (peer access over
+ * NVLink) and returns the pointer at `offset`; lattice_ipc_close unmaps it (reference
+ * counted per allocation). */
+#define LATTICE_IPC_HANDLE_BYTES 64
+lattice_status lattice_ipc_handle(const void* dptr, uint8_t* handle, int64_t* offset);
+lattice_status lattice_ipc_open(const uint8_t* handle, int64_t offset, void** dptr);
+lattice_status lattice_ipc_close(void* dptr);
+
+/* Stream-ordered cross-GPU barrier. flags: DEVICE array [world] of pointers (peer-mapped)
+ * to every rank's zero-initialised uint32 array of world + 1 words. All ranks must call it
+ * the same number of times; a rank that does not arrive within timeout_s seconds makes the
+ * kernel give up and set *status = 1 (DEVICE int32) instead of hanging the GPU. */
+lattice_status lattice_peer_barrier(uint32_t* const* flags, int32_t rank, int32_t world,
+                                    double timeout_s, int32_t* status, lattice_stream stream);
+
 /* Sender side of the static ids exchange: out[o][j] = ids[bounds[o] + j] for
  * j < bounds[o+1] - bounds[o] (o < slices); slices longer than cap set *overflow = 1.
  * All sizes are read on the device: no host synchronisation. */
@@ -239,9 +290,21 @@ typedef struct {
     int32_t pooled_layout;       /* 0: raw sums [B][n][d], caller order (the net normalises)
                                     1: table-wise shards [S][B][n/S][d] bf16, already
                                        rms-normalised by the owners (lattice_embedding_bag
-                                       with normalize = 1), S = shards */
+                                       with normalize = 1), S = shards
+                                    2: in place -- X0 (lattice_net_buffer 0) was already
+                                       written in domain-sorted order by
+                                       lattice_peer_embedding_bag after lattice_net_bucket
+                                       ran for this batch; `pooled` is ignored */
     int32_t shards;
 } lattice_batch;
+
+/* Domain bucketing of a batch ahead of the forward (pooled_layout 2): writes the
+ * domain-sorted row of every sample, readable through lattice_net_buffer(net, 1). */
+lattice_status lattice_net_bucket(lattice_net* net, int64_t batch, const int32_t* domain,
+                                  lattice_stream stream);
+/* Workspace pointers for peer export: 0 = X0 [max_batch][n][d] (net dtype, the embedding
+ * stage's output), 1 = sample_pos int32 [max_batch]. NULL for an unknown index. */
+void* lattice_net_buffer(lattice_net* net, int32_t which);
 
 /* logits: DEVICE fp32 [B][heads] in the caller's sample order. */
 lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch, float* logits,

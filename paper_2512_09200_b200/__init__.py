@@ -65,6 +65,13 @@ class BagArgs(ctypes.Structure):
                 ("slice_cap", _I64)]
 
 
+class PeerBagArgs(ctypes.Structure):
+    _fields_ = [("rank", _I32), ("world", _I32), ("features_local", _I32), ("feature_base", _I32),
+                ("batch", _I64), ("dim", _I32), ("table_dtype", _I32), ("tables", _P), ("rows", _P),
+                ("offsets", _P), ("ids", _P), ("sample_pos", _P), ("out", _P), ("out_dtype", _I32),
+                ("out_row_stride", _I64), ("normalize", _I32), ("check", _I32)]
+
+
 class GemmArgs(ctypes.Structure):
     _fields_ = [("M", _I64), ("N", _I64), ("K", _I64), ("A", _P), ("lda", _I64), ("B", _P),
                 ("ldb", _I64), ("C", _P), ("ldc", _I64), ("out_dtype", _I32), ("epilogue", _I32),
@@ -108,6 +115,13 @@ _sig("lattice_lengths_to_offsets", ctypes.c_int, [_I64, _P, _P, _P])
 _sig("lattice_pack_slices", ctypes.c_int, [_I32, _P, _P, _I64, _P, _P, _P])
 _sig("lattice_synth_impressions", ctypes.c_int, [_I64, _I32, _U64, _P, _P, _P, _P, _P, _P, _P, _P])
 _sig("lattice_route_heads", ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _P])
+_sig("lattice_peer_embedding_bag", ctypes.c_int, [ctypes.POINTER(PeerBagArgs), _P])
+_sig("lattice_ipc_handle", ctypes.c_int, [_P, _P, ctypes.POINTER(_I64)])
+_sig("lattice_ipc_open", ctypes.c_int, [_P, _I64, ctypes.POINTER(_P)])
+_sig("lattice_ipc_close", ctypes.c_int, [_P])
+_sig("lattice_peer_barrier", ctypes.c_int, [_P, _I32, _I32, ctypes.c_double, _P, _P])
+_sig("lattice_net_bucket", ctypes.c_int, [_P, _I64, _P, _P])
+_sig("lattice_net_buffer", _P, [_P, _I32])
 _sig("lattice_gemm", ctypes.c_int, [ctypes.POINTER(GemmArgs), _P])
 _sig("lattice_net_create", ctypes.c_int, [ctypes.POINTER(NetConfig), ctypes.POINTER(_P)])
 _sig("lattice_net_destroy", None, [_P])
@@ -125,7 +139,9 @@ EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_versio
            "lattice_synth_impressions", "lattice_route_heads", "lattice_gemm",
            "lattice_net_create", "lattice_net_destroy",
            "lattice_net_weight", "lattice_net_forward", "lattice_net_set_timing",
-           "lattice_net_stage_times"]
+           "lattice_net_stage_times", "lattice_peer_embedding_bag", "lattice_ipc_handle",
+           "lattice_ipc_open", "lattice_ipc_close", "lattice_peer_barrier", "lattice_net_bucket",
+           "lattice_net_buffer"]
 
 lib = _lib
 
@@ -242,6 +258,50 @@ def embedding_bag(tables, offsets, ids, batch, out=None, out_dtype=None, sample_
                 sources, slice_cap)
     check(_lib.lattice_embedding_bag(ctypes.byref(a), _stream(stream)))
     return out
+
+
+def peer_embedding_bag(rank, world, tables, table_ptrs, rows, feature_base, batch, offsets_ptrs,
+                       ids_ptrs, pos_ptrs, out_ptrs, out_row_stride, out_dtype=None, normalize=True,
+                       check_errors=False, stream=None):
+    """Owner side of the peer-memory sharded embedding stage (lattice_peer_embedding_bag):
+    the *_ptrs arguments are int64 CUDA tensors [world] of (peer-mapped) device pointers."""
+    import torch
+    D = tables[0].shape[1]
+    tdt = tables[0].dtype
+    odt = out_dtype or tdt
+    a = PeerBagArgs(rank, world, len(tables), feature_base, batch, D, F32 if tdt == torch.float32 else BF16,
+                    _p(table_ptrs), _p(rows), _p(offsets_ptrs), _p(ids_ptrs), _p(pos_ptrs), _p(out_ptrs),
+                    F32 if odt == torch.float32 else BF16, out_row_stride, 1 if normalize else 0,
+                    1 if check_errors else 0)
+    check(_lib.lattice_peer_embedding_bag(ctypes.byref(a), _stream(stream)))
+
+
+IPC_HANDLE_BYTES = 64
+
+
+def ipc_handle(ptr):
+    """-> (64-byte handle of the allocation holding device pointer `ptr`, byte offset)."""
+    buf = (ctypes.c_uint8 * IPC_HANDLE_BYTES)()
+    off = _I64()
+    check(_lib.lattice_ipc_handle(ctypes.c_void_p(int(ptr)), buf, ctypes.byref(off)))
+    return bytes(buf), off.value
+
+
+def ipc_open(handle, offset):
+    """Map a peer rank's exported allocation; returns the device pointer at `offset`."""
+    buf = (ctypes.c_uint8 * IPC_HANDLE_BYTES).from_buffer_copy(handle)
+    out = ctypes.c_void_p()
+    check(_lib.lattice_ipc_open(buf, offset, ctypes.byref(out)))
+    return out.value
+
+
+def ipc_close(ptr):
+    check(_lib.lattice_ipc_close(ctypes.c_void_p(int(ptr))))
+
+
+def peer_barrier(flag_ptrs, rank, world, status, timeout_s=30.0, stream=None):
+    """Stream-ordered cross-GPU barrier over peer-mapped flag arrays (lattice_peer_barrier)."""
+    check(_lib.lattice_peer_barrier(_p(flag_ptrs), rank, world, timeout_s, _p(status), _stream(stream)))
 
 
 def lengths_to_offsets(lengths, out=None, stream=None):
@@ -409,6 +469,31 @@ class Network:
         else:
             b.table_dtype = F32 if table_dtype == torch.float32 else BF16
             b.tables, b.rows, b.offsets, b.ids = _p(table_ptrs), _p(rows), _p(offsets), _p(ids)
+        check(_lib.lattice_net_forward(self._h, ctypes.byref(b), _p(logits), _stream(stream)))
+        return logits
+
+    def bucket(self, domain, stream=None):
+        """Domain bucketing ahead of an in-place forward (lattice_net_bucket)."""
+        check(_lib.lattice_net_bucket(self._h, domain.shape[0], _p(domain), _stream(stream)))
+
+    def buffer(self, which):
+        """Device pointer of a workspace buffer: 0 = X0, 1 = sample_pos (lattice_net_buffer)."""
+        p = _lib.lattice_net_buffer(self._h, which)
+        if not p:
+            raise UsageError(f"lattice_net_buffer: unknown buffer {which}")
+        return p
+
+    def forward_in_place(self, domain, logits=None, stream=None):
+        """Forward over an X0 already filled by lattice_peer_embedding_bag (pooled_layout 2)."""
+        import torch
+        B = domain.shape[0]
+        if logits is None:
+            logits = torch.empty((B, self.cfg["heads"]), dtype=torch.float32, device=domain.device)
+        b = Batch()
+        b.batch = B
+        b.domain = _p(domain)
+        b.table_dtype = F32 if self.cfg["dtype"] in ("f32", "fp32", "float32") else BF16
+        b.pooled_layout = 2
         check(_lib.lattice_net_forward(self._h, ctypes.byref(b), _p(logits), _stream(stream)))
         return logits
 

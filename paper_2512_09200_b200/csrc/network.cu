@@ -391,6 +391,27 @@ lattice_status lattice_net_stage_times(lattice_net* net, float* ms, int32_t max_
     return LATTICE_OK;
 }
 
+lattice_status lattice_net_bucket(lattice_net* net, int64_t batch, const int32_t* domain, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(net != nullptr && domain != nullptr, "lattice_net_bucket: null argument");
+    LAT_REQUIRE(batch >= 0 && batch <= net->cfg.max_batch, "lattice_net_bucket: batch exceeds max_batch");
+    if (batch == 0) return LATTICE_OK;
+    lattice_status s = lattice_domain_bucket(batch, net->cfg.domains, domain, net->pos, net->order, net->seg, stream);
+    if (s != LATTICE_OK) return s;
+    tiles_kernel<<<1, 256, 0, stream>>>(net->seg, net->cfg.domains, net->tiles, net->n_tiles);
+    LAT_CUDA(cudaGetLastError());
+    return LATTICE_OK;
+}
+
+void* lattice_net_buffer(lattice_net* net, int32_t which) {
+    if (!net) return nullptr;
+    switch (which) {
+        case 0: return net->X[0];
+        case 1: return net->pos;
+        default: return nullptr;
+    }
+}
+
 // Stage boundaries recorded when timing is on: [bucket, bag, (fm_lcb, mlp) x blocks, tower]
 lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch, float* logits,
                                    lattice_stream stream) {
@@ -412,12 +433,13 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
         lattice_status _s = (x);                  \
         if (_s != LATTICE_OK) return _s;          \
     } while (0)
+    const bool in_place = !batch->tables && batch->pooled_layout == 2;  // X0 written by peers
     FWD_TRY(mark());
-    FWD_TRY(lattice_domain_bucket(B, c.domains, batch->domain, net->pos, net->order, net->seg, stream));
-    tiles_kernel<<<1, 256, 0, stream>>>(net->seg, c.domains, net->tiles, net->n_tiles);
-    LAT_CUDA(cudaGetLastError());
+    if (!in_place) FWD_TRY(lattice_net_bucket(net, B, batch->domain, stream));
     FWD_TRY(mark());
-    if (batch->tables) {
+    if (in_place) {
+        // lattice_net_bucket ran for this batch and lattice_peer_embedding_bag filled X0
+    } else if (batch->tables) {
         lattice_bag_args a = {};
         a.features = c.n;
         a.batch = B;

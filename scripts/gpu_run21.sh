@@ -1,0 +1,9 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
+tail -5 gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -3 gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/bench_mid.json 2> gpurun_out/bench_mid.err; tail -c 600 gpurun_out/bench_mid.json
+timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; cat gpurun_out/bench_ref.json
+timeout 600 python bench.py --workload micro --dtype bf16 --cpu-seconds 2 > gpurun_out/bench_micro_bf16.json 2>&1
+echo done

@@ -54,7 +54,25 @@ def main():
     got2 = net.forward(dom, pooled=pooled2, shards=world)
     torch.cuda.synchronize()
     sb.check_overflow()
-    ok = torch.equal(got, ref) and torch.equal(got2, ref)
+    # peer-memory path (IPC over NVLink, one owner kernel, in-kernel barrier flags): the
+    # owners write straight into this rank's X0 -> same logits
+    from paper_2512_09200_b200.peer import PeerBags
+    pb = PeerBags(net, n, B, d, world, rank)
+    pb.register(0, off, ids)
+    got3 = pb.forward(0, dom, list(own.unbind(0)), optrs, orows).clone()
+    # a second batch buffer pair (the e2e double buffer) and repeated steps keep the barrier
+    # epochs in lock step
+    off_b, ids_b = off.clone(), ids.clone()
+    pb.register(1, off_b, ids_b)
+    for i in range(3):
+        got4 = pb.forward(i % 2, dom, list(own.unbind(0)), optrs, orows)
+    torch.cuda.synchronize()
+    pb.check()
+    ok3 = torch.equal(got3, ref) and torch.equal(got4, ref)
+    if not ok3:
+        print(f"rank {rank}: peer path mismatch, max |diff| = {(got3 - ref).abs().max().item()}")
+    pb.close()
+    ok = torch.equal(got, ref) and torch.equal(got2, ref) and ok3
     t = torch.tensor([0 if ok else 1], device="cuda")
     dist.all_reduce(t)
     if rank == 0:
