@@ -85,11 +85,13 @@ __device__ __forceinline__ void bag_range(const BagParams& p, uint32_t bag, cons
     } else {
         s = p.offsets[bag];
         e = p.offsets[bag + 1];
+        len = (int)(e - s);
         if (p.slice_cap > 0) {
             const int64_t r = bag / ((int64_t)p.F * p.B);
             s += r * p.slice_cap - p.offsets[r * p.F * p.B];
         }
         idp = p.ids + s;
+        return;
     }
     len = (int)(e - s);
 }

@@ -64,6 +64,32 @@ def test_normalize_permute_and_sharded_output():
     assert (got[:, :3] == 0).all() and (got[:, 7:] == 0).all()
 
 
+def test_sources_and_static_slices_match_compact_layout():
+    """Bags laid out [R][F][B] (sources = R, the owner side of the ids all-to-all), with ids in
+    a compact CSR or in fixed per-source slices (slice_cap): both equal R independent calls."""
+    import torch
+    import paper_2512_09200_b200 as L
+    F, rows, D, B, R = 3, 2000, 128, 301, 3
+    tab = torch.empty((F, rows, D), dtype=torch.bfloat16, device="cuda")
+    L.fill_tables(tab, SEED_T)
+    parts = [L.synth_bags(F, B, 40, rows, SEED_D + r) for r in range(R)]
+    want = torch.cat([L.embedding_bag(list(tab.unbind(0)), o, i, B) for o, i in parts])
+    # compact CSR over [R][F][B]
+    lens = torch.cat([o[1:] - o[:-1] for o, _ in parts])
+    off = torch.zeros(R * F * B + 1, dtype=torch.int64, device="cuda")
+    off[1:] = torch.cumsum(lens, 0)
+    ids = torch.cat([i[: int(o[-1])] for o, i in parts])
+    got = L.embedding_bag(list(tab.unbind(0)), off, ids, B, sources=R)
+    assert torch.equal(got, want)
+    # fixed slices: source r's ids at r * cap, offsets still the global CSR
+    cap = max(int(o[-1]) for o, _ in parts) + 7
+    sl = torch.full((R * cap,), -1, dtype=torch.int32, device="cuda")
+    for r, (o, i) in enumerate(parts):
+        sl[r * cap: r * cap + int(o[-1])] = i[: int(o[-1])]
+    got2 = L.embedding_bag(list(tab.unbind(0)), off, sl, B, sources=R, slice_cap=cap)
+    assert torch.equal(got2, want)
+
+
 def test_bad_id_reports_first_offender():
     import torch
     import paper_2512_09200_b200 as L
