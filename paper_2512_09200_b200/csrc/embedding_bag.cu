@@ -50,66 +50,6 @@ struct BagParams {
     int32_t src_foff;
 };
 
-// Bag numbering (32-bit: the host guarantees R * F * B < 2^31). Plain mode: [r][f][b].
-// Peer mode: [f][r][b] -- one table stays hot in L2 across all sources (measured faster on
-// 2 x B200 than interleaving the sources bag by bag).
-template <bool PEER>
-__device__ __forceinline__ void decode(const BagParams& p, uint32_t bag, int& f, int& r, uint32_t& b) {
-    const uint32_t R = (uint32_t)p.R, B = (uint32_t)p.B, F = (uint32_t)p.F;
-    if (PEER) {
-        const uint32_t fr = bag / B;
-        r = (int)(fr % R);
-        f = (int)(fr / R);
-        b = bag - fr * B;
-    } else {
-        const uint32_t rf = bag / B;
-        r = (int)(rf / F);
-        f = (int)(rf - (uint32_t)r * F);
-        b = bag - rf * B;
-    }
-}
-
-// First id and length of bag `bag` (CSR, CSR rebased into fixed per-source slices, or -- peer
-// mode -- the source rank's own CSR read over NVLink).
-template <bool PEER>
-__device__ __forceinline__ void bag_range(const BagParams& p, uint32_t bag, const int32_t*& idp, int& len) {
-    int64_t s, e;
-    if constexpr (PEER) {
-        int f, r;
-        uint32_t b;
-        decode<true>(p, bag, f, r, b);
-        const int64_t* off = p.p_off[r] + (int64_t)(p.src_foff + f) * p.B + b;
-        s = off[0];
-        e = off[1];
-        idp = p.p_ids[r] + s;
-    } else {
-        s = p.offsets[bag];
-        e = p.offsets[bag + 1];
-        len = (int)(e - s);
-        if (p.slice_cap > 0) {
-            const int64_t r = bag / ((int64_t)p.F * p.B);
-            s += r * p.slice_cap - p.offsets[r * p.F * p.B];
-        }
-        idp = p.ids + s;
-        return;
-    }
-    len = (int)(e - s);
-}
-
-// Position of id pointer q in the ids array it came from (DataError index; cold path).
-template <bool PEER>
-__device__ __forceinline__ unsigned long long id_position(const BagParams& p, uint32_t bag, const int32_t* q) {
-    if constexpr (PEER) {
-        int f, r;
-        uint32_t b;
-        decode<true>(p, bag, f, r, b);
-        return (unsigned long long)(q - p.p_ids[r]);
-    }
-    return (unsigned long long)(q - p.ids);
-}
-
-__device__ __align__(16) uint4 g_zero_row[64];  // 1 KB of zeros: the row of an invalid id
-
 __device__ __forceinline__ uint4 ld_stream(const void* p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -188,13 +128,71 @@ __device__ __forceinline__ void store_out<__nv_bfloat16, 8>(__nv_bfloat16* dst, 
 }
 
 constexpr int kBagWarps = 8;
+__device__ __align__(16) uint4 g_zero_row[64];  // 1 KB of zeros: the row of an invalid id
 
+// ---- direct kernel (single GPU and the NCCL-exchange owner side) ----------------------------
 // Persistent warps with dynamic scheduling: a warp claims kChunk consecutive bags at a time
 // from a global counter, so all warps stay inside a narrow window of the bag sequence -- the
 // sequence is table-major, so the live working set is about one table and repeated rows hit
 // in L2 instead of re-reading HBM. While the current bag's rows are in flight, the next bag's
-// offsets and first 32 ids are already being fetched, so the offsets -> ids -> rows chain of
-// one bag overlaps the row traffic of the previous one.
+// offsets and first 32 ids are already being fetched; with local offsets / ids, 40 warps per SM
+// hide the rest of that chain.
+namespace direct {
+template <bool PEER>
+__device__ __forceinline__ void decode(const BagParams& p, uint32_t bag, int& f, int& r, uint32_t& b) {
+    const uint32_t R = (uint32_t)p.R, B = (uint32_t)p.B, F = (uint32_t)p.F;
+    if (PEER) {
+        const uint32_t fr = bag / B;
+        r = (int)(fr % R);
+        f = (int)(fr / R);
+        b = bag - fr * B;
+    } else {
+        const uint32_t rf = bag / B;
+        r = (int)(rf / F);
+        f = (int)(rf - (uint32_t)r * F);
+        b = bag - rf * B;
+    }
+}
+
+// First id and length of bag `bag` (CSR, CSR rebased into fixed per-source slices, or -- peer
+// mode -- the source rank's own CSR read over NVLink).
+template <bool PEER>
+__device__ __forceinline__ void bag_range(const BagParams& p, uint32_t bag, const int32_t*& idp, int& len) {
+    int64_t s, e;
+    if constexpr (PEER) {
+        int f, r;
+        uint32_t b;
+        decode<true>(p, bag, f, r, b);
+        const int64_t* off = p.p_off[r] + (int64_t)(p.src_foff + f) * p.B + b;
+        s = off[0];
+        e = off[1];
+        idp = p.p_ids[r] + s;
+    } else {
+        s = p.offsets[bag];
+        e = p.offsets[bag + 1];
+        len = (int)(e - s);
+        if (p.slice_cap > 0) {
+            const int64_t r = bag / ((int64_t)p.F * p.B);
+            s += r * p.slice_cap - p.offsets[r * p.F * p.B];
+        }
+        idp = p.ids + s;
+        return;
+    }
+    len = (int)(e - s);
+}
+
+// Position of id pointer q in the ids array it came from (DataError index; cold path).
+template <bool PEER>
+__device__ __forceinline__ unsigned long long id_position(const BagParams& p, uint32_t bag, const int32_t* q) {
+    if constexpr (PEER) {
+        int f, r;
+        uint32_t b;
+        decode<true>(p, bag, f, r, b);
+        return (unsigned long long)(q - p.p_ids[r]);
+    }
+    return (unsigned long long)(q - p.ids);
+}
+
 constexpr int kChunk = 4;
 
 __device__ __forceinline__ uint32_t claim_chunk(unsigned long long* counter, int lane) {
@@ -326,6 +324,241 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
     if constexpr (PEER) __threadfence_system();
 }
 
+}  // namespace direct
+
+// ---- staged kernel (peer mode: offsets / ids / sample_pos read over NVLink) -------------------
+namespace staged {
+
+// Work item = a chunk of up to kChunk consecutive samples of one (source, table) segment, so
+// the chunk's offsets, ids and output rows are contiguous. Persistent warps claim chunks from
+// a global counter (all warps stay inside a narrow window of the segment sequence, which is
+// table-major, so the live working set is about one table and repeated rows hit in L2).
+// Each warp double-buffers chunk metadata in shared memory: while it gathers the rows of chunk
+// c, the ids and output rows of chunk c+1 are already in flight (cp.async) and the offsets of
+// chunk c+2 are being loaded -- the offsets -> ids -> rows chain of a chunk never sits on the
+// critical path, which matters most in peer mode where offsets / ids / sample_pos are read
+// from the source rank over NVLink.
+constexpr int kChunk = 4;
+constexpr int kIdsCap = 192;  // ids staged per chunk; longer chunks read the rest from global
+
+struct __align__(16) Stage {
+    int32_t off[kChunk + 1];  // bag starts relative to the chunk's first id
+    int32_t pos[kChunk];      // output row of each bag
+    int32_t f, r, b0, n;      // table, source, first sample, bags
+    const int32_t* idg;       // the chunk's first id in global memory
+    int32_t ids[kIdsCap];
+};
+
+__device__ __forceinline__ uint32_t claim_chunk(unsigned long long* counter, int lane) {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(counter, 1ull);
+    return (uint32_t)__shfl_sync(0xffffffffu, c, 0);
+}
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Chunk c -> segment and samples. Plain mode segments are [r][f] (the CSR order); peer mode
+// segments are [f][r] so one table is pooled for every source before the next. 32-bit: the
+// host guarantees R * F * B < 2^31.
+template <bool PEER>
+__device__ __forceinline__ void locate(const BagParams& p, uint32_t c, uint32_t cps, int& f, int& r, uint32_t& b0,
+                                       int& n) {
+    const uint32_t seg = c / cps;
+    b0 = (c - seg * cps) * kChunk;
+    n = (uint32_t)p.B - b0 < (uint32_t)kChunk ? (int)((uint32_t)p.B - b0) : kChunk;
+    if (PEER) {
+        f = (int)(seg / (uint32_t)p.R);
+        r = (int)(seg - (uint32_t)f * (uint32_t)p.R);
+    } else {
+        r = (int)(seg / (uint32_t)p.F);
+        f = (int)(seg - (uint32_t)r * (uint32_t)p.F);
+    }
+}
+
+// Offsets of chunk c's bags (lane i <= n holds the start of bag i / the end of the chunk).
+template <bool PEER>
+__device__ __forceinline__ int64_t chunk_offsets(const BagParams& p, uint32_t c, uint32_t cps, int lane) {
+    int f, r, n;
+    uint32_t b0;
+    locate<PEER>(p, c, cps, f, r, b0, n);
+    if (lane > n) return 0;
+    if (PEER) return p.p_off[r][(int64_t)(p.src_foff + f) * p.B + b0 + lane];
+    return p.offsets[((int64_t)r * p.F + f) * p.B + b0 + lane];
+}
+
+// Fill stage S for chunk c whose offsets are `o` (per lane, from chunk_offsets): header and
+// relative offsets by plain stores, ids and output rows by cp.async (one commit group).
+template <bool PEER>
+__device__ __forceinline__ void stage_chunk(const BagParams& p, Stage& S, uint32_t c, uint32_t cps, int64_t o,
+                                            int lane) {
+    int f, r, n;
+    uint32_t b0;
+    locate<PEER>(p, c, cps, f, r, b0, n);
+    const int64_t o0 = __shfl_sync(0xffffffffu, o, 0);
+    const int64_t oN = __shfl_sync(0xffffffffu, o, n);
+    const int32_t* idg;
+    if (PEER) {
+        idg = p.p_ids[r] + o0;
+    } else {
+        int64_t shift = 0;
+        if (p.slice_cap > 0) shift = r * p.slice_cap - p.offsets[(int64_t)r * p.F * p.B];
+        idg = p.ids + o0 + shift;
+    }
+    if (lane <= n) S.off[lane] = (int32_t)(o - o0);
+    if (lane == 0) {
+        S.f = f;
+        S.r = r;
+        S.b0 = (int32_t)b0;
+        S.n = n;
+        S.idg = idg;
+    }
+    const int cnt = (int)(oN - o0) < kIdsCap ? (int)(oN - o0) : kIdsCap;
+    for (int q = lane; q < cnt; q += 32) cp_async4(&S.ids[q], idg + q);
+    if (lane < n) {
+        if (PEER)
+            cp_async4(&S.pos[lane], p.p_pos[r] + b0 + lane);
+        else if (p.pos)
+            cp_async4(&S.pos[lane], p.pos + (int64_t)r * p.B + b0 + lane);
+        else
+            S.pos[lane] = (int32_t)((int64_t)r * p.B + b0 + lane);
+    }
+    cp_async_commit();
+}
+
+// Position of global id pointer q in the ids array it came from (DataError index; cold path).
+template <bool PEER>
+__device__ __noinline__ unsigned long long id_position(const BagParams& p, int r, const int32_t* q) {
+    return (unsigned long long)(q - (PEER ? p.p_ids[r] : p.ids));
+}
+
+
+// N passes of RPP rows each: every lane issues N*CPL 16-byte row loads back to back, then
+// accumulates them. Ids come from the stage (q < kIdsCap) or global. MASK: rows at or past
+// `len` read the zero row instead (bag tail).
+template <typename TT, int LPR, int CPL, int N, bool MASK, bool PEER>
+__device__ __forceinline__ void gather_step(const BagParams& p, const Stage& S, int sk, int j, int len,
+                                            const TT* __restrict__ table, uint32_t rows, int sub, int cl,
+                                            bool keep, uint64_t pol, float* acc) {
+    constexpr int EPC = Elem<TT>::kPerChunk;
+    constexpr int RPP = 32 / LPR;
+    uint4 v[N][CPL];
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+        const int jj = j + u * RPP + sub;
+        const int q = sk + jj;
+        const bool live = !MASK || jj < len;
+        int id = 0;
+        if (live) id = q < kIdsCap ? S.ids[q] : __ldg(S.idg + q);
+        bool ok = (uint32_t)id < rows;
+        if (live && !ok) atomicMin(p.err, id_position<PEER>(p, S.r, S.idg + q));
+        ok = ok && live;
+        const TT* row = ok ? table + (size_t)(uint32_t)id * p.D : reinterpret_cast<const TT*>(g_zero_row);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+            v[u][c] = keep ? ld_row_keep(row + (c * LPR + cl) * EPC, pol) : ld_stream(row + (c * LPR + cl) * EPC);
+    }
+#pragma unroll
+    for (int u = 0; u < N; ++u)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) Elem<TT>::add(acc + c * EPC, v[u][c]);
+}
+
+// Pool, normalise and store the bags of the staged chunk S.
+template <typename TT, typename OT, int LPR, int CPL, int U, bool PEER>
+__device__ __forceinline__ void pool_chunk(const BagParams& p, const Stage& S, int lane, bool keep, uint64_t pol) {
+    constexpr int EPC = Elem<TT>::kPerChunk;
+    constexpr int RPP = 32 / LPR;           // rows per pass
+    constexpr int UT = U >= 4 ? U / 2 : U;  // passes per masked tail step
+    const int sub = lane / LPR, cl = lane % LPR;
+    const int f = S.f, n = S.n;
+    const TT* __restrict__ table = static_cast<const TT*>(p.tables[f]);
+    const int64_t rows64 = p.rows[f];
+    const uint32_t rows = rows64 < 0x7fffffff ? (uint32_t)rows64 : 0x7fffffffu;
+    OT* out = static_cast<OT*>(PEER ? p.p_out[S.r] : p.out) + (int64_t)(p.out_foff + f) * p.D;
+    for (int k = 0; k < n; ++k) {
+        const int sk = S.off[k];
+        const int len = S.off[k + 1] - sk;
+        float acc[CPL * EPC];
+#pragma unroll
+        for (int i = 0; i < CPL * EPC; ++i) acc[i] = 0.0f;
+        int j = 0;
+        for (; j + RPP * U <= len; j += RPP * U)
+            gather_step<TT, LPR, CPL, U, false, PEER>(p, S, sk, j, len, table, rows, sub, cl, keep, pol, acc);
+        for (; j < len; j += RPP * UT)
+            gather_step<TT, LPR, CPL, UT, true, PEER>(p, S, sk, j, len, table, rows, sub, cl, keep, pol, acc);
+        // fold the RPP row groups: lanes with equal cl end up with the full sum
+#pragma unroll
+        for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+            for (int i = 0; i < CPL * EPC; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+        if (p.normalize) {  // rms_norm over D (numerics.hpp:81-90), eps 1e-6
+            float ss = 0.0f;
+#pragma unroll
+            for (int i = 0; i < CPL * EPC; ++i) ss += acc[i] * acc[i];
+#pragma unroll
+            for (int o = 1; o < LPR; o <<= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+            const float inv = 1.0f / sqrtf(ss / (float)p.D + 1e-6f);
+#pragma unroll
+            for (int i = 0; i < CPL * EPC; ++i) acc[i] *= inv;
+        }
+        if (sub == 0) {
+            OT* dst = out + (int64_t)S.pos[k] * p.out_stride;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) store_out<OT, EPC>(dst + (c * LPR + cl) * EPC, acc + c * EPC);
+        }
+    }
+}
+
+template <typename TT, typename OT, int LPR, int CPL, int U, int MINB, bool PEER>
+__global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagParams p) {
+    __shared__ Stage stages[kBagWarps][2];
+    const int lane = threadIdx.x & 31;
+    Stage* stg = stages[threadIdx.x >> 5];
+    const uint32_t cps = (uint32_t)((p.B + kChunk - 1) / kChunk);
+    const uint32_t total = (uint32_t)p.R * (uint32_t)p.F * cps;
+    const bool keep = p.l2keep != 0;
+    const uint64_t pol = policy_evict_last();
+
+    uint32_t c = claim_chunk(p.counter, lane);
+    if (c >= total) return;
+    stage_chunk<PEER>(p, stg[0], c, cps, chunk_offsets<PEER>(p, c, cps, lane), lane);
+    uint32_t cn = claim_chunk(p.counter, lane);
+    int64_t on = cn < total ? chunk_offsets<PEER>(p, cn, cps, lane) : 0;
+    int s = 0;
+    while (true) {
+        // stage the next chunk (its offsets were requested one chunk ago), then wait for this one
+        if (cn < total) {
+            stage_chunk<PEER>(p, stg[s ^ 1], cn, cps, on, lane);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        // claim the chunk after next and start its offsets
+        const uint32_t cnn = cn < total ? claim_chunk(p.counter, lane) : total;
+        const int64_t onn = cnn < total ? chunk_offsets<PEER>(p, cnn, cps, lane) : 0;
+        pool_chunk<TT, OT, LPR, CPL, U, PEER>(p, stg[s], lane, keep, pol);
+        __syncwarp();  // stage s is refilled next iteration
+        if (cn >= total) break;
+        cn = cnn;
+        on = onn;
+        s ^= 1;
+    }
+    // peer mode: this warp's remote row stores are ordered before the barrier kernel that
+    // follows on the stream releases them to the destination ranks
+    if constexpr (PEER) __threadfence_system();
+}
+
+}  // namespace staged
+
+
 template <typename K>
 unsigned persistent_grid(K kernel, int64_t bags) {
     int per_sm = 0;
@@ -346,26 +579,51 @@ int bag_variant(int row_bytes, bool peer) {
         forced = e ? std::atoi(e) : -1;
     }
     if (forced >= 0 && forced <= 2) return forced;
-    (void)peer;  // peer mode: variant 2 too (16 B of spill at 64 registers still beats variant 1's
-                 // 24 warps/SM: 8.2 vs 9.7 ms on the mid embedding stage, profiles/r01)
-    return row_bytes >= 512 ? 0 : 2;  // measured on B200 (scripts/bag_sweep.py, profiles/r01)
+    (void)peer;
+    (void)row_bytes;
+    return 0;  // U=4 at 40 warps/SM: best for both kernels, bf16 and fp32 (profiles/r01/bag_ab.log)
 }
 
 template <typename TT, typename OT, int LPR, int CPL, bool PEER>
 void launch_one(const BagParams& p, cudaStream_t st, int row_bytes) {
     const int64_t bags = (int64_t)p.R * p.F * p.B;
+    // peer mode runs the staged kernel (hides the NVLink latency of the offsets -> ids chain:
+    // 8.8 vs 10.8 ms owner kernel at 4 x B200); local bags run the direct kernel (7.1 vs 7.9 ms
+    // on the mid stage, 16.3 vs 15.0 M samples/s on the bf16 micro). LATTICE_BAG_KERNEL =
+    // direct | staged overrides for A/B runs.
+    static const int forced = [] {
+        const char* e = std::getenv("LATTICE_BAG_KERNEL");
+        return !e ? -1 : std::string(e) == "staged" ? 1 : std::string(e) == "direct" ? 0 : -1;
+    }();
+    const bool use_staged = forced >= 0 ? forced == 1 : PEER;
+    if (!use_staged) {
+        switch (bag_variant(row_bytes, PEER)) {
+            case 0:
+                direct::bag_kernel<TT, OT, LPR, CPL, 4, 5, PEER>
+                    <<<persistent_grid(direct::bag_kernel<TT, OT, LPR, CPL, 4, 5, PEER>, bags), kBagWarps * 32, 0, st>>>(p);
+                break;
+            case 2:
+                direct::bag_kernel<TT, OT, LPR, CPL, 8, 4, PEER>
+                    <<<persistent_grid(direct::bag_kernel<TT, OT, LPR, CPL, 8, 4, PEER>, bags), kBagWarps * 32, 0, st>>>(p);
+                break;
+            default:
+                direct::bag_kernel<TT, OT, LPR, CPL, 8, 3, PEER>
+                    <<<persistent_grid(direct::bag_kernel<TT, OT, LPR, CPL, 8, 3, PEER>, bags), kBagWarps * 32, 0, st>>>(p);
+        }
+        return;
+    }
     switch (bag_variant(row_bytes, PEER)) {
         case 0:
-            bag_kernel<TT, OT, LPR, CPL, 4, 5, PEER>
-                <<<persistent_grid(bag_kernel<TT, OT, LPR, CPL, 4, 5, PEER>, bags), kBagWarps * 32, 0, st>>>(p);
+            staged::bag_kernel<TT, OT, LPR, CPL, 4, 5, PEER>
+                <<<persistent_grid(staged::bag_kernel<TT, OT, LPR, CPL, 4, 5, PEER>, bags), kBagWarps * 32, 0, st>>>(p);
             break;
         case 2:
-            bag_kernel<TT, OT, LPR, CPL, 8, 4, PEER>
-                <<<persistent_grid(bag_kernel<TT, OT, LPR, CPL, 8, 4, PEER>, bags), kBagWarps * 32, 0, st>>>(p);
+            staged::bag_kernel<TT, OT, LPR, CPL, 8, 4, PEER>
+                <<<persistent_grid(staged::bag_kernel<TT, OT, LPR, CPL, 8, 4, PEER>, bags), kBagWarps * 32, 0, st>>>(p);
             break;
         default:
-            bag_kernel<TT, OT, LPR, CPL, 8, 3, PEER>
-                <<<persistent_grid(bag_kernel<TT, OT, LPR, CPL, 8, 3, PEER>, bags), kBagWarps * 32, 0, st>>>(p);
+            staged::bag_kernel<TT, OT, LPR, CPL, 8, 3, PEER>
+                <<<persistent_grid(staged::bag_kernel<TT, OT, LPR, CPL, 8, 3, PEER>, bags), kBagWarps * 32, 0, st>>>(p);
     }
 }
 
