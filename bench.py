@@ -286,7 +286,11 @@ def run_mid(args, rank, world, local):
         MID_ROWS, MID_B = LARGE_ROWS, LARGE_B
     # full consolidated portfolio: 16 domains, heads = 4 objectives x 3 attribution windows,
     # Zipper window assignment + window-routed heads in every step (mid-width backbone)
-    c = dict(MID, domains=16, heads=FULL_TASKS * len(FULL_WINDOWS)) if full else (LARGE if large else MID)
+    if full and world > 1:  # configs[4] on >= 2 GPUs: the large backbone, table-wise sharded
+        large = True
+        MID_ROWS, MID_B = LARGE_ROWS, LARGE_B
+    backbone = LARGE if large else MID
+    c = dict(backbone, domains=16, heads=FULL_TASKS * len(FULL_WINDOWS)) if full else backbone
     n, d, B = c["n"], c["d"], MID_B
     net = L.Network(**c, max_batch=B, weight_seed=SEED_W)
     sharded = world > 1 or args.exchange == "peer1"  # peer1: the peer path at N=1 (experiments)
@@ -473,8 +477,10 @@ def run_mid(args, rank, world, local):
         metric = "Lattice Network samples/sec (full consolidated portfolio, forward step)"
         wl = ("full consolidated portfolio: 16 domains x (4 objectives x 3 windows {90min,1d,7d}) "
               "heads, per-sample Zipper window assignment (seed 7, p=1/3) + window-routed heads each step; "
-              "mid-width backbone (256 sparse feats x 100k rows x 128, l=4, MLP 8192-2048-2048-16384, "
-              "tower 32768-512-12), B=32768/GPU")
+              + ("large backbone (512 tables x 1.5M rows x 128 bf16 = 196.6 GB table-wise sharded, l=4, "
+                 "n=512, MLP 16384-2048-2048-32768, tower 65536-512-12), B=65536/GPU" if large else
+                 "mid-width backbone on 1 GPU (256 sparse feats x 100k rows x 128, l=4, "
+                 "MLP 8192-2048-2048-16384, tower 32768-512-12), B=32768/GPU"))
     elif large:
         metric = "Lattice Network samples/sec (large config, forward step)"
         wl = ("large Lattice Network: 512 tables x 1.5M rows x 128 bf16 (196.6 GB) table-wise sharded, "
@@ -491,7 +497,8 @@ def run_mid(args, rank, world, local):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (counter-based tables/bags/weights)",
         "config": {"workload": wl,
                    "global_batch": world * B, "ids_per_step": n_ids,
-                   "l2": "embedding rows drawn uniformly from 6.6 GB of tables; activations 2.1 GB/buffer (> L2)",
+                   "l2": ("embedding rows drawn uniformly from %.1f GB of tables per GPU; activations %.1f GB/buffer (> L2)"
+                          % (n_tab * MID_ROWS * d * 2 / 1e9, B * n * d * 2 / 1e9)),
                    "parallelism": ((f"table-wise sharded embeddings over {world} GPUs (owner kernel reads "
                                     f"peers' ids and stores pooled rows into their X0 over NVLink via CUDA "
                                     f"IPC, in-kernel barriers, no NCCL on the data path) + dense replicas")
