@@ -331,12 +331,16 @@ def run_mid(args, rank, world, local):
 
     if full:
         imp = L.synth_impressions(B, FULL_TASKS, 7 + rank)
-        routed = torch.empty((B, FULL_TASKS), dtype=torch.float32, device="cuda")
+        nW = len(FULL_WINDOWS)
+        obj_out = (torch.empty((B, FULL_TASKS), dtype=torch.float32, device="cuda"),
+                   torch.empty(FULL_TASKS, dtype=torch.float64, device="cuda"),
+                   torch.empty(nW, dtype=torch.int64, device="cuda"),
+                   torch.empty((nW, FULL_TASKS), dtype=torch.int64, device="cuda"))
         wp = [1.0 / len(FULL_WINDOWS)] * len(FULL_WINDOWS)
 
     def forward(dm, off, ii, out, imp_cols=None):
         if full:  # K5: window assignment + per-window labels of this batch's impressions
-            win, _, _ = L.zipper_assign_labels(*(imp_cols or imp), FULL_WINDOWS, wp, 7, routed=True,
+            win, lab, _ = L.zipper_assign_labels(*(imp_cols or imp), FULL_WINDOWS, wp, 7, routed=False,
                                                check_errors=False)
         if peer:
             pb.forward(key_of[id(off)], dm, tables, ptrs, rows, logits=out)
@@ -346,7 +350,8 @@ def run_mid(args, rank, world, local):
         else:
             net.forward(dm, off, ii, ptrs, rows, torch.bfloat16, logits=out)
         if full:  # the window mask applied to the heads (training routes each sample's loss)
-            L.route_heads(out, win, FULL_TASKS, len(FULL_WINDOWS), out=routed)
+            # post-tower batch step: routed logits, per-task correlation loss (fp64), window summary
+            L.routed_objectives(out, win, lab, FULL_TASKS, nW, check_errors=False, out=obj_out)
 
     def step():
         forward(dom, offsets, ids, logits)
@@ -472,11 +477,11 @@ def run_mid(args, rank, world, local):
         sb.check_overflow()
         launches += 2  # owner bag kernel + offsets scan (the bag slot above is the shard gather)
     if full:
-        launches += 2  # zipper_kernel + route_heads_kernel
+        launches += 6  # zipper_kernel + summary + 2 x (moments + fold) of routed_objectives
     if full:
         metric = "Lattice Network samples/sec (full consolidated portfolio, forward step)"
         wl = ("full consolidated portfolio: 16 domains x (4 objectives x 3 windows {90min,1d,7d}) "
-              "heads, per-sample Zipper window assignment (seed 7, p=1/3) + window-routed heads each step; "
+              "heads, per-sample Zipper window assignment (seed 7, p=1/3) + window-routed heads + correlation loss + window summary each step; "
               + ("large backbone (512 tables x 1.5M rows x 128 bf16 = 196.6 GB table-wise sharded, l=4, "
                  "n=512, MLP 16384-2048-2048-32768, tower 65536-512-12), B=65536/GPU" if large else
                  "mid-width backbone on 1 GPU (256 sparse feats x 100k rows x 128, l=4, "

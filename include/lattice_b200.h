@@ -184,6 +184,46 @@ lattice_status lattice_rownorm(int32_t mode, int64_t rows, int64_t width, double
                                const float* x, float* out, int32_t check, lattice_stream stream);
 
 /* ======================================================================================
+ * Post-tower batch reductions. fp64, deterministic (fixed-order
+ * per-block partials, no float atomics).
+ * lattice_correlation_loss -- replaces lattice::correlation_loss (numerics.hpp:46-78) for
+ *   `cols` column pairs at once: out[c] = clamp(1 - Cov(x_c, y_c) / (sx*sy + eps), 0, 2),
+ *   population moments, two passes, 1.0 when either side is constant. x/y DEVICE fp64
+ *   [n][ld]; out DEVICE [cols]. eps <= 0 / n < 2 -> USAGE; non-finite -> DATA (check = 1).
+ * lattice_window_summary -- replaces lattice::window_routing_summary (datasets.hpp:256-283):
+ *   counts[w] = records routed to window w, positives[w][t] = their own-window positives
+ *   (positive_rate = positives / count, 0 when count = 0, computed by the caller). window [n],
+ *   labels [n][T][W] as written by lattice_zipper_assign_labels; a window >= W -> USAGE
+ *   (check = 1). counts / positives DEVICE int64.
+ * lattice_routed_objectives -- the fused batch step after the towers: routed[b][t] =
+ *   logits[b][t*W + window[b]] (optional), corr[t] = correlation_loss(routed label,
+ *   stable_sigmoid(routed logit)) over the batch (ground-truth vs predicted
+ *   label distribution), and the window summary.
+ * ==================================================================================== */
+lattice_status lattice_correlation_loss(int64_t n, int32_t cols, const double* x, int64_t ldx,
+                                        const double* y, int64_t ldy, double eps, double* out,
+                                        int32_t check, lattice_stream stream);
+lattice_status lattice_window_summary(int64_t n, int32_t tasks, int32_t windows,
+                                      const uint8_t* window, const uint8_t* labels, int64_t* counts,
+                                      int64_t* positives, int32_t check, lattice_stream stream);
+
+typedef struct {
+    int64_t n;
+    int32_t tasks, windows;
+    const float* logits;     /* [n][tasks*windows] (tower output, caller order) */
+    const uint8_t* window;   /* [n] assigned window */
+    const uint8_t* labels;   /* [n][tasks][windows] */
+    double eps;
+    float* routed;           /* optional out [n][tasks] */
+    double* corr;            /* out [tasks] */
+    int64_t* counts;         /* out [windows] */
+    int64_t* positives;      /* out [windows][tasks] */
+    int32_t check;           /* 1: synchronise; bad window -> USAGE, non-finite -> DATA */
+} lattice_objective_args;
+
+lattice_status lattice_routed_objectives(const lattice_objective_args* args, lattice_stream stream);
+
+/* ======================================================================================
  * Synthetic inputs: counter-based, identical to oracle/ so inputs
  * never cross PCIe.
  * ==================================================================================== */

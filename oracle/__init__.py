@@ -87,6 +87,12 @@ def load_oracle():
         lib.lo_synth_impressions.argtypes = [_I64, ctypes.c_int, _U64, _P, _P, _P, _P, _P, _P, _P]
         lib.lo_bf16_round.restype = ctypes.c_float
         lib.lo_bf16_round.argtypes = [ctypes.c_float]
+        lib.lo_correlation_loss.restype = ctypes.c_int
+        lib.lo_correlation_loss.argtypes = [_P, _P, _SZ, _D, _P]
+        lib.lo_window_summary.restype = ctypes.c_int
+        lib.lo_window_summary.argtypes = [_I64, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P]
+        lib.lo_routed_objectives.restype = ctypes.c_int
+        lib.lo_routed_objectives.argtypes = [_I64, ctypes.c_int, ctypes.c_int, _P, _P, _P, _D, _P, _P, _P, _P]
         _oracle = lib
     return _oracle
 
@@ -118,6 +124,10 @@ def load_ref():
             f = getattr(lib, name)
             f.restype = ctypes.c_int
             f.argtypes = [_P, _SZ, _D, _P]
+        lib.ref_correlation_loss.restype = ctypes.c_int
+        lib.ref_correlation_loss.argtypes = [_P, _P, _SZ, _D, _P]
+        lib.ref_window_summary.restype = ctypes.c_int
+        lib.ref_window_summary.argtypes = [_I64, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P, _P]
         _ref = lib
     return _ref
 
@@ -185,6 +195,58 @@ def vec_op(lib, name, x, eps=1e-6):
     out = np.zeros(max(len(x), 1), np.float64)
     rc = getattr(lib, name)(ptr(x) if len(x) else None, len(x), eps, ptr(out))
     return rc, out[: len(x)]
+
+
+def correlation_loss(x, y, eps=1e-6, lib=None):
+    """-> (rc, loss): lo_correlation_loss (or ref_correlation_loss with lib=load_ref())."""
+    lib = lib or load_oracle()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    out = np.zeros(1, np.float64)
+    name = "ref_correlation_loss" if hasattr(lib, "ref_correlation_loss") else "lo_correlation_loss"
+    rc = getattr(lib, name)(ptr(x) if len(x) else None, ptr(y) if len(y) else None, len(x), eps, ptr(out))
+    return rc, float(out[0])
+
+
+def window_summary(window, labels, W):
+    """lo_window_summary: (rc, counts [W], positives [W, T])."""
+    window = np.ascontiguousarray(window, dtype=np.uint8)
+    labels = np.ascontiguousarray(labels, dtype=np.uint8)
+    n, T = len(window), labels.shape[1]
+    counts = np.zeros(W, np.int64)
+    pos = np.zeros((W, T), np.int64)
+    rc = load_oracle().lo_window_summary(n, T, W, ptr(window), ptr(labels), ptr(counts), ptr(pos))
+    return rc, counts, pos
+
+
+def ref_window_summary(window, labels, W):
+    """The reference's window_routing_summary: (rc, counts [W], rates [W, T])."""
+    window = np.ascontiguousarray(window, dtype=np.uint8)
+    labels = np.ascontiguousarray(labels, dtype=np.uint8)
+    n, T = len(window), labels.shape[1]
+    dur = np.arange(1, W + 1, dtype=np.int64) * 1000
+    pr = np.full(W, 1.0 / W)
+    pr[-1] = 1.0 - pr[:-1].sum()
+    counts = np.zeros(W, np.int64)
+    rates = np.zeros((W, T), np.float64)
+    rc = load_ref().ref_window_summary(n, T, W, ptr(window), ptr(labels), ptr(dur), ptr(pr), ptr(counts),
+                                       ptr(rates))
+    return rc, counts, rates
+
+
+def routed_objectives(logits, window, labels, eps=1e-6):
+    """lo_routed_objectives: (rc, routed [n, T], corr [T], counts [W], positives [W, T])."""
+    logits = np.ascontiguousarray(logits, dtype=np.float32)
+    window = np.ascontiguousarray(window, dtype=np.uint8)
+    labels = np.ascontiguousarray(labels, dtype=np.uint8)
+    n, T, W = labels.shape
+    routed = np.zeros((n, T), np.float32)
+    corr = np.zeros(T, np.float64)
+    counts = np.zeros(W, np.int64)
+    pos = np.zeros((W, T), np.int64)
+    rc = load_oracle().lo_routed_objectives(n, T, W, ptr(logits), ptr(window), ptr(labels), eps, ptr(routed),
+                                            ptr(corr), ptr(counts), ptr(pos))
+    return rc, routed, corr, counts, pos
 
 
 def synth_bags(F, B, max_len, rows, seed):

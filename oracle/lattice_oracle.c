@@ -193,6 +193,79 @@ int lo_swish_rn_hard(const double* x, size_t n, double eps, double* out) {
 }
 
 /* ---------------------------------------------------------------------------------------
+ * Post-tower reductions: correlation_loss (numerics.hpp:46-78), window_routing_summary
+ * (datasets.hpp:262-283) and the routed-objective batch step built from them.
+ * ------------------------------------------------------------------------------------- */
+int lo_correlation_loss(const double* x, const double* y, size_t n, double eps, double* out) {
+    if (!(eps > 0.0)) return 1;
+    if (n < 2) return 1;
+    for (size_t i = 0; i < n; ++i)
+        if (!isfinite(x[i]) || !isfinite(y[i])) return 2;
+    const double dn = (double)n;
+    double mx = 0.0, my = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        mx += x[i];
+        my += y[i];
+    }
+    mx /= dn;
+    my /= dn;
+    double cov = 0.0, vx = 0.0, vy = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        const double dx = x[i] - mx, dy = y[i] - my;
+        cov += dx * dy;
+        vx += dx * dx;
+        vy += dy * dy;
+    }
+    cov /= dn;
+    const double sx = sqrt(vx / dn), sy = sqrt(vy / dn);
+    if (sx == 0.0 || sy == 0.0) {
+        *out = 1.0;
+        return 0;
+    }
+    double loss = 1.0 - cov / (sx * sy + eps);
+    *out = loss < 0.0 ? 0.0 : (loss > 2.0 ? 2.0 : loss);
+    return 0;
+}
+
+int lo_window_summary(int64_t n, int T, int W, const uint8_t* window, const uint8_t* labels,
+                      int64_t* counts, int64_t* positives) {
+    for (int w = 0; w < W; ++w) {
+        counts[w] = 0;
+        for (int t = 0; t < T; ++t) positives[(int64_t)w * T + t] = 0;
+    }
+    for (int64_t i = 0; i < n; ++i) {
+        const int w = window[i];
+        if (w >= W) return 1;
+        ++counts[w];
+        for (int t = 0; t < T; ++t) positives[(int64_t)w * T + t] += labels[(i * T + t) * W + w];
+    }
+    return 0;
+}
+
+int lo_routed_objectives(int64_t n, int T, int W, const float* logits, const uint8_t* window,
+                         const uint8_t* labels, double eps, float* routed, double* corr,
+                         int64_t* counts, int64_t* positives) {
+    const int rc = lo_window_summary(n, T, W, window, labels, counts, positives);
+    if (rc) return rc;
+    double* y = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double* p = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    int status = 0;
+    for (int t = 0; t < T && !status; ++t) {
+        for (int64_t i = 0; i < n; ++i) {
+            const int w = window[i];
+            const float z = logits[i * (int64_t)T * W + (int64_t)t * W + w];
+            if (routed) routed[i * T + t] = z;
+            y[i] = (double)labels[(i * T + t) * W + w];
+            p[i] = stable_sigmoid((double)z);
+        }
+        status = lo_correlation_loss(y, p, (size_t)n, eps, &corr[t]);
+    }
+    free(y);
+    free(p);
+    return status;
+}
+
+/* ---------------------------------------------------------------------------------------
  * Synthetic values
  * ------------------------------------------------------------------------------------- */
 float lo_table_value(uint64_t seed, int64_t f, int64_t r, int D, int64_t rows, int64_t c) {

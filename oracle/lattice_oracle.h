@@ -124,6 +124,23 @@ typedef struct {
 void lo_net_forward(const lo_net_cfg* cfg, const lo_net_weights* w, int64_t count,
                     const float* pooled, const int32_t* dom, float* logits, int threads);
 
+/* ---- post-tower reductions ----------------------------------------
+ * lo_correlation_loss: numerics.hpp:46-78 (1 - Cov/(sx*sy+eps), population moments, two
+ * passes, clamped to [0,2], 1.0 when either side is constant). Returns 0 ok, 1 UsageError
+ * (eps <= 0, n < 2), 2 DataError (non-finite).
+ * lo_window_summary: datasets.hpp:262-283 -- counts[w] records routed to window w and
+ * positives[w][t] of their own-window labels (rate = positives / count, 0 when count = 0).
+ * Returns 1 (UsageError) for a window >= W.
+ * lo_routed_objectives: the batch step the GPU fuses -- routed[b][t] = logits[b][t*W + w_b],
+ * y = labels[b][t][w_b], p = stable_sigmoid(routed) (numerics.hpp:29-33, fp64), corr[t] =
+ * correlation_loss(y[:, t], p[:, t]) and the window summary. */
+int lo_correlation_loss(const double* x, const double* y, size_t n, double eps, double* out);
+int lo_window_summary(int64_t n, int T, int W, const uint8_t* window, const uint8_t* labels,
+                      int64_t* counts, int64_t* positives);
+int lo_routed_objectives(int64_t n, int T, int W, const float* logits, const uint8_t* window,
+                         const uint8_t* labels, double eps, float* routed, double* corr,
+                         int64_t* counts, int64_t* positives);
+
 /* Round-to-nearest-even to bf16, returned as float. */
 float lo_bf16_round(float x);
 

@@ -129,4 +129,36 @@ int ref_swish_rn_hard(const double* x, size_t n, double eps, double* out) {
         [&] { return copy_out(lattice_ref::swish_rn_hard(std::span<const double>(x, n), eps), out); });
 }
 
+// numerics.hpp:46
+int ref_correlation_loss(const double* x, const double* y, size_t n, double eps, double* out) {
+    return guarded([&] {
+        *out = lattice_ref::correlation_loss(std::span<const double>(x, n), std::span<const double>(y, n), eps);
+        return 0;
+    });
+}
+
+// datasets.hpp:262 over columns: the dataset is rebuilt from window[n] / labels[n][T][W]
+// (tasks "t0".., windows "w0".. in config order); counts[W] and rates[W][T] come back in
+// window order.
+int ref_window_summary(int64_t n, int T, int W, const uint8_t* window, const uint8_t* labels,
+                       const int64_t* durations, const double* probs, int64_t* counts, double* rates) {
+    return guarded([&] {
+        lattice_ref::ZippedDataset ds{{}, {}, make_config(W, durations, probs, 7), {}};
+        for (int t = 0; t < T; ++t) ds.tasks.push_back("t" + std::to_string(t));
+        ds.records.resize(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) {
+            auto& r = ds.records[static_cast<size_t>(i)];
+            r.assigned_window = window[i];
+            r.window_labels.assign(labels + i * T * W, labels + (i + 1) * T * W);
+        }
+        const auto sum = lattice_ref::window_routing_summary(ds);
+        for (int w = 0; w < W; ++w) {
+            const auto& s = sum.at("w" + std::to_string(w));
+            counts[w] = static_cast<int64_t>(s.count);
+            for (int t = 0; t < T; ++t) rates[w * T + t] = s.positive_rate.at("t" + std::to_string(t));
+        }
+        return 0;
+    });
+}
+
 }  // extern "C"

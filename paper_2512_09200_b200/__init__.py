@@ -72,6 +72,12 @@ class PeerBagArgs(ctypes.Structure):
                 ("out_row_stride", _I64), ("normalize", _I32), ("check", _I32)]
 
 
+class ObjectiveArgs(ctypes.Structure):
+    _fields_ = [("n", _I64), ("tasks", _I32), ("windows", _I32), ("logits", _P), ("window", _P),
+                ("labels", _P), ("eps", ctypes.c_double), ("routed", _P), ("corr", _P), ("counts", _P),
+                ("positives", _P), ("check", _I32)]
+
+
 class GemmArgs(ctypes.Structure):
     _fields_ = [("M", _I64), ("N", _I64), ("K", _I64), ("A", _P), ("lda", _I64), ("B", _P),
                 ("ldb", _I64), ("C", _P), ("ldc", _I64), ("out_dtype", _I32), ("epilogue", _I32),
@@ -122,6 +128,9 @@ _sig("lattice_ipc_close", ctypes.c_int, [_P])
 _sig("lattice_peer_barrier", ctypes.c_int, [_P, _I32, _I32, ctypes.c_double, _P, _P])
 _sig("lattice_net_bucket", ctypes.c_int, [_P, _I64, _P, _P])
 _sig("lattice_net_buffer", _P, [_P, _I32])
+_sig("lattice_correlation_loss", ctypes.c_int, [_I64, _I32, _P, _I64, _P, _I64, ctypes.c_double, _P, _I32, _P])
+_sig("lattice_window_summary", ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _P, _I32, _P])
+_sig("lattice_routed_objectives", ctypes.c_int, [ctypes.POINTER(ObjectiveArgs), _P])
 _sig("lattice_gemm", ctypes.c_int, [ctypes.POINTER(GemmArgs), _P])
 _sig("lattice_net_create", ctypes.c_int, [ctypes.POINTER(NetConfig), ctypes.POINTER(_P)])
 _sig("lattice_net_destroy", None, [_P])
@@ -141,7 +150,8 @@ EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_versio
            "lattice_net_weight", "lattice_net_forward", "lattice_net_set_timing",
            "lattice_net_stage_times", "lattice_peer_embedding_bag", "lattice_ipc_handle",
            "lattice_ipc_open", "lattice_ipc_close", "lattice_peer_barrier", "lattice_net_bucket",
-           "lattice_net_buffer"]
+           "lattice_net_buffer", "lattice_correlation_loss", "lattice_window_summary",
+           "lattice_routed_objectives"]
 
 lib = _lib
 
@@ -220,6 +230,51 @@ def route_heads(logits, window, tasks, windows, out=None, stream=None):
     if out is None:
         out = torch.empty((B, tasks), dtype=torch.float32, device=logits.device)
     check(_lib.lattice_route_heads(B, tasks, windows, _p(logits), _p(window), _p(out), _stream(stream)))
+    return out
+
+
+def correlation_loss(x, y, eps=1e-6, check_errors=True, stream=None):
+    """lattice::correlation_loss (numerics.hpp:46) per column of fp64 CUDA matrices x, y [n, cols]
+    (1-D vectors are one column). Returns fp64 [cols]."""
+    import torch
+    if x.dim() == 1:
+        x, y = x[:, None], y[:, None]
+    n, cols = x.shape
+    out = torch.empty(cols, dtype=torch.float64, device=x.device)
+    check(_lib.lattice_correlation_loss(n, cols, _p(x), x.stride(0), _p(y), y.stride(0), eps, _p(out),
+                                        1 if check_errors else 0, _stream(stream)))
+    return out
+
+
+def window_summary(window, labels, windows, check_errors=True, stream=None):
+    """lattice::window_routing_summary (datasets.hpp:262) over device columns: window uint8 [n],
+    labels uint8 [n, T, W]. Returns (counts int64 [W], positives int64 [W, T])."""
+    import torch
+    n = window.shape[0]
+    T = labels.shape[1] if labels.dim() == 3 else 0
+    counts = torch.empty(windows, dtype=torch.int64, device=window.device)
+    pos = torch.empty((windows, T), dtype=torch.int64, device=window.device)
+    check(_lib.lattice_window_summary(n, T, windows, _p(window), _p(labels), _p(counts), _p(pos),
+                                      1 if check_errors else 0, _stream(stream)))
+    return counts, pos
+
+
+def routed_objectives(logits, window, labels, tasks, windows, eps=1e-6, routed=None, check_errors=True,
+                      stream=None, out=None):
+    """Post-tower batch step: routed logits, per-task correlation loss (routed label vs
+    sigmoid(routed logit), fp64) and the window summary. Returns (routed, corr, counts, positives)."""
+    import torch
+    n = logits.shape[0]
+    dev = logits.device
+    if out is None:
+        out = (torch.empty((n, tasks), dtype=torch.float32, device=dev),
+               torch.empty(tasks, dtype=torch.float64, device=dev),
+               torch.empty(windows, dtype=torch.int64, device=dev),
+               torch.empty((windows, tasks), dtype=torch.int64, device=dev))
+    r, corr, counts, pos = out
+    a = ObjectiveArgs(n, tasks, windows, _p(logits), _p(window), _p(labels), eps, _p(r), _p(corr), _p(counts),
+                      _p(pos), 1 if check_errors else 0)
+    check(_lib.lattice_routed_objectives(ctypes.byref(a), _stream(stream)))
     return out
 
 
