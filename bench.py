@@ -28,6 +28,15 @@ sys.path.insert(0, ROOT)
 SEED_T, SEED_D = 0x1A77, 0x1A78
 
 
+def load_traffic(workload, kernel):
+    """DRAM bytes per launch (group) of `kernel` from the committed ncu capture, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
+            return json.load(f).get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -218,7 +227,9 @@ def run_micro(args, rank, world, local):
                 "h2d_bytes_per_step": (F * B + 1) * 8 + n_ids * 4,
                 "d2h_bytes_per_step": B * F * D * s_tab},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": None, "kernel": "bag_kernel",
+                     "frac": achieved / hbm,
+                     "traffic": load_traffic("micro_bf16", "bag_kernel") if dt == torch.bfloat16 else None,
+                     "kernel": "bag_kernel",
                      "peak_source": src, "algorithmic_bytes_per_launch": alg,
                      "kernel_ms_mean": kernel_ms, "kernel_ms_min": min(kms), "kernel_ms_max": max(kms)},
         "gpu_launches": args.steps,
@@ -515,7 +526,8 @@ def run_mid(args, rank, world, local):
                                       (sum(t.numel() * t.element_size() for t in imp) if full else 0),
                 "d2h_bytes_per_step": B * c["heads"] * 4},
         "roofline": {"bound": "tensor", "achieved": mlp_achieved, "peak": tf_sust, "unit": "TFLOP/s",
-                     "frac": mlp_achieved / tf_sust, "traffic": None,
+                     "frac": mlp_achieved / tf_sust,
+                     "traffic": load_traffic("mid", "gemm_mlp_group") if args.workload == "mid" else None,
                      "kernel": "gemm_kernel (FMB MLP, 3 GEMMs per block, fused swish_rn / residual-norm)",
                      "peak_source": f"{src} sustained (kernel timed inside the step)",
                      "algorithmic_flops_per_launch_group": mlp_fl, "ms": mlp_ms},
