@@ -36,7 +36,8 @@ struct BagParams {
     int32_t R;  // source ranks: bags laid out [R][F][B]
     int64_t slice_cap;  // > 0: source r's ids start at r * slice_cap (static exchange buffer)
     unsigned long long* counter;  // work-claim counter (zeroed per launch)
-    int32_t l2keep;  // 1: table rows loaded with an L2 evict_last policy
+    int32_t l2keep;  // bit 0: table rows loaded with an L2 evict_last policy; bit 1: pooled rows
+                     // stored with evict_first (LATTICE_BAG_L2KEEP)
     // Peer mode (lattice_peer_embedding_bag): this rank owns features [src_foff, src_foff+F)
     // of every source rank's CSR and pools them for all R sources, reading each source's
     // offsets / ids / sample_pos from that source's HBM over NVLink and writing the pooled row
@@ -106,25 +107,43 @@ struct Elem<__nv_bfloat16> {
     }
 };
 
+// 16-byte store; ef: with an L2 evict_first policy (pooled rows are not re-read by this kernel)
+__device__ __forceinline__ void st16(void* dst, uint4 v, bool ef, uint64_t pol) {
+    if (ef)
+        asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dst),
+                     "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+                     : "memory");
+    else
+        *reinterpret_cast<uint4*>(dst) = v;
+}
+__device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
+
 template <typename OT, int N>
-__device__ __forceinline__ void store_out(OT* dst, const float* v);
+__device__ __forceinline__ void store_out(OT* dst, const float* v, bool ef = false, uint64_t pol = 0);
 template <>
-__device__ __forceinline__ void store_out<float, 4>(float* dst, const float* v) {
-    *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+__device__ __forceinline__ void store_out<float, 4>(float* dst, const float* v, bool ef, uint64_t pol) {
+    st16(dst, make_uint4(f2u(v[0]), f2u(v[1]), f2u(v[2]), f2u(v[3])), ef, pol);
 }
 template <>
-__device__ __forceinline__ void store_out<float, 8>(float* dst, const float* v) {
-    reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
-    reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+__device__ __forceinline__ void store_out<float, 8>(float* dst, const float* v, bool ef, uint64_t pol) {
+    st16(dst, make_uint4(f2u(v[0]), f2u(v[1]), f2u(v[2]), f2u(v[3])), ef, pol);
+    st16(dst + 4, make_uint4(f2u(v[4]), f2u(v[5]), f2u(v[6]), f2u(v[7])), ef, pol);
 }
 template <>
-__device__ __forceinline__ void store_out<__nv_bfloat16, 4>(__nv_bfloat16* dst, const float* v) {
+__device__ __forceinline__ void store_out<__nv_bfloat16, 4>(__nv_bfloat16* dst, const float* v, bool, uint64_t) {
     *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]));
 }
 template <>
-__device__ __forceinline__ void store_out<__nv_bfloat16, 8>(__nv_bfloat16* dst, const float* v) {
-    *reinterpret_cast<uint4*>(dst) = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
-                                                pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+__device__ __forceinline__ void store_out<__nv_bfloat16, 8>(__nv_bfloat16* dst, const float* v, bool ef,
+                                                            uint64_t pol) {
+    st16(dst, make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                         pack_bf16x2(v[6], v[7])),
+         ef, pol);
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 
 constexpr int kBagWarps = 8;
@@ -244,8 +263,10 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
     if (bag >= total) return;
     uint32_t chunk_end = bag + kChunk < total ? bag + kChunk : total;
     const int sub = lane / LPR, cl = lane % LPR;
-    const bool keep = p.l2keep != 0;
+    const bool keep = (p.l2keep & 1) != 0;
+    const bool ef = (p.l2keep & 2) != 0;
     const uint64_t pol = policy_evict_last();
+    const uint64_t pol_ef = policy_evict_first();
     const int32_t* idp;
     int len;
     bag_range<PEER>(p, bag, idp, len);
@@ -312,7 +333,7 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
             OT* dst = static_cast<OT*>(PEER ? p.p_out[r] : p.out) + row * p.out_stride +
                       (int64_t)(p.out_foff + f) * p.D;
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) store_out<OT, EPC>(dst + (c * LPR + cl) * EPC, acc + c * EPC);
+            for (int c = 0; c < CPL; ++c) store_out<OT, EPC>(dst + (c * LPR + cl) * EPC, acc + c * EPC, ef, pol_ef);
         }
         bag = nbag;
         idp = nidp;
@@ -523,7 +544,7 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
     Stage* stg = stages[threadIdx.x >> 5];
     const uint32_t cps = (uint32_t)((p.B + kChunk - 1) / kChunk);
     const uint32_t total = (uint32_t)p.R * (uint32_t)p.F * cps;
-    const bool keep = p.l2keep != 0;
+    const bool keep = (p.l2keep & 1) != 0;
     const uint64_t pol = policy_evict_last();
 
     uint32_t c = claim_chunk(p.counter, lane);
@@ -627,11 +648,15 @@ void launch_one(const BagParams& p, cudaStream_t st, int row_bytes) {
     }
 }
 
+// Default 3: table rows evict_last + pooled-row stores evict_first. A table's rows are re-read
+// ~6x within the ~30 us its bags are in flight (mid: 655K ids over 100K rows); without the hint
+// the streaming ids/outputs push them out of L2 (24% hit rate). Mid embedding stage 7.2 -> 5.5
+// ms, step 26.1-27.5 -> 24.3-24.5 ms, GEMMs unchanged (profiles/r01/bag_l2.log).
 int bag_l2keep() {
     static int v = -1;
     if (v < 0) {
         const char* e = std::getenv("LATTICE_BAG_L2KEEP");
-        v = e ? std::atoi(e) : 0;
+        v = e ? std::atoi(e) : 3;
     }
     return v;
 }

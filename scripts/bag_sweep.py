@@ -32,10 +32,11 @@ print(json.dumps(dict(ms=ms, GBs=by/ms/1e6)))
     return r.stdout.strip() or r.stderr[-300:]
 
 if len(sys.argv) > 1 and sys.argv[1] == "l2":
-    for rows in (100000, 20000):
-        for keep in (0, 1):
+    # LATTICE_BAG_L2KEEP bit 0: rows evict_last, bit 1: pooled-row stores evict_first
+    for rows in (100000, 1000000):
+        for keep in (0, 1, 2, 3):
             print("mid_bf16 rows", rows, "keep", keep,
-                  one(256, rows, 128, 32768, "bfloat16", 2, True, keep), flush=True)
+                  one(256, rows, 128, 32768, "bfloat16", 0, True, keep), flush=True)
     sys.exit(0)
 for name, cfg in [("micro_f32", (64, 1000000, 128, 16384, "float32")),
                   ("micro_bf16", (64, 1000000, 128, 16384, "bfloat16")),
