@@ -184,6 +184,21 @@ lattice_status lattice_rownorm(int32_t mode, int64_t rows, int64_t width, double
                                const float* x, float* out, int32_t check, lattice_stream stream);
 
 /* ======================================================================================
+ * Dense features across consolidated domains -- replaces the value side of
+ * lattice::merge_domains (datasets.hpp:144-173): records keep their domain's feature values,
+ * re-laid out under the union schema with zero padding for features their domain never
+ * declared. The union schema itself (first-seen union of feature names) and the
+ * "undeclared feature" DataError are string-level work done by the caller / C++ drop-in,
+ * which passes src_col[g][c] = index of union column c in domain g's declared order, or -1.
+ * values: DEVICE fp32 [n][max_declared] (record b's values in its domain's declared order),
+ * domain: DEVICE int32 [n]. out: DEVICE [n][out_width] in out_dtype (columns past the union
+ * width are zero: GEMM padding). A domain outside [0, domains) -> DATA (check = 1).
+ * ==================================================================================== */
+lattice_status lattice_merge_dense(int64_t n, int32_t domains, int32_t max_declared, const int32_t* domain,
+                                   const float* values, const int32_t* src_col, int32_t out_width,
+                                   int32_t out_dtype, void* out, int32_t check, lattice_stream stream);
+
+/* ======================================================================================
  * Post-tower batch reductions. fp64, deterministic (fixed-order
  * per-block partials, no float atomics).
  * lattice_correlation_loss -- replaces lattice::correlation_loss (numerics.hpp:46-78) for
@@ -305,6 +320,13 @@ typedef struct {
     uint64_t weight_seed;
     int32_t dtype;         /* storage/compute dtype: LATTICE_BF16 (kind::f16 tensor cores) or
                               LATTICE_F32 (kind::tf32; d = 64 only) */
+    /* dense-feature processor: the last `dense_features` of the n embeddings are
+       O_d = reshape(D2 . swish_rn(D1 . x_dense), [dense_features][d]) (D1 [dense_hidden]
+       [dense_in], D2 [dense_features*d][dense_hidden]); the first n - dense_features come from
+       the embedding tables. The mixing norm (rms_norm_d) applies to both. 0 = no dense part. */
+    int32_t dense_features;
+    int32_t dense_in;      /* multiple of 8 (pad the merged dense matrix) */
+    int32_t dense_hidden;  /* multiple of 8 in [8, 2048] */
 } lattice_net_config;
 
 typedef struct lattice_net lattice_net;
@@ -313,7 +335,8 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
 void lattice_net_destroy(lattice_net* net);
 /* Device pointer of a weight tensor (bf16): kind 1 Y^T [k][n], 2 W_L [nL][n],
  * 3 MLP layer `index` [out][in], 4 tower W1 [G][tower_hidden][n*d], 5 tower W2 fp32
- * [G][heads][tower_hidden]. block ignored for 4/5. */
+ * [G][heads][tower_hidden], 6 dense D1 [dense_hidden][dense_in], 7 dense D2
+ * [dense_features*d][dense_hidden]. block ignored for 4-7. */
 const void* lattice_net_weight(lattice_net* net, int32_t block, int32_t kind, int32_t index);
 
 typedef struct {
@@ -327,7 +350,8 @@ typedef struct {
     const int32_t* ids;
     /* or, when tables == NULL: already pooled embeddings in table_dtype */
     const void* pooled;
-    int32_t pooled_layout;       /* 0: raw sums [B][n][d], caller order (the net normalises)
+    int32_t pooled_layout;       /* 0: raw sums [B][n - dense_features][d], caller order (the
+                                       net normalises)
                                     1: table-wise shards [S][B][n/S][d] bf16, already
                                        rms-normalised by the owners (lattice_embedding_bag
                                        with normalize = 1), S = shards
@@ -336,6 +360,8 @@ typedef struct {
                                        lattice_peer_embedding_bag after lattice_net_bucket
                                        ran for this batch; `pooled` is ignored */
     int32_t shards;
+    const void* dense;           /* DEVICE [B][dense_in] in the net dtype (caller order) when
+                                    cfg.dense_features > 0 (e.g. lattice_merge_dense output) */
 } lattice_batch;
 
 /* Domain bucketing of a batch ahead of the forward (pooled_layout 2): writes the

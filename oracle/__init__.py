@@ -91,6 +91,11 @@ def load_oracle():
         lib.lo_correlation_loss.argtypes = [_P, _P, _SZ, _D, _P]
         lib.lo_window_summary.restype = ctypes.c_int
         lib.lo_window_summary.argtypes = [_I64, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P]
+        lib.lo_merge_dense.restype = _I64
+        lib.lo_merge_dense.argtypes = [_I64, ctypes.c_int, ctypes.c_int, _P, _P, _P, ctypes.c_int, ctypes.c_int, _P]
+        lib.lo_dense_processor.restype = None
+        lib.lo_dense_processor.argtypes = [ctypes.POINTER(LoNetCfg), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                           _P, _P, _I64, _P, _P, ctypes.c_int]
         lib.lo_routed_objectives.restype = ctypes.c_int
         lib.lo_routed_objectives.argtypes = [_I64, ctypes.c_int, ctypes.c_int, _P, _P, _P, _D, _P, _P, _P, _P]
         _oracle = lib
@@ -126,6 +131,8 @@ def load_ref():
             f.argtypes = [_P, _SZ, _D, _P]
         lib.ref_correlation_loss.restype = ctypes.c_int
         lib.ref_correlation_loss.argtypes = [_P, _P, _SZ, _D, _P]
+        lib.ref_merge_domains.restype = ctypes.c_int
+        lib.ref_merge_domains.argtypes = [ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P, _P]
         lib.ref_window_summary.restype = ctypes.c_int
         lib.ref_window_summary.argtypes = [_I64, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P, _P]
         _ref = lib
@@ -247,6 +254,47 @@ def routed_objectives(logits, window, labels, eps=1e-6):
     rc = load_oracle().lo_routed_objectives(n, T, W, ptr(logits), ptr(window), ptr(labels), eps, ptr(routed),
                                             ptr(corr), ptr(counts), ptr(pos))
     return rc, routed, corr, counts, pos
+
+
+def merge_dense(domain, values, src_col, bf16=False):
+    """lo_merge_dense: (first bad record or -1, out [n, width] fp32)."""
+    domain = np.ascontiguousarray(domain, dtype=np.int32)
+    values = np.ascontiguousarray(values, dtype=np.float32)
+    src_col = np.ascontiguousarray(src_col, dtype=np.int32)
+    n, md = values.shape
+    G, width = src_col.shape
+    out = np.zeros((n, width), np.float32)
+    bad = load_oracle().lo_merge_dense(n, G, md, ptr(domain), ptr(values), ptr(src_col), width, int(bf16), ptr(out))
+    return bad, out
+
+
+def ref_merge_domains(decl, n_rec, values):
+    """The reference's merge_domains on integer-named features: decl int32 [G, max_decl] (-1 =
+    unused), n_rec records per domain (grouped in order), values fp64 [n, max_decl]. Returns
+    (rc, union feature ids, matrix [n, n_union])."""
+    decl = np.ascontiguousarray(decl, dtype=np.int32)
+    n_rec = np.ascontiguousarray(n_rec, dtype=np.int64)
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    G, md = decl.shape
+    n = int(n_rec.sum())
+    uid = np.zeros(G * md + 1, np.int32)
+    nu = ctypes.c_int32()
+    out = np.zeros(max(n * G * md, 1), np.float64)
+    rc = load_ref().ref_merge_domains(G, md, ptr(decl), ptr(n_rec), ptr(values), ptr(uid), ctypes.byref(nu),
+                                      ptr(out))
+    k = nu.value
+    return rc, uid[:k], out[: n * k].reshape(n, k)
+
+
+def dense_processor(cfg, n_dense, dense_in, dense_hidden, D1, D2, dense, pooled, threads=0):
+    """lo_dense_processor: fills rows [n - n_dense, n) of pooled [count, n, d] in place."""
+    D1 = np.ascontiguousarray(D1, dtype=np.float32)
+    D2 = np.ascontiguousarray(D2, dtype=np.float32)
+    dense = np.ascontiguousarray(dense, dtype=np.float32)
+    assert pooled.flags.c_contiguous and pooled.dtype == np.float32
+    load_oracle().lo_dense_processor(ctypes.byref(cfg), n_dense, dense_in, dense_hidden, ptr(D1), ptr(D2),
+                                     dense.shape[0], ptr(dense), ptr(pooled), threads)
+    return pooled
 
 
 def synth_bags(F, B, max_len, rows, seed):

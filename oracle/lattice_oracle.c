@@ -541,3 +541,60 @@ void lo_synth_impressions(int64_t n, int T, uint64_t seed, uint8_t* ub, int64_t*
     uo[n] = 9 * n;
     ao[n] = 7 * n;
 }
+
+/* ---------------------------------------------------------------------------------------
+ * Dense features: merge_domains values (datasets.hpp:144-173) and the dense processor
+ * (PAPER.md:277).
+ * ------------------------------------------------------------------------------------- */
+int64_t lo_merge_dense(int64_t n, int G, int max_decl, const int32_t* domain, const float* values,
+                       const int32_t* src_col, int width, int bf16, float* out) {
+    int64_t bad = -1;
+    for (int64_t b = 0; b < n; ++b) {
+        const int g = domain[b];
+        if (g < 0 || g >= G) {
+            if (bad < 0) bad = b;
+            for (int c = 0; c < width; ++c) out[b * width + c] = 0.0f;
+            continue;
+        }
+        for (int c = 0; c < width; ++c) {
+            const int j = src_col[(int64_t)g * width + c];
+            const float v = j >= 0 ? values[b * max_decl + j] : 0.0f;
+            out[b * width + c] = bf16 ? lo_bf16_round(v) : v;
+        }
+    }
+    return bad;
+}
+
+void lo_dense_processor(const lo_net_cfg* cfg, int n_dense, int dense_in, int dense_hidden,
+                        const float* D1, const float* D2, int64_t count, const float* dense,
+                        float* pooled, int threads) {
+    const int n = cfg->n, d = cfg->d, nc = cfg->n - n_dense, od = n_dense * d;
+#ifdef _OPENMP
+    if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel
+#endif
+    {
+        double* h = (double*)malloc(sizeof(double) * (size_t)dense_hidden * 2);
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 4)
+#endif
+        for (int64_t s = 0; s < count; ++s) {
+            const float* x = dense + (size_t)s * dense_in;
+            for (int o = 0; o < dense_hidden; ++o) {
+                double acc = 0.0;
+                for (int i = 0; i < dense_in; ++i) acc += (double)D1[(size_t)o * dense_in + i] * (double)x[i];
+                h[o] = acc;
+            }
+            act(cfg, h, (size_t)dense_hidden, h + dense_hidden);
+            for (int o = 0; o < dense_hidden; ++o) h[o] = q(cfg, h[dense_hidden + o]);
+            float* dst = pooled + ((size_t)s * n + nc) * d;
+            for (int o = 0; o < od; ++o) {
+                double acc = 0.0;
+                for (int i = 0; i < dense_hidden; ++i) acc += (double)D2[(size_t)o * dense_hidden + i] * h[i];
+                dst[o] = (float)q(cfg, acc);
+            }
+        }
+        free(h);
+    }
+}
+

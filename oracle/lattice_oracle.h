@@ -124,6 +124,19 @@ typedef struct {
 void lo_net_forward(const lo_net_cfg* cfg, const lo_net_weights* w, int64_t count,
                     const float* pooled, const int32_t* dom, float* logits, int threads);
 
+/* ---- dense features -------------------------------------------------
+ * lo_merge_dense: the value side of merge_domains (datasets.hpp:144-173) over columns --
+ * out[b][c] = values[b][src_col[g_b][c]] or 0 (the pad) when src_col is -1; bf16 = 1 rounds to
+ * bf16. Returns the first record with a domain outside [0, G), or -1.
+ * lo_dense_processor: PAPER.md:277 -- O_d = D2 . q(act(D1 . x)) per sample, each value q()-rounded
+ * (the GPU stores it in the net dtype), written as raw rows [nc, nc + n_dense) of pooled
+ * ([count][n][d]) so lo_net_forward's mixing norm treats it like the pooled sparse rows. */
+int64_t lo_merge_dense(int64_t n, int G, int max_decl, const int32_t* domain, const float* values,
+                       const int32_t* src_col, int width, int bf16, float* out);
+void lo_dense_processor(const lo_net_cfg* cfg, int n_dense, int dense_in, int dense_hidden,
+                        const float* D1, const float* D2, int64_t count, const float* dense,
+                        float* pooled, int threads);
+
 /* ---- post-tower reductions ----------------------------------------
  * lo_correlation_loss: numerics.hpp:46-78 (1 - Cov/(sx*sy+eps), population moments, two
  * passes, clamped to [0,2], 1.0 when either side is constant). Returns 0 ok, 1 UsageError

@@ -161,4 +161,38 @@ int ref_window_summary(int64_t n, int T, int W, const uint8_t* window, const uin
     });
 }
 
+// datasets.hpp:144 over columns. Domain g declares features "f<decl[g][j]>" (j < max_decl,
+// -1 = unused slot); its n_rec[g] records (grouped by domain, in order) carry values[r][j] for
+// every declared j. Writes the union feature ids (first-seen order) to union_ids and the
+// padded matrix [n][n_union] in union order; returns 0 / 1 (UsageError) / 2 (DataError).
+int ref_merge_domains(int G, int max_decl, const int32_t* decl, const int64_t* n_rec, const double* values,
+                      int32_t* union_ids, int32_t* n_union, double* out) {
+    return guarded([&] {
+        std::vector<lattice_ref::DomainDataset> ds;
+        int64_t r = 0;
+        for (int g = 0; g < G; ++g) {
+            std::vector<std::string> feats;
+            for (int j = 0; j < max_decl; ++j)
+                if (decl[g * max_decl + j] >= 0) feats.push_back("f" + std::to_string(decl[g * max_decl + j]));
+            lattice_ref::DomainDataset d{lattice_ref::DatasetSchema::create("d" + std::to_string(g), feats), {}};
+            for (int64_t i = 0; i < n_rec[g]; ++i, ++r) {
+                lattice_ref::DomainRecord rec;
+                rec.domain = d.schema.domain;
+                for (int j = 0; j < max_decl; ++j)
+                    if (decl[g * max_decl + j] >= 0)
+                        rec.values["f" + std::to_string(decl[g * max_decl + j])] = values[r * max_decl + j];
+                d.records.push_back(std::move(rec));
+            }
+            ds.push_back(std::move(d));
+        }
+        const auto u = lattice_ref::merge_domains(ds);
+        *n_union = static_cast<int32_t>(u.schema.features.size());
+        for (size_t c = 0; c < u.schema.features.size(); ++c) union_ids[c] = std::stoi(u.schema.features[c].substr(1));
+        for (size_t i = 0; i < u.records.size(); ++i)
+            for (size_t c = 0; c < u.schema.features.size(); ++c)
+                out[i * u.schema.features.size() + c] = u.records[i].values.at(u.schema.features[c]);
+        return 0;
+    });
+}
+
 }  // extern "C"

@@ -88,13 +88,14 @@ class NetConfig(ctypes.Structure):
     _fields_ = [("n", _I32), ("d", _I32), ("blocks", _I32), ("nF", _I32), ("nL", _I32),
                 ("k", _I32), ("n_mlp", _I32), ("mlp", _I32 * 6), ("domains", _I32),
                 ("heads", _I32), ("tower_hidden", _I32), ("hard", _I32), ("max_batch", _I64),
-                ("weight_seed", _U64), ("dtype", _I32)]
+                ("weight_seed", _U64), ("dtype", _I32), ("dense_features", _I32), ("dense_in", _I32),
+                ("dense_hidden", _I32)]
 
 
 class Batch(ctypes.Structure):
     _fields_ = [("batch", _I64), ("domain", _P), ("table_dtype", _I32), ("tables", _P),
                 ("rows", _P), ("offsets", _P), ("ids", _P), ("pooled", _P),
-                ("pooled_layout", _I32), ("shards", _I32)]
+                ("pooled_layout", _I32), ("shards", _I32), ("dense", _P)]
 
 
 def _sig(name, res, args):
@@ -131,6 +132,7 @@ _sig("lattice_net_buffer", _P, [_P, _I32])
 _sig("lattice_correlation_loss", ctypes.c_int, [_I64, _I32, _P, _I64, _P, _I64, ctypes.c_double, _P, _I32, _P])
 _sig("lattice_window_summary", ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _P, _I32, _P])
 _sig("lattice_routed_objectives", ctypes.c_int, [ctypes.POINTER(ObjectiveArgs), _P])
+_sig("lattice_merge_dense", ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _I32, _I32, _P, _I32, _P])
 _sig("lattice_gemm", ctypes.c_int, [ctypes.POINTER(GemmArgs), _P])
 _sig("lattice_net_create", ctypes.c_int, [ctypes.POINTER(NetConfig), ctypes.POINTER(_P)])
 _sig("lattice_net_destroy", None, [_P])
@@ -151,7 +153,7 @@ EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_versio
            "lattice_net_stage_times", "lattice_peer_embedding_bag", "lattice_ipc_handle",
            "lattice_ipc_open", "lattice_ipc_close", "lattice_peer_barrier", "lattice_net_bucket",
            "lattice_net_buffer", "lattice_correlation_loss", "lattice_window_summary",
-           "lattice_routed_objectives"]
+           "lattice_routed_objectives", "lattice_merge_dense"]
 
 lib = _lib
 
@@ -359,6 +361,35 @@ def peer_barrier(flag_ptrs, rank, world, status, timeout_s=30.0, stream=None):
     check(_lib.lattice_peer_barrier(_p(flag_ptrs), rank, world, timeout_s, _p(status), _stream(stream)))
 
 
+def merge_dense(domain, values, src_col, out_width, out_dtype=None, check_errors=True, stream=None):
+    """merge_domains for dense values (datasets.hpp:144-173): domain int32 [n], values fp32
+    [n, max_declared] in each record's domain order, src_col int32 [G, out_width] (union column ->
+    declared index or -1). Returns [n, out_width] (bf16 by default) with zero padding."""
+    import torch
+    n, md = values.shape
+    G = src_col.shape[0]
+    odt = out_dtype or torch.bfloat16
+    out = torch.empty((n, out_width), dtype=odt, device=values.device)
+    check(_lib.lattice_merge_dense(n, G, md, _p(domain), _p(values), _p(src_col), out_width,
+                                   F32 if odt == torch.float32 else BF16, _p(out), 1 if check_errors else 0,
+                                   _stream(stream)))
+    return out
+
+
+def union_schema(declared):
+    """First-seen union of feature names (datasets.hpp:125-132) and the src_col map merge_dense
+    takes: declared = list of per-domain feature-name lists -> (union names, src_col [G][len(union)])
+    (pad the columns with -1 for a wider, GEMM-aligned output)."""
+    union, seen = [], set()
+    for feats in declared:
+        for f in feats:
+            if f not in seen:
+                seen.add(f)
+                union.append(f)
+    src = [[feats.index(u) if u in feats else -1 for u in union] for feats in declared]
+    return union, src
+
+
 def lengths_to_offsets(lengths, out=None, stream=None):
     """int32 bag lengths [n] -> int64 CSR offsets [n+1] (exclusive scan on the GPU)."""
     import torch
@@ -477,11 +508,15 @@ class Network:
     """lattice::Network over the C ABI (lattice_net_*). Weights live on the current device."""
 
     def __init__(self, n, d, blocks, nF, nL, k, mlp, domains, heads, tower_hidden, hard=False,
-                 max_batch=32768, weight_seed=0x1A78, dtype="bf16"):
-        """dtype "bf16" (kind::f16 tensor cores) or "f32" (fp32 storage, kind::tf32; d=64)."""
+                 max_batch=32768, weight_seed=0x1A78, dtype="bf16", dense_features=0, dense_in=0,
+                 dense_hidden=0):
+        """dtype "bf16" (kind::f16 tensor cores) or "f32" (fp32 storage, kind::tf32; d=64).
+        dense_features > 0: the last dense_features of the n embeddings come from the dense
+        processor over a [B, dense_in] dense matrix (forward(dense=...))."""
         self.cfg = dict(n=n, d=d, blocks=blocks, nF=nF, nL=nL, k=k, mlp=list(mlp), domains=domains,
                         heads=heads, tower_hidden=tower_hidden, hard=hard, max_batch=max_batch,
-                        weight_seed=weight_seed, dtype=dtype)
+                        weight_seed=weight_seed, dtype=dtype, dense_features=dense_features,
+                        dense_in=dense_in, dense_hidden=dense_hidden)
         c = NetConfig()
         c.n, c.d, c.blocks, c.nF, c.nL, c.k = n, d, blocks, nF, nL, k
         c.n_mlp = len(mlp) - 1
@@ -490,6 +525,7 @@ class Network:
         c.domains, c.heads, c.tower_hidden, c.hard = domains, heads, tower_hidden, int(hard)
         c.max_batch, c.weight_seed = max_batch, weight_seed
         c.dtype = F32 if dtype in ("f32", "fp32", "float32") else BF16
+        c.dense_features, c.dense_in, c.dense_hidden = dense_features, dense_in, dense_hidden
         h = ctypes.c_void_p()
         check(_lib.lattice_net_create(ctypes.byref(c), ctypes.byref(h)))
         self._h = h
@@ -506,7 +542,7 @@ class Network:
             pass
 
     def forward(self, domain, offsets=None, ids=None, table_ptrs=None, rows=None,
-                table_dtype=None, pooled=None, logits=None, stream=None, shards=0):
+                table_dtype=None, pooled=None, logits=None, stream=None, shards=0, dense=None):
         """shards > 0: `pooled` is the table-wise sharded, owner-normalised bf16 layout
         [S][B][n/S][d] received from the pooled all-to-all."""
         import torch
@@ -524,6 +560,7 @@ class Network:
         else:
             b.table_dtype = F32 if table_dtype == torch.float32 else BF16
             b.tables, b.rows, b.offsets, b.ids = _p(table_ptrs), _p(rows), _p(offsets), _p(ids)
+        b.dense = _p(dense)
         check(_lib.lattice_net_forward(self._h, ctypes.byref(b), _p(logits), _stream(stream)))
         return logits
 
@@ -538,7 +575,7 @@ class Network:
             raise UsageError(f"lattice_net_buffer: unknown buffer {which}")
         return p
 
-    def forward_in_place(self, domain, logits=None, stream=None):
+    def forward_in_place(self, domain, logits=None, stream=None, dense=None):
         """Forward over an X0 already filled by lattice_peer_embedding_bag (pooled_layout 2)."""
         import torch
         B = domain.shape[0]
@@ -549,6 +586,7 @@ class Network:
         b.domain = _p(domain)
         b.table_dtype = F32 if self.cfg["dtype"] in ("f32", "fp32", "float32") else BF16
         b.pooled_layout = 2
+        b.dense = _p(dense)
         check(_lib.lattice_net_forward(self._h, ctypes.byref(b), _p(logits), _stream(stream)))
         return logits
 
@@ -583,4 +621,8 @@ class Network:
                           wdt).float().cpu().numpy().copy()
         out["T2"] = _view(_lib.lattice_net_weight(self._h, 0, 5, 0), (G, H, th),
                           torch.float32).cpu().numpy().copy()
+        if c["dense_features"]:
+            nd_, di, dh = c["dense_features"], c["dense_in"], c["dense_hidden"]
+            out["D1"] = _view(_lib.lattice_net_weight(self._h, 0, 6, 0), (dh, di), wdt).float().cpu().numpy().copy()
+            out["D2"] = _view(_lib.lattice_net_weight(self._h, 0, 7, 0), (nd_ * d, dh), wdt).float().cpu().numpy().copy()
         return out

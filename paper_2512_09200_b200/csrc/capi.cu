@@ -51,7 +51,7 @@ extern "C" {
 
 const char* lattice_last_error(void) { return lat::g_msg.c_str(); }
 int64_t lattice_last_error_index(void) { return lat::g_index; }
-int lattice_abi_version(void) { return 3; }
+int lattice_abi_version(void) { return 4; }
 
 lattice_status lattice_stable_hash(int64_t n, const uint8_t* bytes, const int64_t* off,
                                    uint64_t seed, uint64_t* out, lattice_stream stream) {

@@ -50,8 +50,9 @@ __device__ __forceinline__ void put(__nv_bfloat16* p, float v) { *p = __float2bf
 
 // pooled sums (caller order, [B][n][d] f32 or bf16) -> rms_norm_d -> row pos[b] of X0
 template <typename TI, typename TO>
+// in: [B][n][d] rows of features [foff, foff + n) of an n_out-wide X0 row
 __global__ void pooled_norm_kernel(int64_t B, int n, int d, const TI* __restrict__ in,
-                                   const int32_t* __restrict__ pos, TO* __restrict__ out) {
+                                   const int32_t* __restrict__ pos, TO* __restrict__ out, int n_out, int foff) {
     const int lane = threadIdx.x & 31;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < B * n;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -68,7 +69,7 @@ __global__ void pooled_norm_kernel(int64_t B, int n, int d, const TI* __restrict
         }
         ss = warp_sum(ss);
         const float denom = sqrtf(ss / (float)d + 1e-6f);
-        TO* dst = out + ((int64_t)pos[b] * n + f) * d;
+        TO* dst = out + ((int64_t)pos[b] * n_out + foff + f) * d;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int c = lane + 32 * i;
@@ -80,7 +81,7 @@ __global__ void pooled_norm_kernel(int64_t B, int n, int d, const TI* __restrict
 // table-wise shards [S][B][n/S][d] (already normalised by their owners) -> X0 rows pos[b];
 // one warp per (b, f), 16-byte vectors; dtype-agnostic (vec = d * es / 16)
 __global__ void shard_gather_kernel(int64_t B, int n, int d, int es, int S, const uint8_t* __restrict__ in,
-                                    const int32_t* __restrict__ pos, uint8_t* __restrict__ out) {
+                                    const int32_t* __restrict__ pos, uint8_t* __restrict__ out, int n_out) {
     const int lane = threadIdx.x & 31;
     const int nl = n / S;
     const int row = d * es;      // bytes per embedding
@@ -91,7 +92,7 @@ __global__ void shard_gather_kernel(int64_t B, int n, int d, int es, int S, cons
         const int f = (int)(w - b * n);
         const int o = f / nl, fl = f - o * nl;
         const uint4* src = reinterpret_cast<const uint4*>(in + (((int64_t)o * B + b) * nl + fl) * row);
-        uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)pos[b] * n + f) * row);
+        uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)pos[b] * n_out + f) * row);
         for (int i = lane; i < vec; i += 32) dst[i] = src[i];
     }
 }
@@ -112,6 +113,9 @@ struct lattice_net {
     std::vector<void*> mlp;      // [blocks * n_mlp] -> [out][in]
     void* T1 = nullptr;          // [G * th][n*d]
     float* T2 = nullptr;         // [G][heads][th] fp32
+    void* D1 = nullptr;          // dense processor [dense_hidden][dense_in]
+    void* D2 = nullptr;          // [dense_features*d][dense_hidden]
+    void *Din = nullptr, *Hd = nullptr, *Od = nullptr;  // dense input copy, hidden, output rows
     // workspace
     int32_t *pos = nullptr, *order = nullptr, *seg = nullptr;
     int4* tiles = nullptr;
@@ -123,6 +127,7 @@ struct lattice_net {
     std::vector<lat::fm::Plan> fm_plans;              // [blocks]
     std::vector<lat::gemm::GemmPlan> mlp_plans;       // [blocks * n_mlp]
     lat::gemm::GemmPlan tower_plan;
+    lat::gemm::GemmPlan dense_plans[2];
     // timing
     bool timing = false;
     std::vector<cudaEvent_t> ev;
@@ -189,6 +194,14 @@ lattice_status validate(const lattice_net_config* c) {
     if (c->tower_hidden < 8 || c->tower_hidden > 2048 || c->tower_hidden % 8)
         return set_error(LATTICE_USAGE, "network: tower_hidden must be a multiple of 8 in [8, 2048]");
     if (c->max_batch < 1 || c->max_batch > (1ll << 30)) return set_error(LATTICE_USAGE, "network: bad max_batch");
+    if (c->dense_features < 0 || c->dense_features >= c->n)
+        return set_error(LATTICE_USAGE, "network: dense_features must be in [0, n)");
+    if (c->dense_features > 0) {
+        if (c->dense_in < 8 || c->dense_in % 8)
+            return set_error(LATTICE_USAGE, "network: dense_in must be a positive multiple of 8");
+        if (c->dense_hidden < 8 || c->dense_hidden > 2048 || c->dense_hidden % 8)
+            return set_error(LATTICE_USAGE, "network: dense_hidden must be a multiple of 8 in [8, 2048]");
+    }
     return LATTICE_OK;
 }
 
@@ -247,6 +260,34 @@ lattice_status build_plans(lattice_net* net) {
                            in, out, p, (int)((Bm + 127) / 128), net->f32);
             if (s != LATTICE_OK) return s;
         }
+    }
+    if (c.dense_features > 0) {  // dense processor: swish_rn hidden layer, linear out
+        gemm::Params d1 = {};
+        d1.M = (int)Bm;
+        d1.N = c.dense_hidden;
+        d1.K = c.dense_in;
+        d1.out_bf16 = net->f32 ? 0 : 1;
+        d1.N_full = c.dense_hidden;
+        d1.C = net->Hd;
+        d1.ldc = c.dense_hidden;
+        d1.epi = c.hard ? gemm::kSwishHard : gemm::kSwish;
+        d1.cluster = (c.dense_hidden + 255) / 256;
+        lattice_status s = gemm::plan(&net->dense_plans[0], net->Din, c.dense_in, Bm, net->D1, c.dense_in,
+                                      c.dense_hidden, d1, (int)((Bm + 127) / 128), net->f32);
+        if (s != LATTICE_OK) return s;
+        gemm::Params d2 = {};
+        d2.M = (int)Bm;
+        d2.N = c.dense_features * c.d;
+        d2.K = c.dense_hidden;
+        d2.out_bf16 = net->f32 ? 0 : 1;
+        d2.N_full = d2.N;
+        d2.C = net->Od;
+        d2.ldc = d2.N;
+        d2.epi = gemm::kStore;
+        d2.cluster = 1;
+        s = gemm::plan(&net->dense_plans[1], net->Hd, c.dense_hidden, Bm, net->D2, c.dense_hidden, d2.N, d2,
+                       (int)((Bm + 127) / 128), net->f32);
+        if (s != LATTICE_OK) return s;
     }
     gemm::Params p = {};
     p.M = (int)Bm;
@@ -323,6 +364,16 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
         NET_TRY(lattice_fill_weights(net->T2 + (size_t)g * c.heads * c.tower_hidden, LATTICE_F32, c.heads,
                                      c.tower_hidden, seed, weight_tag(g, 5, 0), nullptr));
     }
+    if (c.dense_features > 0) {
+        const int od = c.dense_features * c.d;
+        NET_TRY(dalloc_bytes(net, &net->D1, es * (size_t)c.dense_hidden * c.dense_in));
+        NET_TRY(dalloc_bytes(net, &net->D2, es * (size_t)od * c.dense_hidden));
+        NET_TRY(lattice_fill_weights(net->D1, wdt, c.dense_hidden, c.dense_in, seed, weight_tag(0, 6, 0), nullptr));
+        NET_TRY(lattice_fill_weights(net->D2, wdt, od, c.dense_hidden, seed, weight_tag(0, 7, 0), nullptr));
+        NET_TRY(dalloc_bytes(net, &net->Din, es * (size_t)Bm * c.dense_in));
+        NET_TRY(dalloc_bytes(net, &net->Hd, es * (size_t)Bm * c.dense_hidden));
+        NET_TRY(dalloc_bytes(net, &net->Od, es * (size_t)Bm * od));
+    }
     int max_hidden = 8;
     for (int i = 1; i < c.n_mlp; ++i) max_hidden = max_hidden > c.mlp[i] ? max_hidden : c.mlp[i];
     NET_TRY(dalloc(net, &net->pos, (size_t)Bm));
@@ -361,6 +412,8 @@ const void* lattice_net_weight(lattice_net* net, int32_t block, int32_t kind, in
                        : nullptr;
         case 4: return net->T1;
         case 5: return net->T2;
+        case 6: return net->D1;
+        case 7: return net->D2;
         default: return nullptr;
     }
 }
@@ -434,6 +487,7 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
         if (_s != LATTICE_OK) return _s;          \
     } while (0)
     const bool in_place = !batch->tables && batch->pooled_layout == 2;  // X0 written by peers
+    const int nc = c.n - c.dense_features;  // sparse (table-pooled) embeddings come first
     FWD_TRY(mark());
     if (!in_place) FWD_TRY(lattice_net_bucket(net, B, batch->domain, stream));
     FWD_TRY(mark());
@@ -441,7 +495,7 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
         // lattice_net_bucket ran for this batch and lattice_peer_embedding_bag filled X0
     } else if (batch->tables) {
         lattice_bag_args a = {};
-        a.features = c.n;
+        a.features = nc;
         a.batch = B;
         a.dim = c.d;
         a.table_dtype = batch->table_dtype;
@@ -460,33 +514,55 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
         FWD_TRY(lattice_embedding_bag(&a, stream));
     } else {
         LAT_REQUIRE(batch->pooled != nullptr, "lattice_net_forward: need tables or pooled input");
-        const int64_t warps = B * c.n;
+        const int64_t warps = B * nc;
         const unsigned grid = (unsigned)((warps * 32 + 255) / 256 < 148 * 64 ? (warps * 32 + 255) / 256 : 148 * 64);
         if (batch->pooled_layout == 1) {
-            LAT_REQUIRE(batch->shards >= 1 && c.n % batch->shards == 0 &&
+            LAT_REQUIRE(batch->shards >= 1 && nc % batch->shards == 0 &&
                             batch->table_dtype == (net->f32 ? LATTICE_F32 : LATTICE_BF16),
                         "lattice_net_forward: sharded pooled input needs the net dtype and shards dividing n");
-            shard_gather_kernel<<<grid, 256, 0, stream>>>(B, c.n, c.d, (int)net->es, batch->shards,
+            shard_gather_kernel<<<grid, 256, 0, stream>>>(B, nc, c.d, (int)net->es, batch->shards,
                                                           static_cast<const uint8_t*>(batch->pooled), net->pos,
-                                                          static_cast<uint8_t*>(net->X[0]));
+                                                          static_cast<uint8_t*>(net->X[0]), c.n);
         } else if (batch->table_dtype == LATTICE_F32) {
             if (net->f32)
                 pooled_norm_kernel<float, float><<<grid, 256, 0, stream>>>(
-                    B, c.n, c.d, static_cast<const float*>(batch->pooled), net->pos, static_cast<float*>(net->X[0]));
+                    B, nc, c.d, static_cast<const float*>(batch->pooled), net->pos, static_cast<float*>(net->X[0]), c.n, 0);
             else
                 pooled_norm_kernel<float, __nv_bfloat16><<<grid, 256, 0, stream>>>(
-                    B, c.n, c.d, static_cast<const float*>(batch->pooled), net->pos,
-                    static_cast<__nv_bfloat16*>(net->X[0]));
+                    B, nc, c.d, static_cast<const float*>(batch->pooled), net->pos,
+                    static_cast<__nv_bfloat16*>(net->X[0]), c.n, 0);
         } else {
             if (net->f32)
                 pooled_norm_kernel<__nv_bfloat16, float><<<grid, 256, 0, stream>>>(
-                    B, c.n, c.d, static_cast<const __nv_bfloat16*>(batch->pooled), net->pos,
-                    static_cast<float*>(net->X[0]));
+                    B, nc, c.d, static_cast<const __nv_bfloat16*>(batch->pooled), net->pos,
+                    static_cast<float*>(net->X[0]), c.n, 0);
             else
                 pooled_norm_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, stream>>>(
-                    B, c.n, c.d, static_cast<const __nv_bfloat16*>(batch->pooled), net->pos,
-                    static_cast<__nv_bfloat16*>(net->X[0]));
+                    B, nc, c.d, static_cast<const __nv_bfloat16*>(batch->pooled), net->pos,
+                    static_cast<__nv_bfloat16*>(net->X[0]), c.n, 0);
         }
+        LAT_CUDA(cudaGetLastError());
+    }
+    if (c.dense_features > 0) {  // dense processor -> rows [nc, n) of X0
+        LAT_REQUIRE(batch->dense != nullptr, "lattice_net_forward: the network has dense features; batch.dense is null");
+        LAT_CUDA(cudaMemcpyAsync(net->Din, batch->dense, net->es * (size_t)B * c.dense_in, cudaMemcpyDeviceToDevice,
+                                 stream));
+        for (int i = 0; i < 2; ++i) {
+            gemm::GemmPlan g = net->dense_plans[i];
+            g.p.M = (int)B;
+            g.grid_y = (int)((B + 127) / 128);
+            FWD_TRY(gemm::launch(g, stream));
+        }
+        const int64_t warps = B * c.dense_features;
+        const unsigned grid = (unsigned)((warps * 32 + 255) / 256 < 148 * 64 ? (warps * 32 + 255) / 256 : 148 * 64);
+        if (net->f32)
+            pooled_norm_kernel<float, float><<<grid, 256, 0, stream>>>(
+                B, c.dense_features, c.d, static_cast<const float*>(net->Od), net->pos,
+                static_cast<float*>(net->X[0]), c.n, nc);
+        else
+            pooled_norm_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, stream>>>(
+                B, c.dense_features, c.d, static_cast<const __nv_bfloat16*>(net->Od), net->pos,
+                static_cast<__nv_bfloat16*>(net->X[0]), c.n, nc);
         LAT_CUDA(cudaGetLastError());
     }
     FWD_TRY(mark());
