@@ -269,7 +269,9 @@ def dense_flops_per_sample(c):
     n, d, k, nL = c["n"], c["d"], c["k"], c["nL"]
     mlp = c["mlp"]
     per_block = 4 * n * d * k + 2 * nL * n * d + 2 * sum(mlp[i] * mlp[i + 1] for i in range(len(mlp) - 1))
-    return c["blocks"] * per_block + 2 * (n * d * c["tower_hidden"] + c["tower_hidden"] * c["heads"])
+    dense = 2 * (c.get("dense_in", 0) * c.get("dense_hidden", 0) +
+                 c.get("dense_hidden", 0) * c.get("dense_features", 0) * d)  # dense processor
+    return c["blocks"] * per_block + 2 * (n * d * c["tower_hidden"] + c["tower_hidden"] * c["heads"]) + dense
 
 
 def mlp_flops_per_sample(c):
@@ -278,6 +280,7 @@ def mlp_flops_per_sample(c):
 
 
 FULL_TASKS, FULL_WINDOWS = 4, [5400000, 86400000, 604800000]  # O = 4 objectives, {90min, 1d, 7d}
+FULL_DENSE = (16, 64, 256)  # dense embeddings, union-schema width, dense processor hidden
 
 
 LARGE = dict(n=512, d=128, blocks=4, nF=256, nL=256, k=32, mlp=[16384, 2048, 2048, 32768],
@@ -301,31 +304,33 @@ def run_mid(args, rank, world, local):
         large = True
         MID_ROWS, MID_B = LARGE_ROWS, LARGE_B
     backbone = LARGE if large else MID
-    c = dict(backbone, domains=16, heads=FULL_TASKS * len(FULL_WINDOWS)) if full else backbone
+    c = dict(backbone, domains=16, heads=FULL_TASKS * len(FULL_WINDOWS), dense_features=FULL_DENSE[0],
+             dense_in=FULL_DENSE[1], dense_hidden=FULL_DENSE[2]) if full else backbone
     n, d, B = c["n"], c["d"], MID_B
+    nc = n - c.get("dense_features", 0)  # embeddings pooled from tables (the rest: dense processor)
     net = L.Network(**c, max_batch=B, weight_seed=SEED_W)
     sharded = world > 1 or args.exchange == "peer1"  # peer1: the peer path at N=1 (experiments)
     peer = sharded and args.exchange in ("peer", "peer1")
     if sharded:  # table-wise: this rank owns features [rank*n/W, (rank+1)*n/W)
         from paper_2512_09200_b200.sharded import ShardedBags
-        sb = ShardedBags(n, B, d, world, rank)
+        sb = ShardedBags(nc, B, d, world, rank)
         n_tab = sb.Fl
         tab = torch.empty((n_tab, MID_ROWS, d), dtype=torch.bfloat16, device="cuda")
         L.fill_tables(tab, SEED_T, feature_base=sb.owned()[0], rows_total=MID_ROWS)
         if peer:  # owners write pooled rows straight into every rank's X0 over NVLink
             from paper_2512_09200_b200.peer import PeerBags
-            pb = PeerBags(net, n, B, d, world, rank)
+            pb = PeerBags(net, nc, B, d, world, rank, row_stride=n * d)
         else:
             send = torch.empty((world * B, sb.Fl, d), dtype=torch.bfloat16, device="cuda")
             recv = torch.empty_like(send)
     else:
-        n_tab = n
-        tab = torch.empty((n, MID_ROWS, d), dtype=torch.bfloat16, device="cuda")
+        n_tab = nc
+        tab = torch.empty((nc, MID_ROWS, d), dtype=torch.bfloat16, device="cuda")
         L.fill_tables(tab, SEED_T)
     tables = list(tab.unbind(0))
     ptrs = torch.tensor([t.data_ptr() for t in tables], dtype=torch.int64, device="cuda")
     rows = torch.full((n_tab,), MID_ROWS, dtype=torch.int64, device="cuda")
-    offsets, ids = L.synth_bags(n, B, MID_MAXLEN, MID_ROWS, SEED_D + rank)
+    offsets, ids = L.synth_bags(nc, B, MID_MAXLEN, MID_ROWS, SEED_D + rank)
     dom = L.synth_domains(B, c["domains"], SEED_D + rank)
     n_ids = int(offsets[-1].item())
     if peer:
@@ -342,6 +347,18 @@ def run_mid(args, rank, world, local):
 
     if full:
         imp = L.synth_impressions(B, FULL_TASKS, 7 + rank)
+        # dense features of the 16 consolidated domains: domain g declares its own subset of a
+        # 64-name pool; merge_domains re-lays them out under the union schema every step
+        g_dense = torch.Generator().manual_seed(0xD15E)
+        declared = [[f"x{int(i)}" for i in torch.randperm(FULL_DENSE[1], generator=g_dense)[:8 + 3 * g]]
+                    for g in range(c["domains"])]
+        union, src = L.union_schema(declared)
+        src_col = torch.full((c["domains"], FULL_DENSE[1]), -1, dtype=torch.int32)
+        src_col[:, : len(union)] = torch.tensor(src, dtype=torch.int32)
+        src_col = src_col.cuda()
+        max_decl = max(len(x) for x in declared)
+        dvals = torch.randn((B, max_decl), generator=torch.Generator(device="cuda").manual_seed(rank),
+                            device="cuda")
         nW = len(FULL_WINDOWS)
         obj_out = (torch.empty((B, FULL_TASKS), dtype=torch.float32, device="cuda"),
                    torch.empty(FULL_TASKS, dtype=torch.float64, device="cuda"),
@@ -349,17 +366,20 @@ def run_mid(args, rank, world, local):
                    torch.empty((nW, FULL_TASKS), dtype=torch.int64, device="cuda"))
         wp = [1.0 / len(FULL_WINDOWS)] * len(FULL_WINDOWS)
 
-    def forward(dm, off, ii, out, imp_cols=None):
+    def forward(dm, off, ii, out, imp_cols=None, dv=None):
+        dense = None
         if full:  # K5: window assignment + per-window labels of this batch's impressions
             win, lab, _ = L.zipper_assign_labels(*(imp_cols or imp), FULL_WINDOWS, wp, 7, routed=False,
                                                check_errors=False)
+            # merge_domains (union schema, zero padding) -> the dense processor's input
+            dense = L.merge_dense(dm, dvals if dv is None else dv, src_col, FULL_DENSE[1], check_errors=False)
         if peer:
-            pb.forward(key_of[id(off)], dm, tables, ptrs, rows, logits=out)
+            pb.forward(key_of[id(off)], dm, tables, ptrs, rows, logits=out, dense=dense)
         elif sharded:
             pooled = sb.forward_embeddings(off, ii, tables, ptrs, rows, send=send, recv=recv)
-            net.forward(dm, pooled=pooled, shards=world, logits=out)
+            net.forward(dm, pooled=pooled, shards=world, logits=out, dense=dense)
         else:
-            net.forward(dm, off, ii, ptrs, rows, torch.bfloat16, logits=out)
+            net.forward(dm, off, ii, ptrs, rows, torch.bfloat16, logits=out, dense=dense)
         if full:  # the window mask applied to the heads (training routes each sample's loss)
             # post-tower batch step: routed logits, per-task correlation loss (fp64), window summary
             L.routed_objectives(out, win, lab, FULL_TASKS, nW, check_errors=False, out=obj_out)
@@ -388,6 +408,7 @@ def run_mid(args, rank, world, local):
     # per-stage device times (separate pass, events between stages)
     net.set_timing(True)
     stages, emb_ms, peer_split = [], [], []
+    dense0 = L.merge_dense(dom, dvals, src_col, FULL_DENSE[1]) if full else None
     for _ in range(5):
         if peer:  # bucket + barrier + owner kernel (NVLink reads/stores) + barrier
             barrier(world)
@@ -395,7 +416,7 @@ def run_mid(args, rank, world, local):
             a0.record(stream)
             pb.forward_embeddings("main", dom, tables, ptrs, rows, timed=True)
             a1.record(stream)
-            net.forward_in_place(dom, logits=logits)
+            net.forward_in_place(dom, logits=logits, dense=dense0)
             torch.cuda.synchronize()
             emb_ms.append(a0.elapsed_time(a1))
             peer_split.append(pb.stage_ms())
@@ -404,7 +425,7 @@ def run_mid(args, rank, world, local):
             a0.record(stream)
             pooled = sb.forward_embeddings(offsets, ids, tables, ptrs, rows, send=send, recv=recv)
             a1.record(stream)
-            net.forward(dom, pooled=pooled, shards=world, logits=logits)
+            net.forward(dom, pooled=pooled, shards=world, logits=logits, dense=dense0)
             torch.cuda.synchronize()
             emb_ms.append(a0.elapsed_time(a1))
         else:
@@ -418,7 +439,7 @@ def run_mid(args, rank, world, local):
     t_mlp = [st[3 + 2 * b] for b in range(c["blocks"])]
     t_tower = st[2 + 2 * c["blocks"]]
     hbm, tf_burst, tf_sust, src = load_peaks()
-    emb_bytes = micro_bytes(n_ids, n, B, d, 2, 2)
+    emb_bytes = micro_bytes(n_ids, nc, B, d, 2, 2)
     flops = dense_flops_per_sample(c) * B
     mlp_fl = mlp_flops_per_sample(c) * B
     mlp_ms = statistics.mean(t_mlp)
@@ -441,6 +462,8 @@ def run_mid(args, rank, world, local):
     if full:  # the impression log columns travel with the batch too
         h_imp = [t.cpu().pin_memory() for t in imp]
         d_imp = [[torch.empty_like(t) for t in imp] for _ in range(2)]
+        h_dv = dvals.cpu().pin_memory()
+        d_dv = [torch.empty_like(dvals) for _ in range(2)]
     cstream = torch.cuda.Stream()
     copied = [torch.cuda.Event() for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
@@ -455,6 +478,7 @@ def run_mid(args, rank, world, local):
             if full:
                 for dst, src in zip(d_imp[i % 2], h_imp):
                     dst.copy_(src, non_blocking=True)
+                d_dv[i % 2].copy_(h_dv, non_blocking=True)
             copied[i % 2].record(cstream)
 
     def e2e_run(k):
@@ -466,7 +490,7 @@ def run_mid(args, rank, world, local):
                 h2d(i + 1)
             stream.wait_event(copied[i % 2])
             o, ii, dm = bufs[i % 2]
-            forward(dm, o, ii, logits, d_imp[i % 2] if full else None)
+            forward(dm, o, ii, logits, d_imp[i % 2] if full else None, d_dv[i % 2] if full else None)
             consumed[i % 2].record(stream)
             h_out.copy_(logits, non_blocking=True)
 
@@ -492,7 +516,9 @@ def run_mid(args, rank, world, local):
     if full:
         metric = "Lattice Network samples/sec (full consolidated portfolio, forward step)"
         wl = ("full consolidated portfolio: 16 domains x (4 objectives x 3 windows {90min,1d,7d}) "
-              "heads, per-sample Zipper window assignment (seed 7, p=1/3) + window-routed heads + correlation loss + window summary each step; "
+              "heads, per-sample Zipper window assignment (seed 7, p=1/3) + window-routed heads + correlation loss + window summary each step; 16 dense embeddings from a "
+              "dense processor (64-wide union schema of the domains' dense features, merge_domains zero "
+              "padding, MLP 64-256-16x128) in place of 16 tables; "
               + ("large backbone (512 tables x 1.5M rows x 128 bf16 = 196.6 GB table-wise sharded, l=4, "
                  "n=512, MLP 16384-2048-2048-32768, tower 65536-512-12), B=65536/GPU" if large else
                  "mid-width backbone on 1 GPU (256 sparse feats x 100k rows x 128, l=4, "
@@ -522,8 +548,9 @@ def run_mid(args, rank, world, local):
                                    (f"table-wise sharded embeddings over {world} GPUs (ids + pooled "
                                     f"all-to-all, NCCL/NVLink) + dense replicas")) if sharded else "1 GPU"},
         "e2e": {"value": world * B / (e2e_ms / 1e3), "unit": "samples/s",
-                "h2d_bytes_per_step": (n * B + 1) * 8 + n_ids * 4 + B * 4 +
-                                      (sum(t.numel() * t.element_size() for t in imp) if full else 0),
+                "h2d_bytes_per_step": (nc * B + 1) * 8 + n_ids * 4 + B * 4 +
+                                      (sum(t.numel() * t.element_size() for t in imp) + dvals.numel() * 4
+                                       if full else 0),
                 "d2h_bytes_per_step": B * c["heads"] * 4},
         "roofline": {"bound": "tensor", "achieved": mlp_achieved, "peak": tf_sust, "unit": "TFLOP/s",
                      "frac": mlp_achieved / tf_sust,

@@ -36,7 +36,9 @@ import torch.distributed as dist
 
 class PeerBags:
     def __init__(self, net, n_features, batch, dim, world, rank, group=None, timeout_s=30.0, ops=None,
-                 device="cuda"):
+                 device="cuda", row_stride=None):
+        """n_features: table-pooled embeddings (sharded); row_stride: elements per X0 row
+        (n * d when the network also has dense embeddings after the pooled ones)."""
         if n_features % world:
             raise ValueError("table-wise sharding needs the feature count divisible by the world size")
         if ops is None:
@@ -45,6 +47,7 @@ class PeerBags:
         self.net = net
         self.F, self.B, self.D, self.W, self.r = n_features, batch, dim, world, rank
         self.Fl = n_features // world
+        self.row_stride = row_stride or n_features * dim
         self.group = group
         self.timeout_s = timeout_s
         self.device = device
@@ -96,16 +99,16 @@ class PeerBags:
             if "stores" in dbg:
                 out_ptrs = loc(out_ptrs)
         self.ops.peer_embedding_bag(self.r, self.W, tables, table_ptrs, rows, self.r * self.Fl, self.B,
-                                    off_ptrs, ids_ptrs, pos_ptrs, out_ptrs, self.F * self.D,
+                                    off_ptrs, ids_ptrs, pos_ptrs, out_ptrs, self.row_stride,
                                     normalize=True, stream=stream)
 
-    def forward(self, key, domain, tables, table_ptrs, rows, logits=None, stream=None):
+    def forward(self, key, domain, tables, table_ptrs, rows, logits=None, stream=None, dense=None):
         """Steps 1-5 of the module docstring: logits of this rank's batch."""
         self.net.bucket(domain, stream=stream)
         self.barrier(stream)
         self.pool(key, tables, table_ptrs, rows, stream)
         self.barrier(stream)
-        return self.net.forward_in_place(domain, logits=logits, stream=stream)
+        return self.net.forward_in_place(domain, logits=logits, stream=stream, dense=dense)
 
     def forward_embeddings(self, key, domain, tables, table_ptrs, rows, stream=None, timed=False):
         """Steps 1-4 only (the embedding stage). timed: CUDA events between the sub-steps,

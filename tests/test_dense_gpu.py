@@ -14,7 +14,7 @@ from test_network_gpu import SEED_D, SEED_T, SEED_W, assert_logits_close
 pytestmark = pytest.mark.gpu
 
 DENSE = dict(n=24, d=128, blocks=2, nF=12, nL=12, k=16, mlp=[384, 512, 1536], domains=3, heads=4,
-             tower_hidden=128, dense_features=4, dense_in=32, dense_hidden=256)
+             tower_hidden=128, dense_features=4, dense_in=40, dense_hidden=256)
 
 
 def make_dense(B, G, seed=5):
@@ -37,7 +37,7 @@ def test_merge_dense_bit_exact():
     import paper_2512_09200_b200 as L
     B, G = 5000, 3
     declared, union, src, dom, vals = make_dense(B, G)
-    width = 32  # union (<= 32) padded to the GEMM-friendly width
+    width = 48  # the union (<= 40 names) padded to a GEMM-friendly width
     src_w = np.full((G, width), -1, np.int32)
     src_w[:, : len(union)] = src
     d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
