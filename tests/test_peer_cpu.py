@@ -59,7 +59,7 @@ class FakeNet:
     def bucket(self, domain, stream=None):
         self.log.append(("bucket",))
 
-    def forward_in_place(self, domain, logits=None, stream=None):
+    def forward_in_place(self, domain, logits=None, stream=None, dense=None):
         self.log.append(("forward",))
         return logits
 
@@ -84,6 +84,9 @@ def _worker(rank, world, port, q):
         bag = [e for e in ops.log if e[0] == "bag"][0]
         seq = [e[0] for e in ops.log if e[0] != "close"]
         q.put((rank, bag, seq, off.data_ptr(), ids.data_ptr(), sum(e[0] == "close" for e in ops.log)))
+    except Exception as e:  # surface worker failures instead of a queue timeout
+        q.put((rank, "error", repr(e), 0, 0, 0))
+        raise
     finally:
         dist.destroy_process_group()
 
@@ -99,6 +102,7 @@ def test_peer_exchange_pointer_tables(world):
     res = {}
     for _ in range(world):
         r, bag, seq, offp, idsp, closes = q.get(timeout=120)
+        assert bag != "error", seq
         res[r] = (bag, seq, offp, idsp, closes)
     for p in procs:
         p.join(timeout=60)
