@@ -199,6 +199,47 @@ lattice_status lattice_merge_dense(int64_t n, int32_t domains, int32_t max_decla
                                    int32_t out_dtype, void* out, int32_t check, lattice_stream stream);
 
 /* ======================================================================================
+ * KTAP student-input assembly -- replaces the read side of
+ * TeacherEmbeddingStore::student_query (ktap.hpp:133-152: TTL validity inclusive at exactly
+ * ttl, label smoothing of the teacher logit on read) and student_feature_vector
+ * (ktap.hpp:221-229: [base || teacher embedding], zeros on a miss), with the teacher embedding
+ * clipped (clip_features, numerics.hpp:139) for a batch of queries. The store's
+ * key -> entry map and refresh queue stay on the host (string keys, mutex-serialised writes):
+ * the caller passes each query's entry slot (-1 = absent). The output row can be the
+ * network's dense input (dense_in = base_dim + dim).
+ * ==================================================================================== */
+typedef struct {
+    int64_t n;                   /* queries */
+    int32_t base_dim, dim;       /* base feature width, StoreConfig.dimension */
+    const float* base;           /* [n][base_dim] */
+    const int64_t* slot;         /* [n] store entry of the query's (user, item) pair, -1 = absent */
+    const float* store_emb;      /* [entries][dim] */
+    const float* store_logit;    /* [entries] (required when teacher_logit is set) */
+    const int64_t* written_at;   /* [entries] */
+    int64_t ttl_ms;              /* StoreConfig.ttl_ms (> 0) */
+    int64_t now;                 /* query clock */
+    double clip;                 /* > 0: clip the teacher block to [-clip, clip]; 0: off */
+    double smoothing;            /* in [0, 1): StoreConfig.label_smoothing; < 0: off */
+    int32_t out_dtype;           /* lattice_dtype of out */
+    void* out;                   /* [n][base_dim + dim] */
+    float* teacher_logit;        /* optional [n]: (smoothed) logit on a hit, NaN on a miss */
+    uint8_t* hit;                /* optional [n] */
+} lattice_student_args;
+
+lattice_status lattice_student_inputs(const lattice_student_args* args, lattice_stream stream);
+
+/* Element/row ops of numerics.hpp in fp64, DEVICE arrays: clip_features (:139, bit-exact),
+ * smooth_labels (:147, bit-exact; a label other than 0/1 -> USAGE with check = 1),
+ * swish_rn_jvp (:113-136) per row of a [rows][width] matrix (non-finite -> DATA). */
+lattice_status lattice_clip_features(int64_t n, const double* x, double c, double* out,
+                                     lattice_stream stream);
+lattice_status lattice_smooth_labels(int64_t n, const double* y, double eps_s, double* out,
+                                     int32_t check, lattice_stream stream);
+lattice_status lattice_swish_rn_jvp(int64_t rows, int64_t width, double eps, const double* x,
+                                    const double* tangent, double* out, int32_t check,
+                                    lattice_stream stream);
+
+/* ======================================================================================
  * Post-tower batch reductions. fp64, deterministic (fixed-order
  * per-block partials, no float atomics).
  * lattice_correlation_loss -- replaces lattice::correlation_loss (numerics.hpp:46-78) for

@@ -96,6 +96,15 @@ def load_oracle():
         lib.lo_dense_processor.restype = None
         lib.lo_dense_processor.argtypes = [ctypes.POINTER(LoNetCfg), ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                            _P, _P, _I64, _P, _P, ctypes.c_int]
+        for name in ("lo_clip_features", "lo_smooth_labels"):
+            f = getattr(lib, name)
+            f.restype = ctypes.c_int
+            f.argtypes = [_P, _SZ, _D, _P]
+        lib.lo_swish_rn_jvp.restype = ctypes.c_int
+        lib.lo_swish_rn_jvp.argtypes = [_P, _P, _SZ, _D, _P]
+        lib.lo_student_inputs.restype = None
+        lib.lo_student_inputs.argtypes = [_I64, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P, _I64, _I64, _D, _D,
+                                          ctypes.c_int, _P, _P, _P]
         lib.lo_routed_objectives.restype = ctypes.c_int
         lib.lo_routed_objectives.argtypes = [_I64, ctypes.c_int, ctypes.c_int, _P, _P, _P, _D, _P, _P, _P, _P]
         _oracle = lib
@@ -133,6 +142,15 @@ def load_ref():
         lib.ref_correlation_loss.argtypes = [_P, _P, _SZ, _D, _P]
         lib.ref_merge_domains.restype = ctypes.c_int
         lib.ref_merge_domains.argtypes = [ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P, _P]
+        for name in ("ref_clip_features", "ref_smooth_labels"):
+            f = getattr(lib, name)
+            f.restype = ctypes.c_int
+            f.argtypes = [_P, _SZ, _D, _P]
+        lib.ref_swish_rn_jvp.restype = ctypes.c_int
+        lib.ref_swish_rn_jvp.argtypes = [_P, _P, _SZ, _D, _P]
+        lib.ref_student_queries.restype = ctypes.c_int
+        lib.ref_student_queries.argtypes = [_I64, ctypes.c_int, _P, _P, _P, _I64, _D, _I64, ctypes.c_int, _P, _P,
+                                            _I64, _D, _P, _P, _P]
         lib.ref_window_summary.restype = ctypes.c_int
         lib.ref_window_summary.argtypes = [_I64, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P, _P]
         _ref = lib
@@ -295,6 +313,60 @@ def dense_processor(cfg, n_dense, dense_in, dense_hidden, D1, D2, dense, pooled,
     load_oracle().lo_dense_processor(ctypes.byref(cfg), n_dense, dense_in, dense_hidden, ptr(D1), ptr(D2),
                                      dense.shape[0], ptr(dense), ptr(pooled), threads)
     return pooled
+
+
+def vec_op2(lib, name, x, arg):
+    """(rc, out) of an element op (x, n, scalar, out): clip_features / smooth_labels."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.zeros(max(len(x), 1), np.float64)
+    rc = getattr(lib, name)(ptr(x) if len(x) else None, len(x), arg, ptr(out))
+    return rc, out[: len(x)]
+
+
+def swish_rn_jvp(x, t, eps=1e-6, lib=None):
+    lib = lib or load_oracle()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    out = np.zeros(max(len(x), 1), np.float64)
+    name = "ref_swish_rn_jvp" if hasattr(lib, "ref_swish_rn_jvp") else "lo_swish_rn_jvp"
+    rc = getattr(lib, name)(ptr(x) if len(x) else None, ptr(t) if len(t) else None, len(x), eps, ptr(out))
+    return rc, out[: len(x)]
+
+
+def student_inputs(base, slot, store_emb, store_logit, written_at, ttl, now, clip=0.0, smoothing=-1.0, bf16=False):
+    """lo_student_inputs: (rows [n, base_dim+dim], logit [n], hit [n])."""
+    base = np.ascontiguousarray(base, dtype=np.float32)
+    slot = np.ascontiguousarray(slot, dtype=np.int64)
+    store_emb = np.ascontiguousarray(store_emb, dtype=np.float32)
+    store_logit = np.ascontiguousarray(store_logit, dtype=np.float32)
+    written_at = np.ascontiguousarray(written_at, dtype=np.int64)
+    n, bd = base.shape
+    dim = store_emb.shape[1]
+    out = np.zeros((n, bd + dim), np.float32)
+    logit = np.zeros(n, np.float32)
+    hit = np.zeros(n, np.uint8)
+    load_oracle().lo_student_inputs(n, bd, dim, ptr(base), ptr(slot), ptr(store_emb), ptr(store_logit),
+                                    ptr(written_at), ttl, now, clip, smoothing, int(bf16), ptr(out), ptr(logit),
+                                    ptr(hit))
+    return out, logit, hit
+
+
+def ref_student_queries(base, slot, store_emb, store_logit, written_at, ttl, now, clip=0.0, smoothing=-1.0):
+    """The reference's TeacherEmbeddingStore + student_feature_vector (+ clip_features):
+    (rc, rows fp64, logits fp64 (NaN on miss), hit)."""
+    base = np.ascontiguousarray(base, dtype=np.float64)
+    slot = np.ascontiguousarray(slot, dtype=np.int64)
+    emb = np.ascontiguousarray(store_emb, dtype=np.float64)
+    lg = np.ascontiguousarray(store_logit, dtype=np.float64)
+    wa = np.ascontiguousarray(written_at, dtype=np.int64)
+    n, bd = base.shape
+    E, dim = emb.shape
+    rows = np.zeros((n, bd + dim), np.float64)
+    logits = np.zeros(n, np.float64)
+    hit = np.zeros(n, np.uint8)
+    rc = load_ref().ref_student_queries(E, dim, ptr(emb), ptr(lg), ptr(wa), ttl, smoothing, n, bd, ptr(base),
+                                        ptr(slot), now, clip, ptr(rows), ptr(logits), ptr(hit))
+    return rc, rows, logits, hit
 
 
 def synth_bags(F, B, max_len, rows, seed):

@@ -598,3 +598,64 @@ void lo_dense_processor(const lo_net_cfg* cfg, int n_dense, int dense_in, int de
     }
 }
 
+/* ---------------------------------------------------------------------------------------
+ * numerics.hpp:113-156 element/row ops and the KTAP student-input read side (ktap.hpp).
+ * ------------------------------------------------------------------------------------- */
+int lo_swish_rn_jvp(const double* x, const double* t, size_t n, double eps, double* out) {
+    if (!(eps > 0.0) || n == 0) return 1;
+    for (size_t i = 0; i < n; ++i)
+        if (!isfinite(x[i]) || !isfinite(t[i])) return 2;
+    double ss = 0.0, dot = 0.0;
+    for (size_t i = 0; i < n; ++i) ss += x[i] * x[i];
+    const double dn = (double)n;
+    const double d = sqrt(ss / dn + eps);
+    for (size_t i = 0; i < n; ++i) dot += x[i] * t[i];
+    dot /= dn;
+    const double d3 = d * d * d;
+    for (size_t i = 0; i < n; ++i) {
+        const double r = x[i] / d;
+        const double dr = t[i] / d - x[i] * dot / d3;
+        const double s = stable_sigmoid(r);
+        out[i] = s * (1.0 + r * (1.0 - s)) * dr;
+    }
+    return 0;
+}
+
+int lo_clip_features(const double* x, size_t n, double c, double* out) {
+    if (!(c > 0.0)) return 1;
+    for (size_t i = 0; i < n; ++i) out[i] = x[i] < -c ? -c : (x[i] > c ? c : x[i]);
+    return 0;
+}
+
+int lo_smooth_labels(const double* y, size_t n, double eps_s, double* out) {
+    if (!(eps_s >= 0.0 && eps_s < 1.0)) return 1;
+    for (size_t i = 0; i < n; ++i) {
+        if (y[i] != 0.0 && y[i] != 1.0) return 1;
+        out[i] = y[i] * (1.0 - eps_s) + eps_s / 2.0;
+    }
+    return 0;
+}
+
+void lo_student_inputs(int64_t n, int base_dim, int dim, const float* base, const int64_t* slot,
+                       const float* store_emb, const float* store_logit, const int64_t* written_at,
+                       int64_t ttl, int64_t now, double clip, double smoothing, int bf16, float* out,
+                       float* logit, uint8_t* hit) {
+    const int W = base_dim + dim;
+    for (int64_t q = 0; q < n; ++q) {
+        const int64_t s = slot[q];
+        const int h = s >= 0 && now - written_at[s] <= ttl;
+        float* row = out + q * W;
+        for (int c = 0; c < base_dim; ++c) row[c] = base[q * base_dim + c];
+        for (int c = 0; c < dim; ++c) {
+            double v = h ? (double)store_emb[s * dim + c] : 0.0;
+            if (h && clip > 0.0) v = v < -clip ? -clip : (v > clip ? clip : v);
+            row[base_dim + c] = (float)v;
+        }
+        if (bf16)
+            for (int c = 0; c < W; ++c) row[c] = lo_bf16_round(row[c]);
+        double l = h ? (double)store_logit[s] : NAN;
+        if (h && smoothing >= 0.0) l = l * (1.0 - smoothing) + smoothing / 2.0;
+        logit[q] = (float)l;
+        hit[q] = (uint8_t)h;
+    }
+}

@@ -137,6 +137,20 @@ void lo_dense_processor(const lo_net_cfg* cfg, int n_dense, int dense_in, int de
                         const float* D1, const float* D2, int64_t count, const float* dense,
                         float* pooled, int threads);
 
+/* ---- KTAP student inputs and numerics element ops --------------------
+ * lo_swish_rn_jvp numerics.hpp:113-136; lo_clip_features :139-144; lo_smooth_labels :147-156
+ * (returns 1 for a label other than 0/1). Return codes 0 / 1 UsageError / 2 DataError.
+ * lo_student_inputs: ktap.hpp:133-152 (hit = entry exists and now - written_at <= ttl;
+ * smoothed logit on read) + :221-229 ([base || embedding or zeros]) with the teacher block
+ * clipped (clip > 0). bf16 = 1 rounds the row to bf16. Logit NaN on a miss. */
+int lo_swish_rn_jvp(const double* x, const double* t, size_t n, double eps, double* out);
+int lo_clip_features(const double* x, size_t n, double c, double* out);
+int lo_smooth_labels(const double* y, size_t n, double eps_s, double* out);
+void lo_student_inputs(int64_t n, int base_dim, int dim, const float* base, const int64_t* slot,
+                       const float* store_emb, const float* store_logit, const int64_t* written_at,
+                       int64_t ttl, int64_t now, double clip, double smoothing, int bf16, float* out,
+                       float* logit, uint8_t* hit);
+
 /* ---- post-tower reductions ----------------------------------------
  * lo_correlation_loss: numerics.hpp:46-78 (1 - Cov/(sx*sy+eps), population moments, two
  * passes, clamped to [0,2], 1.0 when either side is constant). Returns 0 ok, 1 UsageError

@@ -13,6 +13,7 @@
 #define lattice lattice_ref
 #include "lattice/core.hpp"
 #include "lattice/datasets.hpp"
+#include "lattice/ktap.hpp"
 #include "lattice/numerics.hpp"
 #undef lattice
 
@@ -191,6 +192,63 @@ int ref_merge_domains(int G, int max_decl, const int32_t* decl, const int64_t* n
         for (size_t i = 0; i < u.records.size(); ++i)
             for (size_t c = 0; c < u.schema.features.size(); ++c)
                 out[i * u.schema.features.size() + c] = u.records[i].values.at(u.schema.features[c]);
+        return 0;
+    });
+}
+
+// numerics.hpp:113-156
+int ref_swish_rn_jvp(const double* x, const double* t, size_t n, double eps, double* out) {
+    return guarded([&] {
+        return copy_out(lattice_ref::swish_rn_jvp(std::span<const double>(x, n), std::span<const double>(t, n), eps),
+                        out);
+    });
+}
+int ref_clip_features(const double* x, size_t n, double c, double* out) {
+    return guarded([&] { return copy_out(lattice_ref::clip_features(std::span<const double>(x, n), c), out); });
+}
+int ref_smooth_labels(const double* y, size_t n, double eps_s, double* out) {
+    return guarded([&] { return copy_out(lattice_ref::smooth_labels(std::span<const double>(y, n), eps_s), out); });
+}
+
+// ktap.hpp:126-229 driven through its public API: entry e = pair ("u<e>", "i<e>") is written by
+// a refresh cycle at written_at[e] with embedding emb[e] and logit logit[e]; query q asks for
+// entry slot[q] (-1 = a pair never written) at `now`; the row is student_feature_vector(result,
+// base[q]) with the teacher block then clipped by clip_features when clip > 0. smoothing < 0 =
+// no label smoothing. Outputs rows [n][base_dim+dim], logits [n] (NaN on a miss), hit [n].
+int ref_student_queries(int64_t entries, int dim, const double* emb, const double* logit, const int64_t* written_at,
+                        int64_t ttl, double smoothing, int64_t n, int base_dim, const double* base,
+                        const int64_t* slot, int64_t now, double clip, double* rows, double* logits_out,
+                        uint8_t* hit_out) {
+    return guarded([&] {
+        lattice_ref::StoreConfig cfg;
+        cfg.dimension = static_cast<size_t>(dim);
+        cfg.ttl_ms = ttl;
+        cfg.refresh_budget = 1;
+        if (smoothing >= 0.0) cfg.label_smoothing = smoothing;
+        lattice_ref::TeacherEmbeddingStore store(cfg);
+        auto key = [](int64_t e) { return lattice_ref::PairKey{"u" + std::to_string(e), "i" + std::to_string(e)}; };
+        for (int64_t e = 0; e < entries; ++e) {
+            store.student_query(key(e), written_at[e]);  // miss -> queued
+            store.teacher_refresh_cycle(
+                [&](const lattice_ref::PairKey&) {
+                    return lattice_ref::TeacherOutput{std::vector<double>(emb + e * dim, emb + (e + 1) * dim), logit[e]};
+                },
+                written_at[e]);
+        }
+        const int W = base_dim + dim;
+        for (int64_t q = 0; q < n; ++q) {
+            const auto k = slot[q] >= 0 ? key(slot[q]) : lattice_ref::PairKey{"absent", "pair"};
+            const auto r = store.student_query(k, now);
+            auto row = lattice_ref::student_feature_vector(
+                r, std::span<const double>(base + q * base_dim, static_cast<size_t>(base_dim)), static_cast<size_t>(dim));
+            if (clip > 0.0) {
+                const auto c = lattice_ref::clip_features(std::span<const double>(row.data() + base_dim, dim), clip);
+                std::copy(c.begin(), c.end(), row.begin() + base_dim);
+            }
+            std::copy(row.begin(), row.end(), rows + q * W);
+            logits_out[q] = r.teacher_logit ? *r.teacher_logit : std::nan("");
+            hit_out[q] = r.hit ? 1 : 0;
+        }
         return 0;
     });
 }

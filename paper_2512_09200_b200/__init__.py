@@ -78,6 +78,13 @@ class ObjectiveArgs(ctypes.Structure):
                 ("positives", _P), ("check", _I32)]
 
 
+class StudentArgs(ctypes.Structure):
+    _fields_ = [("n", _I64), ("base_dim", _I32), ("dim", _I32), ("base", _P), ("slot", _P), ("store_emb", _P),
+                ("store_logit", _P), ("written_at", _P), ("ttl_ms", _I64), ("now", _I64), ("clip", ctypes.c_double),
+                ("smoothing", ctypes.c_double), ("out_dtype", _I32), ("out", _P), ("teacher_logit", _P),
+                ("hit", _P)]
+
+
 class GemmArgs(ctypes.Structure):
     _fields_ = [("M", _I64), ("N", _I64), ("K", _I64), ("A", _P), ("lda", _I64), ("B", _P),
                 ("ldb", _I64), ("C", _P), ("ldc", _I64), ("out_dtype", _I32), ("epilogue", _I32),
@@ -133,6 +140,10 @@ _sig("lattice_correlation_loss", ctypes.c_int, [_I64, _I32, _P, _I64, _P, _I64, 
 _sig("lattice_window_summary", ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _P, _I32, _P])
 _sig("lattice_routed_objectives", ctypes.c_int, [ctypes.POINTER(ObjectiveArgs), _P])
 _sig("lattice_merge_dense", ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _I32, _I32, _P, _I32, _P])
+_sig("lattice_student_inputs", ctypes.c_int, [ctypes.POINTER(StudentArgs), _P])
+_sig("lattice_clip_features", ctypes.c_int, [_I64, _P, ctypes.c_double, _P, _P])
+_sig("lattice_smooth_labels", ctypes.c_int, [_I64, _P, ctypes.c_double, _P, _I32, _P])
+_sig("lattice_swish_rn_jvp", ctypes.c_int, [_I64, _I64, ctypes.c_double, _P, _P, _P, _I32, _P])
 _sig("lattice_gemm", ctypes.c_int, [ctypes.POINTER(GemmArgs), _P])
 _sig("lattice_net_create", ctypes.c_int, [ctypes.POINTER(NetConfig), ctypes.POINTER(_P)])
 _sig("lattice_net_destroy", None, [_P])
@@ -153,7 +164,8 @@ EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_versio
            "lattice_net_stage_times", "lattice_peer_embedding_bag", "lattice_ipc_handle",
            "lattice_ipc_open", "lattice_ipc_close", "lattice_peer_barrier", "lattice_net_bucket",
            "lattice_net_buffer", "lattice_correlation_loss", "lattice_window_summary",
-           "lattice_routed_objectives", "lattice_merge_dense"]
+           "lattice_routed_objectives", "lattice_merge_dense", "lattice_student_inputs",
+           "lattice_clip_features", "lattice_smooth_labels", "lattice_swish_rn_jvp"]
 
 lib = _lib
 
@@ -388,6 +400,54 @@ def union_schema(declared):
                 union.append(f)
     src = [[feats.index(u) if u in feats else -1 for u in union] for feats in declared]
     return union, src
+
+
+def student_inputs(base, slot, store_emb, written_at, ttl_ms, now, store_logit=None, clip=0.0, smoothing=-1.0,
+                   out_dtype=None, stream=None):
+    """KTAP student-input assembly (ktap.hpp:133-152, 221-229): rows [n, base_dim + dim] =
+    [base || clip(teacher embedding) on a valid hit, zeros otherwise], the (smoothed) teacher
+    logit (NaN on a miss) and the hit flags. base fp32 [n, base_dim], slot int64 [n] (-1 absent),
+    store_emb fp32 [entries, dim], written_at int64 [entries]."""
+    import torch
+    n, bd = base.shape
+    dim = store_emb.shape[1]
+    odt = out_dtype or torch.bfloat16
+    out = torch.empty((n, bd + dim), dtype=odt, device=base.device)
+    logit = torch.empty(n, dtype=torch.float32, device=base.device) if store_logit is not None else None
+    hit = torch.empty(n, dtype=torch.uint8, device=base.device)
+    a = StudentArgs(n, bd, dim, _p(base), _p(slot), _p(store_emb), _p(store_logit), _p(written_at), ttl_ms, now,
+                    clip, smoothing, F32 if odt == torch.float32 else BF16, _p(out), _p(logit), _p(hit))
+    check(_lib.lattice_student_inputs(ctypes.byref(a), _stream(stream)))
+    return out, logit, hit
+
+
+def clip_features(x, c, stream=None):
+    """numerics.hpp:139 on an fp64 CUDA tensor."""
+    import torch
+    out = torch.empty_like(x)
+    check(_lib.lattice_clip_features(x.numel(), _p(x), c, _p(out), _stream(stream)))
+    return out
+
+
+def smooth_labels(y, eps_s, check_errors=True, stream=None):
+    """numerics.hpp:147 on an fp64 CUDA tensor of 0/1 labels."""
+    import torch
+    out = torch.empty_like(y)
+    check(_lib.lattice_smooth_labels(y.numel(), _p(y), eps_s, _p(out), 1 if check_errors else 0, _stream(stream)))
+    return out
+
+
+def swish_rn_jvp(x, tangent, eps=1e-6, check_errors=True, stream=None):
+    """numerics.hpp:113 per row of fp64 CUDA matrices (1-D = one row)."""
+    import torch
+    if x.shape != tangent.shape:
+        raise UsageError("swish_rn_jvp: length mismatch")
+    width = x.shape[-1] if x.dim() else 0
+    rows = x.numel() // width if width else 0
+    out = torch.empty_like(x)
+    check(_lib.lattice_swish_rn_jvp(rows, width, eps, _p(x), _p(tangent), _p(out), 1 if check_errors else 0,
+                                    _stream(stream)))
+    return out
 
 
 def lengths_to_offsets(lengths, out=None, stream=None):
