@@ -45,7 +45,8 @@ __global__ void student_kernel(lattice_student_args a, TO* __restrict__ out) {
             if (a.hit) a.hit[q] = hit ? 1 : 0;
             if (a.teacher_logit) {
                 double l = hit ? (double)a.store_logit[s] : __longlong_as_double(0x7ff8000000000000ll);
-                if (hit && a.smoothing >= 0.0) l = l * (1.0 - a.smoothing) + a.smoothing / 2.0;
+                // explicit roundings: no FMA contraction, the same two roundings as ktap.hpp:146
+                if (hit && a.smoothing >= 0.0) l = __dadd_rn(__dmul_rn(l, 1.0 - a.smoothing), a.smoothing / 2.0);
                 a.teacher_logit[q] = (float)l;
             }
         }
@@ -62,7 +63,7 @@ __global__ void smooth_kernel(int64_t n, const double* __restrict__ y, double ep
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double v = y[i];
         if (v != 0.0 && v != 1.0) atomicMin(bad, (unsigned long long)i);
-        out[i] = v * (1.0 - eps) + eps / 2.0;  // numerics.hpp:154
+        out[i] = __dadd_rn(__dmul_rn(v, 1.0 - eps), eps / 2.0);  // numerics.hpp:154, no FMA contraction
     }
 }
 
