@@ -280,7 +280,9 @@ def mlp_flops_per_sample(c):
 
 
 FULL_TASKS, FULL_WINDOWS = 4, [5400000, 86400000, 604800000]  # O = 4 objectives, {90min, 1d, 7d}
-FULL_DENSE = (16, 64, 256)  # dense embeddings, union-schema width, dense processor hidden
+FULL_DENSE = (16, 64, 256)  # dense embeddings, dense processor input width, dense processor hidden
+FULL_MERGED, FULL_TEACHER = 48, 16  # union-schema width of the merged dense features, KTAP teacher dim
+FULL_STORE, FULL_TTL = 1 << 20, 4 * 3600 * 1000  # KTAP teacher store entries, TTL (ms)
 
 
 LARGE = dict(n=512, d=128, blocks=4, nF=256, nL=256, k=32, mlp=[16384, 2048, 2048, 32768],
@@ -350,15 +352,24 @@ def run_mid(args, rank, world, local):
         # dense features of the 16 consolidated domains: domain g declares its own subset of a
         # 64-name pool; merge_domains re-lays them out under the union schema every step
         g_dense = torch.Generator().manual_seed(0xD15E)
-        declared = [[f"x{int(i)}" for i in torch.randperm(FULL_DENSE[1], generator=g_dense)[:8 + 3 * g]]
+        declared = [[f"x{int(i)}" for i in torch.randperm(FULL_MERGED, generator=g_dense)[:8 + 2 * g]]
                     for g in range(c["domains"])]
         union, src = L.union_schema(declared)
-        src_col = torch.full((c["domains"], FULL_DENSE[1]), -1, dtype=torch.int32)
+        src_col = torch.full((c["domains"], FULL_MERGED), -1, dtype=torch.int32)
         src_col[:, : len(union)] = torch.tensor(src, dtype=torch.int32)
         src_col = src_col.cuda()
         max_decl = max(len(x) for x in declared)
         dvals = torch.randn((B, max_decl), generator=torch.Generator(device="cuda").manual_seed(rank),
                             device="cuda")
+        # KTAP teacher store: 1M precomputed teacher embeddings with write times;
+        # each sample's (user, ad) pair maps to an entry (25% never computed), ~1/3 expired
+        gk = torch.Generator(device="cuda").manual_seed(0x7EAC + rank)
+        store_emb = torch.randn((FULL_STORE, FULL_TEACHER), generator=gk, device="cuda")
+        store_logit = torch.randn(FULL_STORE, generator=gk, device="cuda")
+        t_now = 1_700_000_000_000
+        written_at = t_now - torch.randint(0, FULL_TTL * 3 // 2, (FULL_STORE,), generator=gk, device="cuda")
+        slot = torch.randint(0, FULL_STORE, (B,), generator=gk, device="cuda")
+        slot[torch.rand(B, generator=gk, device="cuda") < 0.25] = -1
         nW = len(FULL_WINDOWS)
         obj_out = (torch.empty((B, FULL_TASKS), dtype=torch.float32, device="cuda"),
                    torch.empty(FULL_TASKS, dtype=torch.float64, device="cuda"),
@@ -371,8 +382,12 @@ def run_mid(args, rank, world, local):
         if full:  # K5: window assignment + per-window labels of this batch's impressions
             win, lab, _ = L.zipper_assign_labels(*(imp_cols or imp), FULL_WINDOWS, wp, 7, routed=False,
                                                check_errors=False)
-            # merge_domains (union schema, zero padding) -> the dense processor's input
-            dense = L.merge_dense(dm, dvals if dv is None else dv, src_col, FULL_DENSE[1], check_errors=False)
+            # merge_domains (union schema, zero padding), then KTAP student inputs [merged dense ||
+            # clipped teacher embedding or zeros] -> the dense processor's input
+            dv_, slot_ = dv if dv is not None else (dvals, slot)
+            merged = L.merge_dense(dm, dv_, src_col, FULL_MERGED, out_dtype=torch.float32, check_errors=False)
+            dense, _, _ = L.student_inputs(merged, slot_, store_emb, written_at, FULL_TTL, t_now,
+                                           store_logit=store_logit, clip=3.0, smoothing=0.1)
         if peer:
             pb.forward(key_of[id(off)], dm, tables, ptrs, rows, logits=out, dense=dense)
         elif sharded:
@@ -408,7 +423,8 @@ def run_mid(args, rank, world, local):
     # per-stage device times (separate pass, events between stages)
     net.set_timing(True)
     stages, emb_ms, peer_split = [], [], []
-    dense0 = L.merge_dense(dom, dvals, src_col, FULL_DENSE[1]) if full else None
+    dense0 = L.student_inputs(L.merge_dense(dom, dvals, src_col, FULL_MERGED, out_dtype=torch.float32), slot,
+                              store_emb, written_at, FULL_TTL, t_now)[0] if full else None
     for _ in range(5):
         if peer:  # bucket + barrier + owner kernel (NVLink reads/stores) + barrier
             barrier(world)
@@ -462,8 +478,8 @@ def run_mid(args, rank, world, local):
     if full:  # the impression log columns travel with the batch too
         h_imp = [t.cpu().pin_memory() for t in imp]
         d_imp = [[torch.empty_like(t) for t in imp] for _ in range(2)]
-        h_dv = dvals.cpu().pin_memory()
-        d_dv = [torch.empty_like(dvals) for _ in range(2)]
+        h_dv = (dvals.cpu().pin_memory(), slot.cpu().pin_memory())  # per-step dense values + KTAP slots
+        d_dv = [(torch.empty_like(dvals), torch.empty_like(slot)) for _ in range(2)]
     cstream = torch.cuda.Stream()
     copied = [torch.cuda.Event() for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
@@ -478,7 +494,8 @@ def run_mid(args, rank, world, local):
             if full:
                 for dst, src in zip(d_imp[i % 2], h_imp):
                     dst.copy_(src, non_blocking=True)
-                d_dv[i % 2].copy_(h_dv, non_blocking=True)
+                for dst, src in zip(d_dv[i % 2], h_dv):
+                    dst.copy_(src, non_blocking=True)
             copied[i % 2].record(cstream)
 
     def e2e_run(k):
@@ -513,12 +530,14 @@ def run_mid(args, rank, world, local):
         launches += 2  # owner bag kernel + offsets scan (the bag slot above is the shard gather)
     if full:
         launches += 6  # zipper_kernel + summary + 2 x (moments + fold) of routed_objectives
+        launches += 5  # merge_dense + student_inputs + 2 dense GEMMs + dense row norm
     if full:
         metric = "Lattice Network samples/sec (full consolidated portfolio, forward step)"
         wl = ("full consolidated portfolio: 16 domains x (4 objectives x 3 windows {90min,1d,7d}) "
               "heads, per-sample Zipper window assignment (seed 7, p=1/3) + window-routed heads + correlation loss + window summary each step; 16 dense embeddings from a "
-              "dense processor (64-wide union schema of the domains' dense features, merge_domains zero "
-              "padding, MLP 64-256-16x128) in place of 16 tables; "
+              "dense processor over [48-wide union schema of the domains' dense features (merge_domains "
+              "zero padding) || KTAP teacher embedding (16, 1M-entry store, TTL 4h, clipped; zeros on "
+              "miss)], MLP 64-256-16x128, in place of 16 tables; "
               + ("large backbone (512 tables x 1.5M rows x 128 bf16 = 196.6 GB table-wise sharded, l=4, "
                  "n=512, MLP 16384-2048-2048-32768, tower 65536-512-12), B=65536/GPU" if large else
                  "mid-width backbone on 1 GPU (256 sparse feats x 100k rows x 128, l=4, "
@@ -549,8 +568,8 @@ def run_mid(args, rank, world, local):
                                     f"all-to-all, NCCL/NVLink) + dense replicas")) if sharded else "1 GPU"},
         "e2e": {"value": world * B / (e2e_ms / 1e3), "unit": "samples/s",
                 "h2d_bytes_per_step": (nc * B + 1) * 8 + n_ids * 4 + B * 4 +
-                                      (sum(t.numel() * t.element_size() for t in imp) + dvals.numel() * 4
-                                       if full else 0),
+                                      (sum(t.numel() * t.element_size() for t in imp) + dvals.numel() * 4 +
+                                       slot.numel() * 8 if full else 0),
                 "d2h_bytes_per_step": B * c["heads"] * 4},
         "roofline": {"bound": "tensor", "achieved": mlp_achieved, "peak": tf_sust, "unit": "TFLOP/s",
                      "frac": mlp_achieved / tf_sust,
