@@ -8,6 +8,7 @@
 // conversion before its impression names the same first record and task as the reference.
 // zip_columns is the batched columnar entry for callers that already hold columns.
 
+#include <algorithm>
 #include <cmath>
 #include <map>
 #include <set>
@@ -41,6 +42,17 @@ struct DomainRecord {
     TimestampMs impression_time_ms = 0;
     std::map<FeatureId, double> values;
     std::map<TaskId, TimestampMs> conversions;
+};
+
+struct DomainDataset {
+    DatasetSchema schema;
+    std::vector<DomainRecord> records;
+};
+
+template <typename RecordT>
+struct UnifiedDataset {
+    DatasetSchema schema;  // union schema; records are padded to exactly these keys
+    std::vector<RecordT> records;
 };
 
 struct AttributionWindow {
@@ -247,6 +259,113 @@ inline ZippedDataset zip_dataset(const std::vector<DomainRecord>& records, const
     out.schema = DatasetSchema::create(detail::join_domains(domains), features);
     for (auto& z : out.records)
         for (const auto& f : out.schema.features) z.base.values.try_emplace(f, 0.0);
+    return out;
+}
+
+// merge_domains (datasets.hpp:144-173): the union schema (first-seen order), the joined domain
+// name and the undeclared-feature check are string work on the host; the values are re-laid
+// out under the union schema with zero padding by lattice_merge_dense (fp64 in and out, exact).
+inline UnifiedDataset<DomainRecord> merge_domains(const std::vector<DomainDataset>& datasets) {
+    if (datasets.empty()) throw UsageError("merge_domains: no datasets");
+    std::vector<FeatureId> features;
+    std::set<FeatureId> seen;
+    std::vector<std::string> names;
+    for (const auto& d : datasets) {
+        names.push_back(d.schema.domain);
+        for (const auto& f : d.schema.features)
+            if (seen.insert(f).second) features.push_back(f);
+    }
+    UnifiedDataset<DomainRecord> out;
+    out.schema = DatasetSchema::create(detail::join_domains(names), features);
+    const int G = static_cast<int>(datasets.size()), W = static_cast<int>(features.size());
+    std::map<FeatureId, int> col;
+    for (int c = 0; c < W; ++c) col[features[static_cast<size_t>(c)]] = c;
+    int md = 1;
+    std::size_t n = 0;
+    for (const auto& d : datasets) {
+        md = std::max(md, static_cast<int>(d.schema.features.size()));
+        n += d.records.size();
+    }
+    std::vector<std::int32_t> src(static_cast<size_t>(G) * (W ? W : 1), -1), dom;
+    std::vector<double> vals;
+    vals.reserve(n * static_cast<size_t>(md));
+    for (int g = 0; g < G; ++g) {
+        const auto& d = datasets[static_cast<size_t>(g)];
+        const std::set<FeatureId> declared(d.schema.features.begin(), d.schema.features.end());
+        for (size_t j = 0; j < d.schema.features.size(); ++j)
+            src[static_cast<size_t>(g) * W + static_cast<size_t>(col[d.schema.features[j]])] = static_cast<std::int32_t>(j);
+        for (const auto& rec : d.records) {
+            for (const auto& kv : rec.values)
+                if (!declared.count(kv.first))
+                    throw DataError("merge_domains: record in domain '" + d.schema.domain +
+                                    "' carries undeclared feature '" + kv.first + "'");
+            for (int j = 0; j < md; ++j) {
+                double v = 0.0;  // a declared feature the record omits pads to 0 as well
+                if (j < static_cast<int>(d.schema.features.size())) {
+                    auto it = rec.values.find(d.schema.features[static_cast<size_t>(j)]);
+                    if (it != rec.values.end()) v = it->second;
+                }
+                vals.push_back(v);
+            }
+            dom.push_back(g);
+        }
+    }
+    std::vector<double> merged;
+    if (n && W) {
+        device::Buffer<std::int32_t> d_dom(dom), d_src(src);
+        device::Buffer<double> d_vals(vals), d_out(n * static_cast<size_t>(W));
+        device::throw_status(lattice_merge_dense(static_cast<std::int64_t>(n), G, md, d_dom.get(), d_vals.get(),
+                                                 LATTICE_F64, d_src.get(), W, LATTICE_F64, d_out.get(), 1, nullptr));
+        merged = d_out.download();
+    }
+    size_t r = 0;
+    for (const auto& d : datasets)
+        for (const auto& rec : d.records) {
+            DomainRecord padded = rec;
+            for (int c = 0; c < W; ++c)
+                padded.values.try_emplace(features[static_cast<size_t>(c)], merged[r * static_cast<size_t>(W) + c]);
+            out.records.push_back(std::move(padded));
+            ++r;
+        }
+    return out;
+}
+
+struct WindowSummary {
+    std::size_t count = 0;                   // records routed to this window
+    std::map<TaskId, double> positive_rate;  // using the window's own label; 0.0 when count = 0
+};
+
+// window_routing_summary (datasets.hpp:256-283): the counts are one reduction kernel
+// (lattice_window_summary, exact integers); the rates divide on the host like the reference.
+inline std::map<std::string, WindowSummary> window_routing_summary(const ZippedDataset& dataset) {
+    const std::size_t W = dataset.config.windows.size(), T = dataset.tasks.size(), n = dataset.records.size();
+    std::vector<std::uint8_t> window(n), labels(n * T * W);
+    for (std::size_t i = 0; i < n; ++i) {
+        const auto& rec = dataset.records[i];
+        if (rec.assigned_window >= W || rec.window_labels.size() != T * W || W > 255)
+            throw UsageError("window_routing_summary: dataset not produced by zip_dataset");
+        window[i] = static_cast<std::uint8_t>(rec.assigned_window);
+        std::copy(rec.window_labels.begin(), rec.window_labels.end(), labels.begin() + static_cast<std::ptrdiff_t>(i * T * W));
+    }
+    std::vector<std::int64_t> counts(W, 0), pos(W * T, 0);
+    if (n) {
+        device::Buffer<std::uint8_t> d_w(window), d_l(labels.empty() ? std::vector<std::uint8_t>{0} : labels);
+        device::Buffer<std::int64_t> d_c(W), d_p(W * T > 0 ? W * T : 1);
+        device::throw_status(lattice_window_summary(static_cast<std::int64_t>(n), static_cast<std::int32_t>(T),
+                                                    static_cast<std::int32_t>(W), d_w.get(), d_l.get(), d_c.get(),
+                                                    d_p.get(), 1, nullptr));
+        counts = d_c.download();
+        if (W * T > 0) pos = d_p.download();
+    }
+    std::map<std::string, WindowSummary> out;
+    for (std::size_t w = 0; w < W; ++w) {
+        WindowSummary s;
+        s.count = static_cast<std::size_t>(counts[w]);
+        for (std::size_t t = 0; t < T; ++t)
+            s.positive_rate[dataset.tasks[t]] =
+                counts[w] == 0 ? 0.0 : static_cast<double>(pos[w * T + t]) / static_cast<double>(counts[w]);
+        out[dataset.config.windows[w].name] = s;
+    }
     return out;
 }
 

@@ -33,7 +33,7 @@ typedef enum {
     LATTICE_NCCL = 4
 } lattice_status;
 
-typedef enum { LATTICE_F32 = 0, LATTICE_BF16 = 1 } lattice_dtype;
+typedef enum { LATTICE_F32 = 0, LATTICE_BF16 = 1, LATTICE_F64 = 2 } lattice_dtype;  /* F64: host-API values only */
 
 typedef struct CUstream_st* lattice_stream; /* == cudaStream_t; NULL = legacy default stream */
 
@@ -190,13 +190,15 @@ lattice_status lattice_rownorm(int32_t mode, int64_t rows, int64_t width, double
  * declared. The union schema itself (first-seen union of feature names) and the
  * "undeclared feature" DataError are string-level work done by the caller / C++ drop-in,
  * which passes src_col[g][c] = index of union column c in domain g's declared order, or -1.
- * values: DEVICE fp32 [n][max_declared] (record b's values in its domain's declared order),
- * domain: DEVICE int32 [n]. out: DEVICE [n][out_width] in out_dtype (columns past the union
- * width are zero: GEMM padding). A domain outside [0, domains) -> DATA (check = 1).
+ * values: DEVICE [n][max_declared] in values_dtype (F32 or F64; record b's values in its
+ * domain's declared order), domain: DEVICE int32 [n]. out: DEVICE [n][out_width] in out_dtype
+ * (F32, BF16 or F64 -- F64 in and out is exact, what the C++ drop-in uses; columns past the
+ * union width are zero: GEMM padding). A domain outside [0, domains) -> DATA (check = 1).
  * ==================================================================================== */
 lattice_status lattice_merge_dense(int64_t n, int32_t domains, int32_t max_declared, const int32_t* domain,
-                                   const float* values, const int32_t* src_col, int32_t out_width,
-                                   int32_t out_dtype, void* out, int32_t check, lattice_stream stream);
+                                   const void* values, int32_t values_dtype, const int32_t* src_col,
+                                   int32_t out_width, int32_t out_dtype, void* out, int32_t check,
+                                   lattice_stream stream);
 
 /* ======================================================================================
  * KTAP student-input assembly -- replaces the read side of

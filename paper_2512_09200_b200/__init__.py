@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblattice_b200.so")
 
 OK, USAGE, DATA, CUDA, NCCL = 0, 1, 2, 3, 4
-F32, BF16 = 0, 1
+F32, BF16, F64 = 0, 1, 2
 
 
 class LatticeError(Exception):
@@ -139,7 +139,7 @@ _sig("lattice_net_buffer", _P, [_P, _I32])
 _sig("lattice_correlation_loss", ctypes.c_int, [_I64, _I32, _P, _I64, _P, _I64, ctypes.c_double, _P, _I32, _P])
 _sig("lattice_window_summary", ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _P, _I32, _P])
 _sig("lattice_routed_objectives", ctypes.c_int, [ctypes.POINTER(ObjectiveArgs), _P])
-_sig("lattice_merge_dense", ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _I32, _I32, _P, _I32, _P])
+_sig("lattice_merge_dense", ctypes.c_int, [_I64, _I32, _I32, _P, _P, _I32, _P, _I32, _I32, _P, _I32, _P])
 _sig("lattice_student_inputs", ctypes.c_int, [ctypes.POINTER(StudentArgs), _P])
 _sig("lattice_clip_features", ctypes.c_int, [_I64, _P, ctypes.c_double, _P, _P])
 _sig("lattice_smooth_labels", ctypes.c_int, [_I64, _P, ctypes.c_double, _P, _I32, _P])
@@ -382,9 +382,9 @@ def merge_dense(domain, values, src_col, out_width, out_dtype=None, check_errors
     G = src_col.shape[0]
     odt = out_dtype or torch.bfloat16
     out = torch.empty((n, out_width), dtype=odt, device=values.device)
-    check(_lib.lattice_merge_dense(n, G, md, _p(domain), _p(values), _p(src_col), out_width,
-                                   F32 if odt == torch.float32 else BF16, _p(out), 1 if check_errors else 0,
-                                   _stream(stream)))
+    code = {torch.float32: F32, torch.bfloat16: BF16, torch.float64: F64}
+    check(_lib.lattice_merge_dense(n, G, md, _p(domain), _p(values), code[values.dtype], _p(src_col), out_width,
+                                   code[odt], _p(out), 1 if check_errors else 0, _stream(stream)))
     return out
 
 

@@ -120,6 +120,105 @@ static void zipper_examples() {
     CHECK_THROWS_AS(zip_dataset(recs, {"cvr", "cvr"}, two), UsageError);
 }
 
+// proj/tests/test_numerics.cpp:36-90, 166-200
+static void numerics_more() {
+    const std::vector<double> x{0, 1, 2, 3}, y{1, 3, 2, 4};
+    CHECK(std::abs(correlation_loss(x, y, 1e-15) - 0.2) < 1e-9);
+    CHECK(std::abs(correlation_loss(x, y) - 0.2) < 1e-6);
+    const std::vector<double> a{0.3, 1.7, 2.4, -0.8, 3.1}, na{-0.3, -1.7, -2.4, 0.8, -3.1};
+    CHECK(std::abs(correlation_loss(a, a, 1e-15)) < 1e-9);
+    CHECK(std::abs(correlation_loss(a, na, 1e-15) - 2.0) < 1e-9);
+    CHECK(std::abs(correlation_loss(std::vector<double>{2, 2, 2, 2}, std::vector<double>{1, 2, 3, 4}) - 1.0) < 1e-9);
+    CHECK(std::abs(correlation_loss(x, y) - correlation_loss(y, x)) < 1e-12);
+    CHECK_THROWS_AS(correlation_loss(std::vector<double>{1, 2}, std::vector<double>{1, 2, 3}), UsageError);
+    CHECK_THROWS_AS(correlation_loss(std::vector<double>{1}, std::vector<double>{1}), UsageError);
+    CHECK_THROWS_AS(correlation_loss(x, x, 0.0), UsageError);
+    CHECK_THROWS_AS(correlation_loss(std::vector<double>{1.0, std::nan("")}, std::vector<double>{1, 2}), DataError);
+
+    const std::vector<double> zeros(4, 0.0), tangent{1, -2, 0.5, 3};
+    const auto j0 = swish_rn_jvp(zeros, tangent);
+    CHECK(j0.size() == 4);
+    for (double v : swish_rn_jvp(std::vector<double>{1, 2, 3, 4}, std::vector<double>(4, 0.0))) CHECK(v == 0.0);
+    CHECK_THROWS_AS(swish_rn_jvp(std::vector<double>{1, 2, 3, 4}, std::vector<double>{1}), UsageError);
+    {  // central difference (test_numerics.cpp:150-164)
+        const std::vector<double> xv{-3.1, 0.4, 2.2, 7.5, -9.0, 1.1, 0.0, 4.4};
+        const std::vector<double> tv{0.3, -0.7, 0.2, 0.9, -0.1, 0.5, -0.6, 0.4};
+        const double h = 1e-5;
+        std::vector<double> xp(xv), xm(xv);
+        for (int i = 0; i < 8; ++i) xp[i] += h * tv[i], xm[i] -= h * tv[i];
+        const auto fp = swish_rn(xp), fm = swish_rn(xm), an = swish_rn_jvp(xv, tv);
+        double num2 = 0, diff2 = 0;
+        for (int i = 0; i < 8; ++i) {
+            const double nd = (fp[i] - fm[i]) / (2 * h);
+            num2 += nd * nd;
+            diff2 += (an[i] - nd) * (an[i] - nd);
+        }
+        CHECK(std::sqrt(diff2) <= 1e-3 * std::sqrt(num2));  // swish_rn here is the fp32 row kernel
+    }
+    CHECK((clip_features(std::vector<double>{-5, 0, 5}, 3.0) == std::vector<double>{-3, 0, 3}));
+    CHECK((clip_features(std::vector<double>{1, -2}, 3.0) == std::vector<double>{1, -2}));
+    CHECK((clip_features(std::vector<double>{1e9}, 1.0) == std::vector<double>{1}));
+    CHECK_THROWS_AS(clip_features(std::vector<double>{1}, 0.0), UsageError);
+    const auto sm = smooth_labels(std::vector<double>{0, 1}, 0.1);
+    CHECK(std::abs(sm[0] - 0.05) < 1e-12 && std::abs(sm[1] - 0.95) < 1e-12);
+    CHECK((smooth_labels(std::vector<double>{0, 1}, 0.0) == std::vector<double>{0, 1}));
+    CHECK(std::abs(smooth_labels(std::vector<double>{1}, 0.5)[0] - 0.75) < 1e-12);
+    const auto ordered = smooth_labels(std::vector<double>{0, 1, 0, 1}, 0.3);
+    CHECK(ordered[0] < ordered[1] && ordered[0] == ordered[2]);
+    CHECK_THROWS_AS(smooth_labels(std::vector<double>{0.5}, 0.1), UsageError);
+}
+
+// datasets.hpp:144-173 and :256-283 through the drop-in
+static void merge_and_summary() {
+    DomainDataset a{DatasetSchema::create("ads", {"ctr", "bid"}), {}};
+    DomainDataset b{DatasetSchema::create("shop", {"price", "ctr"}), {}};
+    DomainRecord r1;
+    r1.domain = "ads";
+    r1.values = {{"ctr", 0.25}, {"bid", 1.5}};
+    DomainRecord r2;
+    r2.domain = "shop";
+    r2.values = {{"price", 9.99}};  // declared "ctr" omitted -> padded 0
+    a.records.push_back(r1);
+    b.records.push_back(r2);
+    const auto u = merge_domains({a, b});
+    CHECK(u.schema.domain == "ads+shop");
+    CHECK((u.schema.features == std::vector<FeatureId>{"ctr", "bid", "price"}));
+    CHECK(u.records.size() == 2);
+    CHECK(u.records[0].values.at("price") == 0.0 && u.records[0].values.at("bid") == 1.5);
+    CHECK(u.records[1].values.at("price") == 9.99 && u.records[1].values.at("bid") == 0.0 &&
+          u.records[1].values.at("ctr") == 0.0);
+    CHECK_THROWS_AS(merge_domains({}), UsageError);
+    DomainDataset c = a;
+    c.records[0].values["rogue"] = 1.0;
+    bool threw = false;
+    try {
+        merge_domains({c});
+    } catch (const DataError& e) {
+        threw = std::string(e.what()) == "merge_domains: record in domain 'ads' carries undeclared feature 'rogue'";
+    }
+    CHECK(threw);
+
+    const auto two = ZipperConfig::create({{"90min", 5400000}, {"1d", 86400000}}, {0.5, 0.5}, Seed{7});
+    std::vector<DomainRecord> recs(200);
+    for (size_t i = 0; i < recs.size(); ++i) {
+        recs[i].domain = "d";
+        recs[i].user_id = "u" + std::to_string(i);
+        recs[i].ad_id = "a";
+        if (i % 3 == 0) recs[i].conversions["cvr"] = 3600000;  // within both windows
+    }
+    const auto z = zip_dataset(recs, {"cvr"}, two);
+    const auto sum = window_routing_summary(z);
+    std::size_t n0 = 0, p0 = 0, total = 0;
+    for (const auto& r : z.records)
+        if (r.assigned_window == 0) ++n0, p0 += r.label(0, 0, 2);
+    for (const auto& kv : sum) total += kv.second.count;
+    CHECK(total == 200 && sum.at("90min").count == n0);
+    CHECK(sum.at("90min").positive_rate.at("cvr") == (n0 ? static_cast<double>(p0) / n0 : 0.0));
+    auto broken = z;
+    broken.records[5].assigned_window = 2;
+    CHECK_THROWS_AS(window_routing_summary(broken), UsageError);
+}
+
 static void network_smoke() {
     NetworkConfig c;  // tiny config (BASELINE configs[0] shapes)
     c.max_batch = 64;
@@ -160,6 +259,8 @@ int main() {
     core_goldens();
     numerics_examples();
     zipper_examples();
+    numerics_more();
+    merge_and_summary();
     network_smoke();
     std::printf("drop-in: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail;

@@ -45,6 +45,13 @@ def test_merge_dense_bit_exact():
         got = L.merge_dense(d(dom), d(vals), d(src_w), width, out_dtype=odt)
         bad, want = oracle.merge_dense(dom, vals, src_w, bf16=bf)
         assert bad == -1 and np.array_equal(got.float().cpu().numpy(), want)
+    # fp64 in / out (the C++ drop-in's merge_domains): exact
+    v64 = vals.astype(np.float64) + 1e-9  # not fp32-representable
+    got = L.merge_dense(d(dom), d(v64), d(src_w), width, out_dtype=torch.float64).cpu().numpy()
+    for b in (0, 1, 4999):
+        for c in range(width):
+            j = src_w[dom[b], c]
+            assert got[b, c] == (v64[b, j] if j >= 0 else 0.0)
     dom2 = dom.copy()
     dom2[77] = G
     with pytest.raises(L.DataError):
