@@ -22,6 +22,8 @@ struct NetworkConfig {
     std::int64_t max_batch = 512;
     Seed weight_seed{0x1A79};
     lattice_dtype dtype = LATTICE_F32;  // configs[0] is fp32 (TF32 tensor cores); bf16 otherwise
+    // dense processor: the last dense_features of the n embeddings; 0 = none
+    int dense_features = 0, dense_in = 0, dense_hidden = 0;
 };
 
 // Jagged sparse batch, feature-major CSR: bag (f, b) = ids[offsets[f*B+b] .. offsets[f*B+b+1]).
@@ -59,6 +61,9 @@ public:
         nc.max_batch = c.max_batch;
         nc.weight_seed = c.weight_seed.value;
         nc.dtype = c.dtype;
+        nc.dense_features = c.dense_features;
+        nc.dense_in = c.dense_in;
+        nc.dense_hidden = c.dense_hidden;
         device::throw_status(lattice_net_create(&nc, &net_));
     }
     Network(const Network&) = delete;
@@ -69,10 +74,13 @@ public:
 
     // Logits [B][heads] in batch order, heads = objectives x attribution windows.
     std::vector<float> forward(const SparseBatch& b, const TableSet& t) const {
+        const int sparse = cfg_.n - cfg_.dense_features;
         if (b.domain.size() != static_cast<std::size_t>(b.batch) ||
-            b.offsets.size() != static_cast<std::size_t>(cfg_.n * b.batch + 1))
+            b.offsets.size() != static_cast<std::size_t>(sparse * b.batch + 1))
             throw UsageError("Network::forward: batch arrays do not match batch size");
-        if (t.tables.size() != static_cast<std::size_t>(cfg_.n) || t.rows.size() != t.tables.size())
+        if (cfg_.dense_features > 0)
+            throw UsageError("Network::forward: a network with dense features needs forward_device with batch.dense");
+        if (t.tables.size() != static_cast<std::size_t>(sparse) || t.rows.size() != t.tables.size())
             throw UsageError("Network::forward: need one table per sparse feature");
         device::Buffer<std::int64_t> d_off(b.offsets), d_rows(t.rows);
         device::Buffer<std::int32_t> d_ids(b.ids.empty() ? std::vector<std::int32_t>{0} : b.ids);

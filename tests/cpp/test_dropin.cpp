@@ -146,14 +146,22 @@ static void numerics_more() {
         const double h = 1e-5;
         std::vector<double> xp(xv), xm(xv);
         for (int i = 0; i < 8; ++i) xp[i] += h * tv[i], xm[i] -= h * tv[i];
-        const auto fp = swish_rn(xp), fm = swish_rn(xm), an = swish_rn_jvp(xv, tv);
+        auto swish64 = [](const std::vector<double>& v) {  // numerics.hpp:94 in fp64 (test-side)
+            double ss = 0;
+            for (double e : v) ss += e * e;
+            const double den = std::sqrt(ss / v.size() + 1e-6);
+            std::vector<double> o(v.size());
+            for (size_t i = 0; i < v.size(); ++i) o[i] = (v[i] / den) / (1.0 + std::exp(-v[i] / den));
+            return o;
+        };
+        const auto fp = swish64(xp), fm = swish64(xm), an = swish_rn_jvp(xv, tv);
         double num2 = 0, diff2 = 0;
         for (int i = 0; i < 8; ++i) {
             const double nd = (fp[i] - fm[i]) / (2 * h);
             num2 += nd * nd;
             diff2 += (an[i] - nd) * (an[i] - nd);
         }
-        CHECK(std::sqrt(diff2) <= 1e-3 * std::sqrt(num2));  // swish_rn here is the fp32 row kernel
+        CHECK(std::sqrt(diff2) <= 1e-4 * std::sqrt(num2));  // test_numerics.cpp:161
     }
     CHECK((clip_features(std::vector<double>{-5, 0, 5}, 3.0) == std::vector<double>{-3, 0, 3}));
     CHECK((clip_features(std::vector<double>{1, -2}, 3.0) == std::vector<double>{1, -2}));

@@ -26,3 +26,15 @@ def test_sharded_forward_bit_identical_to_single_gpu():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "bit-identical to the single-GPU path on every rank: True" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
+def test_cpp_sharded_network_bit_identical():
+    """lattice::ShardedNetwork (C++ host over the C ABI, CUDA IPC + peer barriers) across
+    processes: tests/cpp/test_sharded.cpp."""
+    n = min(_gpus(), 4)
+    r = subprocess.run([os.path.join(ROOT, "tests", "cpp", "test_sharded"), str(n)], capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("bit-identical to") == n
