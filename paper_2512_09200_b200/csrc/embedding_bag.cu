@@ -580,12 +580,25 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
 }  // namespace staged
 
 
+// Blocks per SM of the persistent bag grid: occupancy by default; LATTICE_BAG_BLOCKS_PER_SM caps
+// it (1 leaves room for a co-running GEMM / FM CTA on every SM when the embedding stage of the
+// next batch overlaps the dense stage of this one).
+int bag_blocks_cap() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("LATTICE_BAG_BLOCKS_PER_SM");
+        v = e ? std::atoi(e) : 0;
+    }
+    return v;
+}
+
 template <typename K>
 unsigned persistent_grid(K kernel, int64_t bags) {
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBagWarps * 32, 0) != cudaSuccess ||
         per_sm < 1)
         per_sm = 4;
+    if (bag_blocks_cap() > 0 && per_sm > bag_blocks_cap()) per_sm = bag_blocks_cap();
     const int64_t want = (bags + kBagWarps - 1) / kBagWarps;
     const int64_t cap = (int64_t)num_sms() * per_sm;
     return (unsigned)(want < cap ? want : cap);

@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             // X'[nF+row] = rms_norm_d(L[row] + X[nF+row]): two passes over TMEM (sum of squares,
             // then normalise + store) so only the packed residual stays live in registers
-            float ss = 0.0f;
+            float ss8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent FMA chains
 #pragma unroll
             for (int c = 0; c < 128; c += 32) {
                 if (c < d) {
@@ -308,11 +308,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int i = 0; i < 8; ++i) {
                             const float a = v[j + i] + r8[i];
-                            ss += a * a;
+                            ss8[i] = fmaf(a, a, ss8[i]);
                         }
                     }
                 }
             }
+            const float ss = ((ss8[0] + ss8[1]) + (ss8[2] + ss8[3])) + ((ss8[4] + ss8[5]) + (ss8[6] + ss8[7]));
             const float inv = 1.0f / sqrtf(ss * inv_d + 1e-6f);
             T* dst = static_cast<T*>(p.Xout) + (b * p.n + xr) * (int64_t)d;
 #pragma unroll
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::fence_after();
             tc::mbar_arrive(&x_empty[st]);  // every MMA reading this X stage has completed
             float v[2][64];
-            float ss = 0.0f;
+            float ss4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent FMA chains
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) {
                 if (mt < m_tiles) {
@@ -358,10 +359,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (mt * 128 + row < p.n) {
 #pragma unroll
                         for (int j = 0; j < 64; ++j)
-                            if (j < p.k) ss += v[mt][j] * v[mt][j];
+                            if (j < p.k) ss4[j & 3] = fmaf(v[mt][j], v[mt][j], ss4[j & 3]);
                     }
                 }
             }
+            float ss = (ss4[0] + ss4[1]) + (ss4[2] + ss4[3]);
             tc::fence_before();
             tc::mbar_arrive(&tmem_empty[rg]);
             ss = warp_sum(ss);
