@@ -43,6 +43,7 @@ struct BagParams {
     // offsets / ids / sample_pos from that source's HBM over NVLink and writing the pooled row
     // straight into the source's X0. Bags are numbered [f][r][b] so one table stays hot in L2
     // across all sources.
+    uint32_t mB, sB, mF, sF;  // fast division by B and F (magic multiplier, shift), see fastdiv()
     int32_t peer_mode;
     const int64_t* const* p_off;  // [R] source CSR offsets over F_src features
     const int32_t* const* p_ids;  // [R]
@@ -66,6 +67,22 @@ __device__ __forceinline__ uint4 ld_row_keep(const void* p, uint64_t pol) {
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p), "l"(pol));
     return r;
+}
+// x / d for x < 2^31 as one wide multiply and a shift: m = floor(2^(31+l) / d) + 1 with
+// l = ceil(log2 d) keeps the error of x*m / 2^(31+l) below 1/d, so the floor is exact.
+inline void fastdiv(uint32_t d, uint32_t* m, uint32_t* s) {
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    *m = (uint32_t)(((1ull << (31 + l)) / d) + 1);
+    *s = 31 + l;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, uint32_t m, uint32_t s) {
+    return (uint32_t)(((uint64_t)x * m) >> s);
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t pol;
@@ -166,8 +183,8 @@ __device__ __forceinline__ void decode(const BagParams& p, uint32_t bag, int& f,
         f = (int)(fr / R);
         b = bag - fr * B;
     } else {
-        const uint32_t rf = bag / B;
-        r = (int)(rf / F);
+        const uint32_t rf = fdiv(bag, p.mB, p.sB);
+        r = (int)fdiv(rf, p.mF, p.sF);
         f = (int)(rf - (uint32_t)r * F);
         b = bag - rf * B;
     }
@@ -222,10 +239,13 @@ __device__ __forceinline__ uint32_t claim_chunk(unsigned long long* counter, int
 
 // N passes of RPP rows each: every lane issues N*CPL 16-byte row loads back to back, then
 // accumulates them. MASK: rows at or past `cnt` read the zero row instead (bag tail).
-template <typename TT, int LPR, int CPL, int N, bool MASK, bool PEER>
+// CHECK = false: the caller verified that every id of this 32-id window is in range, so rows
+// are addressed without a per-row bound check (the common case); MASK rows past `cnt` still
+// read the zero row.
+template <typename TT, int LPR, int CPL, int N, bool MASK, bool CHECK, bool PEER>
 __device__ __forceinline__ void gather_step(const BagParams& p, uint32_t bag, const int32_t* idp, int base,
                                             const TT* __restrict__ table, uint32_t rows, int my_id, int j,
-                                            int cnt, int sub, int cl, bool keep, uint64_t pol, float* acc) {
+                                            int cnt, int sub, int cl, uint64_t pol, float* acc) {
     constexpr int EPC = Elem<TT>::kPerChunk;
     constexpr int RPP = 32 / LPR;
     uint4 v[N][CPL];
@@ -233,18 +253,17 @@ __device__ __forceinline__ void gather_step(const BagParams& p, uint32_t bag, co
     for (int u = 0; u < N; ++u) {
         const int jj = j + u * RPP + sub;
         const int id = __shfl_sync(0xffffffffu, my_id, jj & 31);
-        bool ok = (uint32_t)id < rows;
-        if (MASK) {
-            const bool live = jj < cnt;
+        bool ok = true;
+        if (CHECK) {
+            ok = (uint32_t)id < rows;
+            const bool live = !MASK || jj < cnt;
             if (live && !ok) atomicMin(p.err, id_position<PEER>(p, bag, idp + base + jj));
-            ok = ok && live;
-        } else if (!ok) {
-            atomicMin(p.err, id_position<PEER>(p, bag, idp + base + jj));
         }
-        const TT* row = ok ? table + (size_t)(uint32_t)id * p.D : reinterpret_cast<const TT*>(g_zero_row);
+        if (MASK) ok = ok && jj < cnt;
+        const TT* row = (!CHECK && !MASK) || ok ? table + (size_t)(uint32_t)id * p.D
+                                                : reinterpret_cast<const TT*>(g_zero_row);
 #pragma unroll
-        for (int c = 0; c < CPL; ++c)
-            v[u][c] = keep ? ld_row_keep(row + (c * LPR + cl) * EPC, pol) : ld_stream(row + (c * LPR + cl) * EPC);
+        for (int c = 0; c < CPL; ++c) v[u][c] = ld_row_keep(row + (c * LPR + cl) * EPC, pol);
     }
 #pragma unroll
     for (int u = 0; u < N; ++u)
@@ -263,9 +282,8 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
     if (bag >= total) return;
     uint32_t chunk_end = bag + kChunk < total ? bag + kChunk : total;
     const int sub = lane / LPR, cl = lane % LPR;
-    const bool keep = (p.l2keep & 1) != 0;
     const bool ef = (p.l2keep & 2) != 0;
-    const uint64_t pol = policy_evict_last();
+    const uint64_t pol = (p.l2keep & 1) ? policy_evict_last() : policy_evict_normal();  // table rows
     const uint64_t pol_ef = policy_evict_first();
     const int32_t* idp;
     int len;
@@ -302,12 +320,21 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
             const int cnt = len - base < 32 ? len - base : 32;
             const int my_id = base == 0 ? first_id : (lane < cnt ? __ldg(idp + base + lane) : 0);
             int j = 0;
-            for (; j + RPP * U <= cnt; j += RPP * U)
-                gather_step<TT, LPR, CPL, U, false, PEER>(p, bag, idp, base, table, rows, my_id, j, cnt, sub, cl,
-                                                          keep, pol, acc);
-            for (; j < cnt; j += RPP * UT)
-                gather_step<TT, LPR, CPL, UT, true, PEER>(p, bag, idp, base, table, rows, my_id, j, cnt, sub, cl,
-                                                          keep, pol, acc);
+            if (__all_sync(0xffffffffu, lane >= cnt || (uint32_t)my_id < rows)) {  // all ids in range
+                for (; j + RPP * U <= cnt; j += RPP * U)
+                    gather_step<TT, LPR, CPL, U, false, false, PEER>(p, bag, idp, base, table, rows, my_id, j, cnt,
+                                                                     sub, cl, pol, acc);
+                for (; j < cnt; j += RPP * UT)
+                    gather_step<TT, LPR, CPL, UT, true, false, PEER>(p, bag, idp, base, table, rows, my_id, j, cnt,
+                                                                     sub, cl, pol, acc);
+            } else {  // some id out of range: checked path (zero contribution + first-offender error)
+                for (; j + RPP * U <= cnt; j += RPP * U)
+                    gather_step<TT, LPR, CPL, U, false, true, PEER>(p, bag, idp, base, table, rows, my_id, j, cnt,
+                                                                    sub, cl, pol, acc);
+                for (; j < cnt; j += RPP * UT)
+                    gather_step<TT, LPR, CPL, UT, true, true, PEER>(p, bag, idp, base, table, rows, my_id, j, cnt,
+                                                                    sub, cl, pol, acc);
+            }
         }
         // next bag's first ids (its offsets were requested before this bag's rows)
         const int next_id = (nbag < total && lane < nlen) ? __ldg(nidp + lane) : 0;
@@ -323,7 +350,7 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
             for (int i = 0; i < CPL * EPC; ++i) ss += acc[i] * acc[i];
 #pragma unroll
             for (int o = 1; o < LPR; o <<= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-            const float inv = 1.0f / sqrtf(ss / (float)p.D + 1e-6f);
+            const float inv = rsqrtf(ss / (float)p.D + 1e-6f);  // MUFU.RSQ (~2 ulp; the row is then rounded to bf16)
 #pragma unroll
             for (int i = 0; i < CPL * EPC; ++i) acc[i] *= inv;
         }
@@ -463,10 +490,10 @@ __device__ __noinline__ unsigned long long id_position(const BagParams& p, int r
 // N passes of RPP rows each: every lane issues N*CPL 16-byte row loads back to back, then
 // accumulates them. Ids come from the stage (q < kIdsCap) or global. MASK: rows at or past
 // `len` read the zero row instead (bag tail).
-template <typename TT, int LPR, int CPL, int N, bool MASK, bool PEER>
+template <typename TT, int LPR, int CPL, int N, bool MASK, bool CHECK, bool PEER>
 __device__ __forceinline__ void gather_step(const BagParams& p, const Stage& S, int sk, int j, int len,
                                             const TT* __restrict__ table, uint32_t rows, int sub, int cl,
-                                            bool keep, uint64_t pol, float* acc) {
+                                            uint64_t pol, float* acc) {
     constexpr int EPC = Elem<TT>::kPerChunk;
     constexpr int RPP = 32 / LPR;
     uint4 v[N][CPL];
@@ -477,13 +504,17 @@ __device__ __forceinline__ void gather_step(const BagParams& p, const Stage& S, 
         const bool live = !MASK || jj < len;
         int id = 0;
         if (live) id = q < kIdsCap ? S.ids[q] : __ldg(S.idg + q);
-        bool ok = (uint32_t)id < rows;
-        if (live && !ok) atomicMin(p.err, id_position<PEER>(p, S.r, S.idg + q));
+        bool ok = true;
+        if (CHECK) {
+            ok = (uint32_t)id < rows;
+            if (live && !ok) atomicMin(p.err, id_position<PEER>(p, S.r, S.idg + q));
+        }
         ok = ok && live;
-        const TT* row = ok ? table + (size_t)(uint32_t)id * p.D : reinterpret_cast<const TT*>(g_zero_row);
+        const TT* row = (!CHECK && !MASK) || ok ? table + (size_t)(uint32_t)id * p.D
+                                                : reinterpret_cast<const TT*>(g_zero_row);
 #pragma unroll
         for (int c = 0; c < CPL; ++c)
-            v[u][c] = keep ? ld_row_keep(row + (c * LPR + cl) * EPC, pol) : ld_stream(row + (c * LPR + cl) * EPC);
+            v[u][c] = ld_row_keep(row + (c * LPR + cl) * EPC, pol);
     }
 #pragma unroll
     for (int u = 0; u < N; ++u)
@@ -493,7 +524,7 @@ __device__ __forceinline__ void gather_step(const BagParams& p, const Stage& S, 
 
 // Pool, normalise and store the bags of the staged chunk S.
 template <typename TT, typename OT, int LPR, int CPL, int U, bool PEER>
-__device__ __forceinline__ void pool_chunk(const BagParams& p, const Stage& S, int lane, bool keep, uint64_t pol) {
+__device__ __forceinline__ void pool_chunk(const BagParams& p, const Stage& S, int lane, uint64_t pol) {
     constexpr int EPC = Elem<TT>::kPerChunk;
     constexpr int RPP = 32 / LPR;           // rows per pass
     constexpr int UT = U >= 4 ? U / 2 : U;  // passes per masked tail step
@@ -510,10 +541,22 @@ __device__ __forceinline__ void pool_chunk(const BagParams& p, const Stage& S, i
 #pragma unroll
         for (int i = 0; i < CPL * EPC; ++i) acc[i] = 0.0f;
         int j = 0;
-        for (; j + RPP * U <= len; j += RPP * U)
-            gather_step<TT, LPR, CPL, U, false, PEER>(p, S, sk, j, len, table, rows, sub, cl, keep, pol, acc);
-        for (; j < len; j += RPP * UT)
-            gather_step<TT, LPR, CPL, UT, true, PEER>(p, S, sk, j, len, table, rows, sub, cl, keep, pol, acc);
+        bool in_range = true;  // every id of the bag valid: gather without per-row checks
+        for (int q = lane; q < len; q += 32) {
+            const int id = sk + q < kIdsCap ? S.ids[sk + q] : __ldg(S.idg + sk + q);
+            in_range &= (uint32_t)id < rows;
+        }
+        if (__all_sync(0xffffffffu, in_range)) {
+            for (; j + RPP * U <= len; j += RPP * U)
+                gather_step<TT, LPR, CPL, U, false, false, PEER>(p, S, sk, j, len, table, rows, sub, cl, pol, acc);
+            for (; j < len; j += RPP * UT)
+                gather_step<TT, LPR, CPL, UT, true, false, PEER>(p, S, sk, j, len, table, rows, sub, cl, pol, acc);
+        } else {
+            for (; j + RPP * U <= len; j += RPP * U)
+                gather_step<TT, LPR, CPL, U, false, true, PEER>(p, S, sk, j, len, table, rows, sub, cl, pol, acc);
+            for (; j < len; j += RPP * UT)
+                gather_step<TT, LPR, CPL, UT, true, true, PEER>(p, S, sk, j, len, table, rows, sub, cl, pol, acc);
+        }
         // fold the RPP row groups: lanes with equal cl end up with the full sum
 #pragma unroll
         for (int o = LPR; o < 32; o <<= 1)
@@ -525,7 +568,7 @@ __device__ __forceinline__ void pool_chunk(const BagParams& p, const Stage& S, i
             for (int i = 0; i < CPL * EPC; ++i) ss += acc[i] * acc[i];
 #pragma unroll
             for (int o = 1; o < LPR; o <<= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-            const float inv = 1.0f / sqrtf(ss / (float)p.D + 1e-6f);
+            const float inv = rsqrtf(ss / (float)p.D + 1e-6f);
 #pragma unroll
             for (int i = 0; i < CPL * EPC; ++i) acc[i] *= inv;
         }
@@ -544,8 +587,7 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
     Stage* stg = stages[threadIdx.x >> 5];
     const uint32_t cps = (uint32_t)((p.B + kChunk - 1) / kChunk);
     const uint32_t total = (uint32_t)p.R * (uint32_t)p.F * cps;
-    const bool keep = (p.l2keep & 1) != 0;
-    const uint64_t pol = policy_evict_last();
+    const uint64_t pol = (p.l2keep & 1) ? policy_evict_last() : policy_evict_normal();
 
     uint32_t c = claim_chunk(p.counter, lane);
     if (c >= total) return;
@@ -565,7 +607,7 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
         // claim the chunk after next and start its offsets
         const uint32_t cnn = cn < total ? claim_chunk(p.counter, lane) : total;
         const int64_t onn = cnn < total ? chunk_offsets<PEER>(p, cnn, cps, lane) : 0;
-        pool_chunk<TT, OT, LPR, CPL, U, PEER>(p, stg[s], lane, keep, pol);
+        pool_chunk<TT, OT, LPR, CPL, U, PEER>(p, stg[s], lane, pol);
         __syncwarp();  // stage s is refilled next iteration
         if (cn >= total) break;
         cn = cnn;
@@ -910,7 +952,9 @@ lattice_status lattice_embedding_bag(const lattice_bag_args* a, lattice_stream s
     BagParams p{a->features, a->batch, a->dim, a->tables, a->rows, a->offsets, a->ids, a->out,
                 a->out_row_stride, a->out_feature_offset, a->sample_pos, a->normalize, err,
                 a->sources > 1 ? a->sources : 1, a->slice_cap > 0 ? a->slice_cap : 0, err + 1,
-                bag_l2keep(), 0, nullptr, nullptr, nullptr, nullptr, 0};
+                bag_l2keep(), 0, 0, 0, 0, 0, nullptr, nullptr, nullptr, nullptr, 0};
+    fastdiv((uint32_t)p.B, &p.mB, &p.sB);
+    fastdiv((uint32_t)p.F, &p.mF, &p.sF);
     lattice_status st;
     if (a->table_dtype == LATTICE_F32)
         st = a->out_dtype == LATTICE_F32 ? launch_bag<float, float>(p, row_bytes, stream)
@@ -968,7 +1012,9 @@ lattice_status lattice_peer_embedding_bag(const lattice_peer_bag_args* a, lattic
     LAT_CUDA(cudaMemsetAsync(err + 1, 0, sizeof(*err), stream));
     BagParams p{a->features_local, a->batch, a->dim, a->tables, a->rows, nullptr, nullptr, nullptr,
                 a->out_row_stride, a->feature_base, nullptr, a->normalize, err, a->world, 0, err + 1,
-                bag_l2keep(), 1, a->offsets, a->ids, a->sample_pos, a->out, a->feature_base};
+                bag_l2keep(), 0, 0, 0, 0, 1, a->offsets, a->ids, a->sample_pos, a->out, a->feature_base};
+    fastdiv((uint32_t)p.B, &p.mB, &p.sB);
+    fastdiv((uint32_t)p.F, &p.mF, &p.sF);
     lattice_status st;
     if (a->table_dtype == LATTICE_F32)
         st = a->out_dtype == LATTICE_F32 ? launch_bag<float, float>(p, row_bytes, stream)
