@@ -34,9 +34,15 @@
 namespace lat {
 namespace fm {
 
+// large variant: 4 LCB + 4 FM epilogue warps
 constexpr int kEpiWarps = 8;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kThreads = 64 + kEpiThreads;
+// resident variant: 8 LCB warps (a warp pair per TMEM lane quarter, half of the d columns
+// each) + 4 FM warps, so the latency-bound LCB epilogue has two warps per sub-partition
+constexpr int kLcbWarps = 8;
+constexpr int kResEpiThreads = (kLcbWarps + 4) * 32;
+constexpr int kResThreads = 64 + kResEpiThreads;
 
 // byte offset of element (row, col) inside a [rows][128 B] SW128 panel, element size ES
 template <int ES>
@@ -110,9 +116,9 @@ struct Geo {
     }
 };
 
-// 10 warps: some SM sub-partitions hold 3 of them, so 168 registers is the ceiling
+// 14 warps: 146 registers per thread is the ceiling
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kResThreads, 1)
     fm_lcb_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWL,
                   const __grid_constant__ CUtensorMap tmYT, const Params p) {
     using Op = tc::Operand<T>;
@@ -141,6 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
     uint64_t* xt_full = bars + 13;  // fp32: X^T copy written (LCB group)
     float* red_f = reinterpret_cast<float*>(bars + 16);  // [2][4] FM-group warp partials
+    float* lcb_ss = reinterpret_cast<float*>(bars + 20);  // [2 parity][2 halves][128 rows] LCB partials
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rcols = region_cols(p);
@@ -152,14 +159,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tma_prefetch(&tmYT);
         for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&x_full[i], 1);
-            tc::mbar_init(&x_empty[i], kEpiThreads);
+            tc::mbar_init(&x_empty[i], kResEpiThreads);
             tc::mbar_init(&pl_full[i], 1);
             tc::mbar_init(&f_full[i], 1);
-            tc::mbar_init(&tmem_empty[i], kEpiThreads);
+            tc::mbar_init(&tmem_empty[i], kResEpiThreads);
         }
         tc::mbar_init(w_full, 1);
-        tc::mbar_init(pbuf_full, 128);  // the LCB group
-        tc::mbar_init(xt_full, 128);    // the LCB group (fp32 only)
+        tc::mbar_init(pbuf_full, kLcbWarps * 32);  // the LCB group
+        tc::mbar_init(xt_full, kLcbWarps * 32);    // the LCB group (fp32 only)
         tc::fence_mbar_init();
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, tcols);
@@ -234,14 +241,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::mma_commit(&f_full[rg]);
             }
         }
-    } else if (warp < 6) {  // ---- LCB group, warps 2..5: thread = TMEM lane
+    } else if (warp < 2 + kLcbWarps) {  // ---- LCB group, warps 2..9: thread = TMEM lane
+        // warps w and w+4 share TMEM lane quarter q; warp half h owns d columns [h*d/2, (h+1)*d/2)
         const int q = warp & 3;
+        const int h = (warp - 2) >> 2;
         const int row = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const float inv_d = 1.0f / (float)d;
         const int xr = p.nF + row;
         const bool live = row < p.nL;
-        const int res_vec = d * ES / 16;  // 16-byte vectors in one residual row (<= 16)
+        const int hd = d / 2, c_lo = h * hd;
+        const int res_vec = hd * ES / 16;  // 16-byte vectors in one half residual row (<= 8)
         int it = 0;
         for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
             const int st = it & 1;
@@ -249,13 +259,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t rph = nreg == 2 ? ((it >> 1) & 1) : (it & 1);
             const uint32_t t_L = tmem + rg * 256 + lane_off + 64;
             const uint8_t* xs = sX + st * g.xstage;
-            // pick up the residual row X[nF+row] as soon as the stage lands, so the stage can
-            // be recycled right after the MMAs (the producer runs two samples ahead)
+            // pick up this half of the residual row X[nF+row] as soon as the stage lands, so
+            // the stage can be recycled right after the MMAs (the producer runs two samples ahead)
             tc::mbar_wait(&x_full[st], (it >> 1) & 1);
-            uint4 res[16];
+            uint4 res[8];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int e = j * (16 / ES);  // first element of vector j
+            for (int j = 0; j < 8; ++j) {
+                const int e = c_lo + j * (16 / ES);  // first element of vector j
                 res[j] = (live && j < res_vec)
                              ? *reinterpret_cast<const uint4*>(xs + (e / EP) * g.xpanel + swz<ES>(xr, e % EP))
                              : make_uint4(0, 0, 0, 0);
@@ -264,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // fp32: X^T[c][i] = X[i][c] into the K-major copy (its previous contents were
                 // consumed by the previous sample's P/L MMAs, whose pl_full this thread saw)
                 const int total = d * npad;
-                for (int idx = row; idx < total; idx += 128) {
+                for (int idx = h * 128 + row; idx < total; idx += kLcbWarps * 32) {
                     const int c = idx / npad, i = idx - c * npad;
                     const float x = *reinterpret_cast<const float*>(xs + (c / EP) * g.xpanel + swz<ES>(i, c % EP));
                     *reinterpret_cast<float*>(sXT + (i / EP) * 16384 + swz<ES>(c, i % EP)) = x;
@@ -276,11 +286,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_wait(&pl_full[rg], rph);
             tc::fence_after();
             // P row `row` (= d index, same TMEM lane as this thread's L row) -> storage dtype ->
-            // Pbuf[j][row], the K-major B operand of F. One Pbuf suffices: pl_full of this
-            // sample completes after the previous sample's F MMAs (same issuing thread).
+            // Pbuf[j][row], the K-major B operand of F; the two halves stage alternate 16-column
+            // chunks. One Pbuf suffices: pl_full of this sample completes after the previous
+            // sample's F MMAs (same issuing thread).
             {
                 const uint32_t t_P = tmem + rg * 256 + lane_off;
-                for (int c0 = 0; c0 < kpad; c0 += 16) {
+                for (int c0 = 16 * h; c0 < kpad; c0 += 32) {
                     float pv[16];
                     tc::tmem_ld16(t_P + c0, pv);
                     if (row < d) {
@@ -293,14 +304,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::fence_async_shared();
                 tc::mbar_arrive(pbuf_full);
             }
-            // X'[nF+row] = rms_norm_d(L[row] + X[nF+row]): two passes over TMEM (sum of squares,
-            // then normalise + store) so only the packed residual stays live in registers
+            // X'[nF+row] = rms_norm_d(L[row] + X[nF+row]): two passes over this half's TMEM
+            // columns (sum of squares, then normalise + store); the two halves' sums of squares
+            // meet in shared memory (parity-buffered by sample) behind one 256-thread barrier
             float ss8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent FMA chains
 #pragma unroll
-            for (int c = 0; c < 128; c += 32) {
-                if (c < d) {
+            for (int c = 0; c < 64; c += 32) {
+                if (c < hd) {
                     float v[32];
-                    tc::tmem_ld32(t_L + c, v);
+                    tc::tmem_ld32(t_L + c_lo + c, v);
 #pragma unroll
                     for (int j = 0; j < 32; j += 8) {
                         float r8[8];
@@ -313,14 +325,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            const float ss = ((ss8[0] + ss8[1]) + (ss8[2] + ss8[3])) + ((ss8[4] + ss8[5]) + (ss8[6] + ss8[7]));
+            float* xss = lcb_ss + (it & 1) * 256;
+            xss[h * 128 + row] = ((ss8[0] + ss8[1]) + (ss8[2] + ss8[3])) + ((ss8[4] + ss8[5]) + (ss8[6] + ss8[7]));
+            tc::named_bar(3, kLcbWarps * 32);
+            const float ss = xss[row] + xss[128 + row];  // same order in both halves
             const float inv = 1.0f / sqrtf(ss * inv_d + 1e-6f);
-            T* dst = static_cast<T*>(p.Xout) + (b * p.n + xr) * (int64_t)d;
+            T* dst = static_cast<T*>(p.Xout) + (b * p.n + xr) * (int64_t)d + c_lo;
 #pragma unroll
-            for (int c = 0; c < 128; c += 32) {
-                if (c < d) {
+            for (int c = 0; c < 64; c += 32) {
+                if (c < hd) {
                     float v[32];
-                    tc::tmem_ld32(t_L + c, v);
+                    tc::tmem_ld32(t_L + c_lo + c, v);
 #pragma unroll
                     for (int j = 0; j < 32; j += 8) {
                         float r8[8];
@@ -334,9 +349,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::fence_before();
             tc::mbar_arrive(&tmem_empty[rg]);
         }
-    } else {  // ---- FM group, warps 6..9: Fin = rms_norm(flatten(X P))
+    } else {  // ---- FM group, warps 10..13: Fin = rms_norm(flatten(X P))
         const int q = warp & 3;
-        const int e = warp - 6;
+        const int e = warp - 2 - kLcbWarps;
         const int row = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const float inv_nk = 1.0f / (float)(p.n * p.k);
@@ -349,23 +364,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_wait(&f_full[rg], rph);
             tc::fence_after();
             tc::mbar_arrive(&x_empty[st]);  // every MMA reading this X stage has completed
-            float v[2][64];
+            // k <= 32: the F rows stay in registers and the region is released before the
+            // stores; k in (32, 64]: the second pass re-reads TMEM (register budget), so the
+            // region is released after it
+            const bool small_k = kpad <= 32;
+            float v[2][32];
             float ss4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent FMA chains
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) {
                 if (mt < m_tiles) {
-                    tc::tmem_ld32(t_F + mt * kpad, v[mt]);
-                    if (kpad > 32) tc::tmem_ld32(t_F + mt * kpad + 32, v[mt] + 32);
-                    if (mt * 128 + row < p.n) {
+                    for (int c0 = 0; c0 < kpad; c0 += 32) {
+                        tc::tmem_ld32(t_F + mt * kpad + c0, v[mt]);
+                        if (mt * 128 + row < p.n) {
 #pragma unroll
-                        for (int j = 0; j < 64; ++j)
-                            if (j < p.k) ss4[j & 3] = fmaf(v[mt][j], v[mt][j], ss4[j & 3]);
+                            for (int j = 0; j < 32; ++j)
+                                if (c0 + j < p.k) ss4[j & 3] = fmaf(v[mt][j], v[mt][j], ss4[j & 3]);
+                        }
                     }
                 }
             }
             float ss = (ss4[0] + ss4[1]) + (ss4[2] + ss4[3]);
-            tc::fence_before();
-            tc::mbar_arrive(&tmem_empty[rg]);
+            if (small_k) {
+                tc::fence_before();
+                tc::mbar_arrive(&tmem_empty[rg]);
+            }
             ss = warp_sum(ss);
             float* red = red_f + (it & 1) * 4;  // parity-buffered: no reuse race across samples
             if (lane == 0) red[e] = ss;
@@ -374,24 +396,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) {
                 const int r = mt * 128 + row;
-                if (mt < m_tiles && r < p.n) {
-                    T* dst = static_cast<T*>(p.Fout) + b * (int64_t)p.n * p.k + (int64_t)r * p.k;
-                    if ((p.k & 7) == 0) {
+                if (mt < m_tiles) {
+                    for (int c0 = 0; c0 < kpad; c0 += 32) {
+                        if (!small_k) tc::tmem_ld32(t_F + mt * kpad + c0, v[mt]);
+                        if (r >= p.n) continue;
+                        T* dst = static_cast<T*>(p.Fout) + b * (int64_t)p.n * p.k + (int64_t)r * p.k + c0;
+                        if ((p.k & 7) == 0) {
 #pragma unroll
-                        for (int j = 0; j < 64; j += 8) {
-                            if (j < p.k) {
-                                float o[8];
+                            for (int j = 0; j < 32; j += 8) {
+                                if (c0 + j < p.k) {
+                                    float o[8];
 #pragma unroll
-                                for (int i = 0; i < 8; ++i) o[i] = v[mt][j + i] * inv;
-                                Store<T>::row8(dst + j, o);
+                                    for (int i = 0; i < 8; ++i) o[i] = v[mt][j + i] * inv;
+                                    Store<T>::row8(dst + j, o);
+                                }
                             }
-                        }
-                    } else {
+                        } else {
 #pragma unroll
-                        for (int j = 0; j < 64; ++j)
-                            if (j < p.k) Store<T>::one(dst + j, v[mt][j] * inv);
+                            for (int j = 0; j < 32; ++j)
+                                if (c0 + j < p.k) Store<T>::one(dst + j, v[mt][j] * inv);
+                        }
                     }
                 }
+            }
+            if (!small_k) {
+                tc::fence_before();
+                tc::mbar_arrive(&tmem_empty[rg]);
             }
         }
     }
@@ -687,7 +717,7 @@ size_t smem_bytes(const Params& p) {
     s += g.pbytes;                         // P
     s += g.xtbytes;                        // fp32: K-major X^T copy
     s += 2 * (size_t)g.xstage;             // X stages
-    s += 128 + 8 * 4 + 64;                 // barriers + reductions
+    s += 128 + 8 * 4 + 2 * 2 * 128 * 4 + 64;  // barriers + FM / LCB reductions
     return s;
 }
 
@@ -752,7 +782,7 @@ lattice_status launch_t(const Plan& pl, cudaStream_t st) {
     }
     const int grid = (int)(pl.p.B < num_sms() ? pl.p.B : num_sms());
     if (grid <= 0) return LATTICE_OK;
-    fm_lcb_kernel<T><<<grid, kThreads, smem_bytes(pl.p), st>>>(pl.tmX, pl.tmWL, pl.tmYT, pl.p);
+    fm_lcb_kernel<T><<<grid, kResThreads, smem_bytes(pl.p), st>>>(pl.tmX, pl.tmWL, pl.tmYT, pl.p);
     LAT_CUDA(cudaGetLastError());
     return LATTICE_OK;
 }

@@ -1,0 +1,8 @@
+summ() { python -c "
+import json,sys
+d=json.loads([l for l in open('$1') if l.startswith('{')][-1])
+st=d.get('stages',{})
+print('$1', round(d['value']), round(d['e2e']['value']), d['ms_per_step'], st.get('embedding',{}).get('ms'), st.get('embedding',{}).get('peer_split_ms'), d['clocks']['sm_mhz'])"; }
+timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29581 bench.py --gpus 4 > gpurun_out/n4.json 2>/dev/null; summ gpurun_out/n4.json
+timeout 300 python bench.py --exchange peer1 > gpurun_out/n1p.json 2>/dev/null; summ gpurun_out/n1p.json
+timeout 300 python bench.py > gpurun_out/n1.json 2>/dev/null; summ gpurun_out/n1.json

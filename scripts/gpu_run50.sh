@@ -1,0 +1,8 @@
+summ() { python -c "
+import json,sys
+d=json.loads([l for l in open('$1') if l.startswith('{')][-1])
+st=d.get('stages',{})
+print('$1', round(d['value']), d['ms_per_step'], st.get('embedding',{}).get('ms'), st.get('fm_lcb'), d['clocks']['sm_mhz'])"; }
+timeout 900 python -m pytest tests/test_network_gpu.py tests/test_dense_gpu.py tests/test_gemm_gpu.py -x -q > gpurun_out/pytest_net.log 2>&1; tail -2 gpurun_out/pytest_net.log
+timeout 300 python bench.py --steps 20 --warmup 5 --cpu-seconds 1 > gpurun_out/n1.json 2>/dev/null; summ gpurun_out/n1.json
+timeout 300 python bench.py --steps 20 --warmup 5 --cpu-seconds 1 > gpurun_out/n1b.json 2>/dev/null; summ gpurun_out/n1b.json
