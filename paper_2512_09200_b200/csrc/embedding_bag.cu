@@ -52,13 +52,6 @@ struct BagParams {
     int32_t src_foff;
 };
 
-__device__ __forceinline__ uint4 ld_stream(const void* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
 // Table rows with an L2 evict_last policy: rows of the table being pooled are re-read by
 // other bags a few microseconds later, while ids/offsets/outputs stream through once.
 __device__ __forceinline__ uint4 ld_row_keep(const void* p, uint64_t pol) {

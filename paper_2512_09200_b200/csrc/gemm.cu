@@ -402,6 +402,151 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2) for the plain and residual-norm epilogues: a cluster of two
+// CTAs on one TPC computes a 256 x BN tile. CTA r loads A rows [m0 + 128r, +128) and B rows
+// [n0 + 128r, +128) (half of the N tile) per k-block, all completions landing on the leader's
+// barrier; the leader issues M = 256 MMAs that read both CTAs' operands, so each SM's smem
+// supplies half of B instead of all of it (the single-CTA kernel's operand traffic is
+// smem-bandwidth bound); each CTA's TMEM holds its 128 accumulator rows x BN columns and its
+// epilogue warps drain them as before.
+// ---------------------------------------------------------------------------------------------
+template <int STAGES, typename T>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+    using Op = tc::Operand<T>;
+    constexpr int BKE = Op::kRow;
+    constexpr int A_BYTES = BM * 128;         // this CTA's 128 A rows
+    constexpr int B_BYTES = (BN / 2) * 128;   // this CTA's half of the N tile
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;   // [2]
+    uint64_t* tempty = tfull + 2;       // [2] (the leader's counts both CTAs' epilogue warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = (int)tc::cluster_rank();
+    const int mt2 = (p.M + 2 * BM - 1) / (2 * BM), nt = (p.N + BN - 1) / BN;
+    const int units = mt2 * nt, first = blockIdx.x / 2, stride = gridDim.x / 2;
+    const int nk = (p.K + BKE - 1) / BKE;
+    auto decode2 = [&](int u, int& m0, int& n0) {  // banded raster over pair M-tiles
+        const int per = kRasterGroup * nt;
+        const int g = u / per, in = u % per;
+        const int rows = min(kRasterGroup, mt2 - g * kRasterGroup);
+        m0 = (g * kRasterGroup + in % rows) * 2 * BM;
+        n0 = (in / rows) * BN;
+    };
+
+    if (warp == 0 && lane == 0) {
+        tc::tma_prefetch(&tmA);
+        tc::tma_prefetch(&tmB);
+        for (int i = 0; i < STAGES; ++i) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&tfull[i], 1);
+            tc::mbar_init(&tempty[i], 8);  // one arrive per epilogue warp of both CTAs
+        }
+        tc::fence_mbar_init();
+    }
+    if (warp == 1) tc::tmem_alloc_cg2(tmem_slot, 2 * BN);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    tc::cluster_sync();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer (both CTAs), completions on the leader's barrier
+            int g = 0;
+            for (int u = first; u < units; u += stride) {
+                int m0, n0;
+                decode2(u, m0, n0);
+                for (int kb = 0; kb < nk; ++kb, ++g) {
+                    const int st = g % STAGES;
+                    const uint32_t ph = (g / STAGES) & 1;
+                    tc::mbar_wait(&empty[st], ph ^ 1);
+                    if (rank == 0) tc::mbar_expect_tx(&full[st], 2 * (A_BYTES + B_BYTES));
+                    const uint32_t bar = tc::mapa(tc::smem_u32(&full[st]), 0);
+                    tc::tma_load_2d_cg2(sA + st * A_BYTES, &tmA, bar, kb * BKE, m0 + rank * BM);
+                    tc::tma_load_2d_cg2(sB + st * B_BYTES, &tmB, bar, kb * BKE, n0 + rank * (BN / 2));
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {  // ---- MMA issuer: the leader only
+            constexpr uint32_t idesc = tc::idesc_fmt(Op::kFormat, 2 * BM, BN, 0, 0);
+            int g = 0, i = 0;
+            for (int u = first; u < units; u += stride, ++i) {
+                const int acc = i & 1;
+                tc::mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
+                tc::fence_after();
+                const uint32_t d_tmem = tmem + acc * BN;
+                for (int kb = 0; kb < nk; ++kb, ++g) {
+                    const int st = g % STAGES;
+                    const uint32_t ph = (g / STAGES) & 1;
+                    tc::mbar_wait(&full[st], ph);
+                    tc::fence_after();
+                    const uint32_t a_base = tc::smem_u32(sA + st * A_BYTES);
+                    const uint32_t b_base = tc::smem_u32(sB + st * B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint64_t ad = tc::sdesc(a_base + k * 32, 16, 1024, 2);
+                        const uint64_t bd = tc::sdesc(b_base + k * 32, 16, 1024, 2);
+                        tc::mma_f16_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    tc::mma_commit_cg2(&empty[st]);
+                }
+                tc::mma_commit_cg2(&tfull[acc]);
+            }
+        }
+    } else {  // ---- epilogue warps 2..5 (both CTAs): this CTA's 128 accumulator rows
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        int i = 0;
+        for (int u = first; u < units; u += stride, ++i) {
+            int m0, n0;
+            decode2(u, m0, n0);
+            const int acc = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            const int64_t m = (int64_t)m0 + rank * BM + row;
+            const bool valid = m < p.M;
+            const uint32_t taddr = tmem + acc * BN + ((uint32_t)(q * 32) << 16);
+            tc::mbar_wait(&tfull[acc], ph);
+            tc::fence_after();
+            if (p.epi == kStore) {
+#pragma unroll 1
+                for (int c = 0; c < BN; c += 32) {
+                    float v[32];
+                    tc::tmem_ld32(taddr + c, v);
+                    if (valid && n0 + c < p.N) store_row32(p, m, n0 + c, v);
+                }
+            } else if (p.group == 128) {
+#pragma unroll 1
+                for (int gc = 0; gc < BN; gc += 128)
+                    if (n0 + gc < p.N) resid_norm_group<128>(p, taddr + gc, m, n0 + gc, valid);
+            } else {
+#pragma unroll 1
+                for (int gc = 0; gc < BN; gc += 64)
+                    if (n0 + gc < p.N) resid_norm_group<64>(p, taddr + gc, m, n0 + gc, valid);
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive_remote(tc::mapa(tc::smem_u32(&tempty[acc]), 0));
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::cluster_sync();  // the leader's MMAs read the peer's smem / write its TMEM until the end
+    if (warp == 1) tc::tmem_dealloc_cg2(tmem, 2 * BN);
+}
+
+// ---------------------------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------------------------
 namespace {
@@ -462,6 +607,56 @@ lattice_status launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Para
 }
 }  // namespace
 
+constexpr int kStages2 = 6;
+
+lattice_status launch_2cta(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t st) {
+    const size_t smem = 1024 + (size_t)kStages2 * (BM * 128 + (BN / 2) * 128) + 256;
+    static bool attr_done = false;
+    if (!attr_done) {
+        LAT_CUDA(cudaFuncSetAttribute(gemm2_kernel<kStages2, __nv_bfloat16>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_done = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static int max_pairs = 0;
+    if (!max_pairs) {
+        cfg.gridDim = dim3(2 * (num_sms() / 2), 1, 1);
+        int mc = 0;
+        if (cudaOccupancyMaxActiveClusters(&mc, gemm2_kernel<kStages2, __nv_bfloat16>, &cfg) != cudaSuccess || mc < 1)
+            mc = num_sms() / 2;
+        max_pairs = mc;
+    }
+    const int units = ((p.M + 2 * BM - 1) / (2 * BM)) * ((p.N + BN - 1) / BN);
+    int pairs = max_pairs < units ? max_pairs : units;
+    if (pairs < 1) pairs = 1;
+    cfg.gridDim = dim3(2 * pairs, 1, 1);
+    LAT_CUDA(cudaLaunchKernelEx(&cfg, gemm2_kernel<kStages2, __nv_bfloat16>, ta, tb, p));
+    return LATTICE_OK;
+}
+
+// The CTA-pair kernel serves bf16 plain / residual-norm GEMMs with at least two M-tiles;
+// LATTICE_GEMM_2CTA=0 turns it off (A/B runs).
+bool use_2cta(const Params& p, bool f32) {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = std::getenv("LATTICE_GEMM_2CTA");
+        env = e ? std::atoi(e) : 1;
+    }
+    return env != 0 && !f32 && p.cluster == 1 && !p.tiles && (p.epi == kStore || p.epi == kResidNorm) &&
+           p.M >= 2 * BM;
+}
+
+
 lattice_status make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
                            uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, bool f32) {
     auto fn = encode_fn();
@@ -482,6 +677,7 @@ lattice_status make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uin
 }
 
 lattice_status launch(const GemmPlan& g, cudaStream_t st) {
+    if (g.two_cta) return launch_2cta(g.ta, g.tb, g.p, st);
     // grid_y carries the number of M units (dense M-tiles, or the tile-table capacity)
     const int nt = (g.p.N + BN - 1) / BN;
     const int units = g.p.cluster > 1 ? g.grid_y : g.grid_y * nt;
@@ -495,7 +691,9 @@ lattice_status plan(GemmPlan* g, const void* A, int64_t lda, int64_t a_rows, con
     const uint32_t bke = f32 ? 32 : 64;
     lattice_status s = make_map_2d(&g->ta, A, (uint64_t)p.K, (uint64_t)a_rows, (uint64_t)lda * es, bke, BM, f32);
     if (s != LATTICE_OK) return s;
-    s = make_map_2d(&g->tb, B, (uint64_t)p.K, (uint64_t)b_rows, (uint64_t)ldb * es, bke, BN, f32);
+    g->two_cta = use_2cta(p, f32);
+    s = make_map_2d(&g->tb, B, (uint64_t)p.K, (uint64_t)b_rows, (uint64_t)ldb * es, bke, g->two_cta ? BN / 2 : BN,
+                    f32);
     if (s != LATTICE_OK) return s;
     g->p = p;
     g->grid_y = grid_y;

@@ -13,7 +13,8 @@ struct GemmPlan {
     Params p;
     int grid_y;
     int stages;
-    bool f32;  // fp32 operands on the TF32 tensor path
+    bool f32;      // fp32 operands on the TF32 tensor path
+    bool two_cta;  // CTA-pair (cta_group::2) kernel: B tensor map boxes are BN/2 rows
 };
 
 lattice_status make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
