@@ -433,7 +433,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int mt2 = (p.M + 2 * BM - 1) / (2 * BM), nt = (p.N + BN - 1) / BN;
     const int units = mt2 * nt, first = blockIdx.x / 2, stride = gridDim.x / 2;
     const int nk = (p.K + BKE - 1) / BKE;
-    auto decode2 = [&](int u, int& m0, int& n0) {  // banded raster over pair M-tiles
+    const bool swish = p.epi == kSwish || p.epi == kSwishHard;
+    auto decode2 = [&](int u, int& m0, int& n0) {
+        if (swish) {  // row-major: a row block's N-tiles are consecutive units (see the exchange)
+            m0 = (u / nt) * 2 * BM;
+            n0 = (u % nt) * BN;
+            return;
+        }
+        // banded raster over pair M-tiles
         const int per = kRasterGroup * nt;
         const int g = u / per, in = u % per;
         const int rows = min(kRasterGroup, mt2 - g * kRasterGroup);
@@ -524,6 +531,47 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int c = 0; c < BN; c += 32) {
                     float v[32];
                     tc::tmem_ld32(taddr + c, v);
+                    if (valid && n0 + c < p.N) store_row32(p, m, n0 + c, v);
+                }
+            } else if (swish) {
+                // swish_rn over the full row (numerics.hpp:94-107): this tile's partial sum of
+                // squares goes to global memory, the row block's (256 rows x all N-tiles) CTAs
+                // count in per CTA half, and every row sums its N-tile partials in tile order
+                // (deterministic). All CTAs are co-resident (persistent grid) and a row block's
+                // tiles are consecutive units, at most one schedule round apart: no deadlock.
+                float ss = 0.0f;
+#pragma unroll 1
+                for (int c = 0; c < BN; c += 32) {
+                    float v[32];
+                    tc::tmem_ld32(taddr + c, v);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) ss += (n0 + c + j < p.N) ? v[j] * v[j] : 0.0f;
+                }
+                const int nn = n0 / BN;
+                if (valid) p.rowpart[m * nt + nn] = ss;
+                __threadfence();
+                __syncwarp();
+                int* cnt = p.rowcnt + (m0 / (2 * BM)) * 2 + rank;
+                if (lane == 0) {
+                    atomicAdd(cnt, 1);
+                    const int want = 4 * nt;  // 4 epilogue warps per N-tile
+                    int seen;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
+                    } while (seen < want);
+                }
+                __syncwarp();
+                float total = 0.0f;
+                if (valid)
+                    for (int t = 0; t < nt; ++t) total += __ldcg(p.rowpart + m * nt + t);
+                const float inv = 1.0f / sqrtf(total / (float)p.N_full + 1e-6f);
+                const bool hard = p.epi == kSwishHard;
+#pragma unroll 1
+                for (int c = 0; c < BN; c += 32) {
+                    float v[32];
+                    tc::tmem_ld32(taddr + c, v);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = act_swish(v[j] * inv, hard);
                     if (valid && n0 + c < p.N) store_row32(p, m, n0 + c, v);
                 }
             } else if (p.group == 128) {
@@ -637,6 +685,8 @@ lattice_status launch_2cta(const CUtensorMap& ta, const CUtensorMap& tb, const P
         max_pairs = mc;
     }
     const int units = ((p.M + 2 * BM - 1) / (2 * BM)) * ((p.N + BN - 1) / BN);
+    if (p.epi == kSwish || p.epi == kSwishHard)
+        LAT_CUDA(cudaMemsetAsync(p.rowcnt, 0, sizeof(int) * 2 * ((p.M + 2 * BM - 1) / (2 * BM)), st));
     int pairs = max_pairs < units ? max_pairs : units;
     if (pairs < 1) pairs = 1;
     cfg.gridDim = dim3(2 * pairs, 1, 1);
@@ -652,8 +702,9 @@ bool use_2cta(const Params& p, bool f32) {
         const char* e = std::getenv("LATTICE_GEMM_2CTA");
         env = e ? std::atoi(e) : 1;
     }
-    return env != 0 && !f32 && p.cluster == 1 && !p.tiles && (p.epi == kStore || p.epi == kResidNorm) &&
-           p.M >= 2 * BM;
+    if (env == 0 || f32 || p.tiles || p.M < 2 * BM) return false;
+    if (p.epi == kSwish || p.epi == kSwishHard) return p.rowpart && p.rowcnt && p.N == p.N_full;
+    return p.cluster == 1 && (p.epi == kStore || p.epi == kResidNorm);
 }
 
 
@@ -692,10 +743,12 @@ lattice_status plan(GemmPlan* g, const void* A, int64_t lda, int64_t a_rows, con
     lattice_status s = make_map_2d(&g->ta, A, (uint64_t)p.K, (uint64_t)a_rows, (uint64_t)lda * es, bke, BM, f32);
     if (s != LATTICE_OK) return s;
     g->two_cta = use_2cta(p, f32);
+    Params pp = p;
+    if (g->two_cta) pp.cluster = 1;  // the pair kernel exchanges row statistics through global memory
     s = make_map_2d(&g->tb, B, (uint64_t)p.K, (uint64_t)b_rows, (uint64_t)ldb * es, bke, g->two_cta ? BN / 2 : BN,
                     f32);
     if (s != LATTICE_OK) return s;
-    g->p = p;
+    g->p = pp;
     g->grid_y = grid_y;
     g->stages = 4;
     g->f32 = f32;
@@ -741,7 +794,15 @@ extern "C" lattice_status lattice_gemm(const lattice_gemm_args* a, lattice_strea
     LAT_REQUIRE(a->in_dtype == LATTICE_BF16 || a->in_dtype == LATTICE_F32, "lattice_gemm: in_dtype must be bf16 or f32");
     const bool f32 = a->in_dtype == LATTICE_F32;
     LAT_REQUIRE(!f32 || (a->K % 4 == 0 && a->lda % 4 == 0 && a->ldb % 4 == 0), "lattice_gemm: fp32 strides");
+    void* ws = nullptr;  // swish row-statistics exchange of the CTA-pair kernel
+    if (p.epi == kSwish || p.epi == kSwishHard) {
+        const size_t rows = (size_t)((a->M + 2 * BM - 1) / (2 * BM)) * 2 * BM;
+        LAT_CUDA(cudaMallocAsync(&ws, rows * p.cluster * sizeof(float) + rows / BM * sizeof(int) + 64, stream));
+        p.rowpart = static_cast<float*>(ws);
+        p.rowcnt = reinterpret_cast<int*>(static_cast<float*>(ws) + rows * p.cluster);
+    }
     lattice_status s = plan(&g, a->A, a->lda, a->M, a->B, a->ldb, a->N, p, (int)((a->M + BM - 1) / BM), f32);
-    if (s != LATTICE_OK) return s;
-    return launch(g, stream);
+    if (s == LATTICE_OK) s = launch(g, stream);
+    if (ws) cudaFreeAsync(ws, stream);
+    return s;
 }

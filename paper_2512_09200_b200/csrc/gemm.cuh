@@ -47,6 +47,10 @@ struct Params {
     int group;
     int cluster;         // CTAs along N sharing a row (row-norm epilogues)
     int N_full;          // width of the normalised row (= N)
+    // CTA-pair swish epilogue: per-row partial sums of squares of every N-tile ([M][N-tiles])
+    // and per (256-row block, CTA half) arrival counters, exchanged through global memory
+    float* rowpart;
+    int* rowcnt;
     // grouped
     const int4* tiles;   // {group, row0, row_end, 0}; nullptr = dense
     const int* n_tiles;

@@ -116,6 +116,8 @@ struct lattice_net {
     void* D1 = nullptr;          // dense processor [dense_hidden][dense_in]
     void* D2 = nullptr;          // [dense_features*d][dense_hidden]
     void *Din = nullptr, *Hd = nullptr, *Od = nullptr;  // dense input copy, hidden, output rows
+    float* rowpart = nullptr;  // swish GEMMs (CTA-pair kernel): row-statistics exchange
+    int* rowcnt = nullptr;
     // workspace
     int32_t *pos = nullptr, *order = nullptr, *seg = nullptr;
     int4* tiles = nullptr;
@@ -248,6 +250,8 @@ lattice_status build_plans(lattice_net* net) {
                 p.ldc = out;
                 p.epi = c.hard ? gemm::kSwishHard : gemm::kSwish;
                 p.cluster = (out + 255) / 256;
+                p.rowpart = net->rowpart;
+                p.rowcnt = net->rowcnt;
             } else {
                 p.C = Xn;
                 p.ldc = nd;
@@ -272,6 +276,8 @@ lattice_status build_plans(lattice_net* net) {
         d1.ldc = c.dense_hidden;
         d1.epi = c.hard ? gemm::kSwishHard : gemm::kSwish;
         d1.cluster = (c.dense_hidden + 255) / 256;
+        d1.rowpart = net->rowpart;
+        d1.rowcnt = net->rowcnt;
         lattice_status s = gemm::plan(&net->dense_plans[0], net->Din, c.dense_in, Bm, net->D1, c.dense_in,
                                       c.dense_hidden, d1, (int)((Bm + 127) / 128), net->f32);
         if (s != LATTICE_OK) return s;
@@ -376,6 +382,11 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
     }
     int max_hidden = 8;
     for (int i = 1; i < c.n_mlp; ++i) max_hidden = max_hidden > c.mlp[i] ? max_hidden : c.mlp[i];
+    {  // row-statistics exchange of the swish GEMMs: [rows][<= 8 N-tiles] + counters
+        const size_t rows = (size_t)((Bm + 255) / 256) * 256;
+        NET_TRY(dalloc(net, &net->rowpart, rows * 8));
+        NET_TRY(dalloc(net, &net->rowcnt, rows / 128 + 16));
+    }
     NET_TRY(dalloc(net, &net->pos, (size_t)Bm));
     NET_TRY(dalloc(net, &net->order, (size_t)Bm));
     NET_TRY(dalloc(net, &net->seg, (size_t)c.domains + 1));
