@@ -369,6 +369,31 @@ def ref_student_queries(base, slot, store_emb, store_logit, written_at, ttl, now
     return rc, rows, logits, hit
 
 
+def net_forward(cfg, w, pooled, dom, bf16=True, hard=False, threads=0):
+    """lo_net_forward for a Network config dict and its weights() (host fp32 arrays):
+    pooled [count, n, d] raw sums, dom [count] -> logits [count, heads]."""
+    c = LoNetCfg()
+    c.n, c.d, c.blocks, c.nF, c.nL, c.k = cfg["n"], cfg["d"], cfg["blocks"], cfg["nF"], cfg["nL"], cfg["k"]
+    c.n_mlp = len(cfg["mlp"]) - 1
+    for i, v in enumerate(cfg["mlp"]):
+        c.mlp[i] = v
+    c.G, c.heads, c.tower_hidden, c.hard, c.bf16 = cfg["domains"], cfg["heads"], cfg["tower_hidden"], int(hard), int(bf16)
+    keep = [np.ascontiguousarray(a, dtype=np.float32) for a in w["YT"] + w["WL"] + w["mlp"]]
+    nb = cfg["blocks"]
+    yt = (_P * nb)(*[a.ctypes.data for a in keep[:nb]])
+    wl = (_P * nb)(*[a.ctypes.data for a in keep[nb:2 * nb]])
+    ml = (_P * len(w["mlp"]))(*[a.ctypes.data for a in keep[2 * nb:]])
+    T1 = np.ascontiguousarray(w["T1"], dtype=np.float32)
+    T2 = np.ascontiguousarray(w["T2"], dtype=np.float32)
+    ws = LoNetWeights(ctypes.cast(yt, _P), ctypes.cast(wl, _P), ctypes.cast(ml, _P), _P(T1.ctypes.data),
+                      _P(T2.ctypes.data))
+    pooled = np.ascontiguousarray(pooled, dtype=np.float32)
+    d = np.ascontiguousarray(dom, dtype=np.int32)
+    out = np.zeros((len(d), cfg["heads"]), np.float32)
+    load_oracle().lo_net_forward(ctypes.byref(c), ctypes.byref(ws), len(d), ptr(pooled), ptr(d), ptr(out), threads)
+    return out
+
+
 def synth_bags(F, B, max_len, rows, seed):
     lib = load_oracle()
     offsets = np.zeros(F * B + 1, np.int64)
