@@ -126,17 +126,23 @@ LARGE_N = dict(n=512, d=128, blocks=1, nF=256, nL=256, k=32, mlp=[16384, 256, 32
                heads=3, tower_hidden=256)
 
 
-def test_large_n_streamed_wl_matches_oracle():
-    """n = 512 / nL = 256 (the large config's backbone width) runs the streamed-W_L FM/LCB
-    variant; widths of the MLP/tower shrunk so the fp64 oracle stays fast."""
+LARGE_N_384 = dict(n=384, d=128, blocks=2, nF=256, nL=128, k=16, mlp=[6144, 256, 32768], domains=2,
+                   heads=3, tower_hidden=256)
+
+
+@pytest.mark.parametrize("cfg", [LARGE_N, LARGE_N_384], ids=["n512_nL256", "n384_nL128"])
+def test_large_n_streamed_matches_oracle(cfg):
+    """n > 256 (the large config's backbone width) runs the large FM/LCB variant (X_b resident,
+    W_L streamed through a TMA ring of panels), n = 384 with zero-padded rows; widths of the
+    MLP/tower shrunk so the fp64 oracle stays fast."""
     import torch
     B, rows = 300, 4000
-    net, tab, ptrs, rws, offsets, ids, dom = build(LARGE_N, B, rows)
+    net, tab, ptrs, rws, offsets, ids, dom = build(cfg, B, rows)
     logits = net.forward(dom, offsets, ids, ptrs, rws, torch.bfloat16)
     torch.cuda.synchronize()
     samples = [0, 1, 150, 299]
-    want, w = oracle_logits(net, LARGE_N, rows, offsets, ids, dom, samples)
-    check_weights_against_generator(w, LARGE_N)
+    want, w = oracle_logits(net, cfg, rows, offsets, ids, dom, samples)
+    check_weights_against_generator(w, cfg)
     assert_logits_close(logits.cpu().numpy()[samples], want)
 
 
