@@ -402,11 +402,20 @@ def run_mid(args, rank, world, local):
     def step():
         forward(dom, offsets, ids, logits)
 
+    step_eager = step
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
+        if args.graph:  # the whole forward step captured once and replayed (no per-kernel host launches)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                forward(dom, offsets, ids, logits)
+            stream = torch.cuda.current_stream()
+            graph.replay()
+            torch.cuda.synchronize()
+            step = graph.replay
         barrier(world)
         torch.cuda.synchronize()
         clk.mark()
@@ -445,7 +454,7 @@ def run_mid(args, rank, world, local):
             torch.cuda.synchronize()
             emb_ms.append(a0.elapsed_time(a1))
         else:
-            step()
+            step_eager()
         stages.append(net.stage_times())
     net.set_timing(False)
     st = [min(s[i] for s in stages) for i in range(len(stages[0]))]  # min: robust to host hiccups
@@ -560,6 +569,7 @@ def run_mid(args, rank, world, local):
                    "global_batch": world * B, "ids_per_step": n_ids,
                    "l2": ("embedding rows drawn uniformly from %.1f GB of tables per GPU; activations %.1f GB/buffer (> L2)"
                           % (n_tab * MID_ROWS * d * 2 / 1e9, B * n * d * 2 / 1e9)),
+                   "launch": "CUDA graph replay of the forward step" if args.graph else "eager launches",
                    "parallelism": ((f"table-wise sharded embeddings over {world} GPUs (owner kernel reads "
                                     f"peers' ids and stores pooled rows into their X0 over NVLink via CUDA "
                                     f"IPC, in-kernel barriers, no NCCL on the data path) + dense replicas")
@@ -691,6 +701,9 @@ def main():
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"], help="micro table dtype")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch every kernel of the timed steps from the host instead of replaying the "
+                         "forward step from a CUDA graph")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl", "peer1"],
                     help="N>1 sharded embedding exchange: peer memory (default) or NCCL all-to-alls")
     args = ap.parse_args()

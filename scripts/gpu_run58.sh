@@ -1,0 +1,3 @@
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo rc=$?; tail -3 gpurun_out/smoke.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/ref.json 2>&1; tail -c 300 gpurun_out/ref.json
