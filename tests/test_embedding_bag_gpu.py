@@ -159,3 +159,27 @@ def test_rownorm_matches_reference_numerics():
         L.rownorm(torch.tensor([[1.0, float("nan")]], device="cuda"), 1)
     with pytest.raises(L.UsageError):
         L.rownorm(torch.zeros((1, 0), device="cuda"), 1)
+
+
+def test_full_micro_config_sampled_and_checksum():
+    """BASELINE configs[1] at full size (64 tables x 1M rows x 128, B = 16384, bf16 tables):
+    sampled samples bit-exact against the oracle, and a size-independent property over the
+    whole batch: the sum of every pooled row equals the sum of every gathered table row (exact
+    in fp64 under the synthetic value scheme), computed on the GPU from the ids alone."""
+    import torch
+    import paper_2512_09200_b200 as L
+    F, rows, D, B = 64, 1_000_000, 128, 16384
+    tab, offsets, ids = make(F, rows, D, B, 40, torch.bfloat16)
+    out = L.embedding_bag(list(tab.unbind(0)), offsets, ids, B, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    o_cpu = offsets.cpu().numpy()
+    i_cpu = ids[: int(o_cpu[-1])].cpu().numpy()
+    for s in (0, 4097, B - 1):
+        ref, bad = oracle.embedding_bag_synth(SEED_T, F, rows, D, B, o_cpu, i_cpu, s, s + 1)
+        assert bad == -1 and np.array_equal(out[s].cpu().numpy(), ref[0])
+    # checksum: sum over bags of pooled rows == sum over every (feature, id) occurrence of the row
+    lens = (offsets[1:] - offsets[:-1])
+    feat = torch.repeat_interleave(torch.arange(F * B, device="cuda") // B, lens)
+    n = int(o_cpu[-1])
+    gathered = tab.view(F * rows, D)[feat * rows + ids[:n].long()].double().sum(0)
+    assert torch.equal(out.double().sum((0, 1)), gathered)

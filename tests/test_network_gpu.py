@@ -204,3 +204,31 @@ def test_config_contract():
     bad["mlp"] = [1024, 4096, 4096]  # last width != nF*d
     with pytest.raises(L.UsageError):
         L.Network(**bad, max_batch=16)
+
+
+def test_mid_config_full_batch_sampled_logits():
+    """BASELINE configs[2] at its full size (256 features x 100k rows, l = 4, MLP 8192-2048-2048-
+    16384, B = 32768): three sampled logits against the fp64 oracle (same tolerance), plus the
+    size-independent property that the per-domain towers see every sample exactly once (a
+    permutation of the batch changes no sample's logits, bit for bit)."""
+    import torch
+    import paper_2512_09200_b200 as L
+    B, rows = 32768, 100000
+    net, tab, ptrs, rws, offsets, ids, dom = build(MID, B, rows)
+    logits = net.forward(dom, offsets, ids, ptrs, rws, torch.bfloat16).clone()
+    torch.cuda.synchronize()
+    samples = [3, 16000, 32767]
+    want, w = oracle_logits(net, MID, rows, offsets, ids, dom, samples)
+    assert_logits_close(logits.cpu().numpy()[samples], want)
+    # permuted batch: reverse the samples (bags and domains), logits must follow exactly
+    n = MID["n"]
+    lens = (offsets[1:] - offsets[:-1]).view(n, B)
+    starts = offsets[:-1].view(n, B)
+    rlens = lens.flip(1).reshape(-1)
+    roff = torch.zeros(n * B + 1, dtype=torch.int64, device="cuda")
+    roff[1:] = torch.cumsum(rlens, 0)
+    src = torch.repeat_interleave(starts.flip(1).reshape(-1), rlens) + (
+        torch.arange(int(roff[-1]), device="cuda") - torch.repeat_interleave(roff[:-1], rlens))
+    rids = ids[src]
+    rl = net.forward(dom.flip(0).contiguous(), roff, rids, ptrs, rws, torch.bfloat16)
+    assert torch.equal(rl.flip(0), logits)
