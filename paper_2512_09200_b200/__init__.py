@@ -13,7 +13,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblattice_b200.so")
+# LATTICE_LIB: load another build of the library (A/B runs of two builds on one box)
+LIB_PATH = os.environ.get("LATTICE_LIB") or os.path.join(_HERE, "liblattice_b200.so")
 
 OK, USAGE, DATA, CUDA, NCCL = 0, 1, 2, 3, 4
 F32, BF16, F64 = 0, 1, 2

@@ -159,6 +159,21 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 constexpr int kBagWarps = 8;
 __device__ __align__(16) uint4 g_zero_row[64];  // 1 KB of zeros: the row of an invalid id
 
+// 1 / sqrt(x) for the rms_norm scale: x = mean(x^2) + 1e-6 is never denormal, so the ftz
+// MUFU.RSQ is the same value as rsqrtf without its denormal fix-up instructions
+// base + id * rowb as ONE IMAD.WIDE.U32 (mad.wide.u32 with the 64-bit base as addend; left to
+// itself the compiler splits it into a wide multiply, a LOP3 and a 64-bit add)
+__device__ __forceinline__ const uint8_t* row_addr(const uint8_t* base, uint32_t id, uint32_t rowb) {
+    uint64_t a;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(id), "r"(rowb), "l"(reinterpret_cast<uint64_t>(base)));
+    return reinterpret_cast<const uint8_t*>(a);
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // ---- direct kernel (single GPU and the NCCL-exchange owner side) ----------------------------
 // Persistent warps with dynamic scheduling: a warp claims kChunk consecutive bags at a time
 // from a global counter, so all warps stay inside a narrow window of the bag sequence -- the
@@ -234,13 +249,16 @@ __device__ __forceinline__ uint32_t claim_chunk(unsigned long long* counter, int
 // accumulates them. MASK: rows at or past `cnt` read the zero row instead (bag tail).
 // CHECK = false: the caller verified that every id of this 32-id window is in range, so rows
 // are addressed without a per-row bound check (the common case); MASK rows past `cnt` still
-// read the zero row.
+// read the zero row. `tlane` / `zlane` are the table / zero row already offset to this lane's
+// first 16-byte column, and a row is exactly LPR*CPL*16 bytes (launch_bag picks LPR, CPL from
+// the row size), so a row address is one IMAD.WIDE of the id.
 template <typename TT, int LPR, int CPL, int N, bool MASK, bool CHECK, bool PEER>
 __device__ __forceinline__ void gather_step(const BagParams& p, uint32_t bag, const int32_t* idp, int base,
-                                            const TT* __restrict__ table, uint32_t rows, int my_id, int j,
-                                            int cnt, int sub, int cl, uint64_t pol, float* acc) {
+                                            const uint8_t* __restrict__ tlane, uint32_t rows, int my_id, int j,
+                                            int cnt, int sub, const uint8_t* zlane, uint64_t pol, float* acc) {
     constexpr int EPC = Elem<TT>::kPerChunk;
     constexpr int RPP = 32 / LPR;
+    constexpr uint32_t ROWB = LPR * CPL * 16;
     uint4 v[N][CPL];
 #pragma unroll
     for (int u = 0; u < N; ++u) {
@@ -253,10 +271,9 @@ __device__ __forceinline__ void gather_step(const BagParams& p, uint32_t bag, co
             if (live && !ok) atomicMin(p.err, id_position<PEER>(p, bag, idp + base + jj));
         }
         if (MASK) ok = ok && jj < cnt;
-        const TT* row = (!CHECK && !MASK) || ok ? table + (size_t)(uint32_t)id * p.D
-                                                : reinterpret_cast<const TT*>(g_zero_row);
+        const uint8_t* row = (!CHECK && !MASK) || ok ? row_addr(tlane, (uint32_t)id, ROWB) : zlane;
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) v[u][c] = ld_row_keep(row + (c * LPR + cl) * EPC, pol);
+        for (int c = 0; c < CPL; ++c) v[u][c] = ld_row_keep(row + c * LPR * 16, pol);
     }
 #pragma unroll
     for (int u = 0; u < N; ++u)
@@ -278,6 +295,7 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
     const bool ef = (p.l2keep & 2) != 0;
     const uint64_t pol = (p.l2keep & 1) ? policy_evict_last() : policy_evict_normal();  // table rows
     const uint64_t pol_ef = policy_evict_first();
+    const uint8_t* zlane = reinterpret_cast<const uint8_t*>(g_zero_row) + cl * 16;
     const int32_t* idp;
     int len;
     bag_range<PEER>(p, bag, idp, len);
@@ -301,7 +319,13 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
             // issued before the row gathers so the NVLink round trip overlaps them
             asm volatile("ld.global.s32 %0, [%1];" : "=r"(peer_row) : "l"(p.p_pos[r] + b));
         }
-        const TT* __restrict__ table = static_cast<const TT*>(p.tables[f]);
+        // the output row is requested before the gathers (its latency hides under them)
+        const int64_t ob = (int64_t)r * p.B + b;  // output sample r*B + b (plain mode)
+        int64_t orow = ob;
+        if constexpr (!PEER) {
+            if (p.pos) orow = __ldg(p.pos + ob);
+        }
+        const uint8_t* __restrict__ tlane = static_cast<const uint8_t*>(p.tables[f]) + cl * 16;
         const int64_t rows64 = p.rows[f];
         const uint32_t rows = rows64 < 0x7fffffff ? (uint32_t)rows64 : 0x7fffffffu;
 
@@ -315,18 +339,18 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
             int j = 0;
             if (__all_sync(0xffffffffu, lane >= cnt || (uint32_t)my_id < rows)) {  // all ids in range
                 for (; j + RPP * U <= cnt; j += RPP * U)
-                    gather_step<TT, LPR, CPL, U, false, false, PEER>(p, bag, idp, base, table, rows, my_id, j, cnt,
-                                                                     sub, cl, pol, acc);
+                    gather_step<TT, LPR, CPL, U, false, false, PEER>(p, bag, idp, base, tlane, rows, my_id, j, cnt, sub,
+                                                                     zlane, pol, acc);
                 for (; j < cnt; j += RPP * UT)
-                    gather_step<TT, LPR, CPL, UT, true, false, PEER>(p, bag, idp, base, table, rows, my_id, j, cnt,
-                                                                     sub, cl, pol, acc);
+                    gather_step<TT, LPR, CPL, UT, true, false, PEER>(p, bag, idp, base, tlane, rows, my_id, j, cnt, sub,
+                                                                     zlane, pol, acc);
             } else {  // some id out of range: checked path (zero contribution + first-offender error)
                 for (; j + RPP * U <= cnt; j += RPP * U)
-                    gather_step<TT, LPR, CPL, U, false, true, PEER>(p, bag, idp, base, table, rows, my_id, j, cnt,
-                                                                    sub, cl, pol, acc);
+                    gather_step<TT, LPR, CPL, U, false, true, PEER>(p, bag, idp, base, tlane, rows, my_id, j, cnt, sub,
+                                                                     zlane, pol, acc);
                 for (; j < cnt; j += RPP * UT)
-                    gather_step<TT, LPR, CPL, UT, true, true, PEER>(p, bag, idp, base, table, rows, my_id, j, cnt,
-                                                                    sub, cl, pol, acc);
+                    gather_step<TT, LPR, CPL, UT, true, true, PEER>(p, bag, idp, base, tlane, rows, my_id, j, cnt, sub,
+                                                                     zlane, pol, acc);
             }
         }
         // next bag's first ids (its offsets were requested before this bag's rows)
@@ -343,13 +367,14 @@ __global__ void __launch_bounds__(kBagWarps * 32, MINB) bag_kernel(const BagPara
             for (int i = 0; i < CPL * EPC; ++i) ss += acc[i] * acc[i];
 #pragma unroll
             for (int o = 1; o < LPR; o <<= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-            const float inv = rsqrtf(ss / (float)p.D + 1e-6f);  // MUFU.RSQ (~2 ulp; the row is then rounded to bf16)
+            // D = LPR*CPL*EPC is a power of two: the product with 1/D equals the division;
+            // MUFU.RSQ (~2 ulp; the row is then rounded to bf16)
+            const float inv = rsqrt_ftz(ss * (1.0f / (LPR * CPL * EPC)) + 1e-6f);
 #pragma unroll
             for (int i = 0; i < CPL * EPC; ++i) acc[i] *= inv;
         }
         if (sub == 0) {
-            const int64_t ob = (int64_t)r * p.B + b;  // output sample r*B + b (plain mode)
-            const int64_t row = PEER ? (int64_t)peer_row : p.pos ? (int64_t)p.pos[ob] : ob;
+            const int64_t row = PEER ? (int64_t)peer_row : orow;
             OT* dst = static_cast<OT*>(PEER ? p.p_out[r] : p.out) + row * p.out_stride +
                       (int64_t)(p.out_foff + f) * p.D;
 #pragma unroll
@@ -482,13 +507,14 @@ __device__ __noinline__ unsigned long long id_position(const BagParams& p, int r
 
 // N passes of RPP rows each: every lane issues N*CPL 16-byte row loads back to back, then
 // accumulates them. Ids come from the stage (q < kIdsCap) or global. MASK: rows at or past
-// `len` read the zero row instead (bag tail).
+// `len` read the zero row instead (bag tail). tlane / zlane: as in direct::gather_step.
 template <typename TT, int LPR, int CPL, int N, bool MASK, bool CHECK, bool PEER>
 __device__ __forceinline__ void gather_step(const BagParams& p, const Stage& S, int sk, int j, int len,
-                                            const TT* __restrict__ table, uint32_t rows, int sub, int cl,
-                                            uint64_t pol, float* acc) {
+                                            const uint8_t* __restrict__ tlane, uint32_t rows, int sub,
+                                            const uint8_t* zlane, uint64_t pol, float* acc) {
     constexpr int EPC = Elem<TT>::kPerChunk;
     constexpr int RPP = 32 / LPR;
+    constexpr uint32_t ROWB = LPR * CPL * 16;
     uint4 v[N][CPL];
 #pragma unroll
     for (int u = 0; u < N; ++u) {
@@ -503,11 +529,9 @@ __device__ __forceinline__ void gather_step(const BagParams& p, const Stage& S, 
             if (live && !ok) atomicMin(p.err, id_position<PEER>(p, S.r, S.idg + q));
         }
         ok = ok && live;
-        const TT* row = (!CHECK && !MASK) || ok ? table + (size_t)(uint32_t)id * p.D
-                                                : reinterpret_cast<const TT*>(g_zero_row);
+        const uint8_t* row = (!CHECK && !MASK) || ok ? row_addr(tlane, (uint32_t)id, ROWB) : zlane;
 #pragma unroll
-        for (int c = 0; c < CPL; ++c)
-            v[u][c] = ld_row_keep(row + (c * LPR + cl) * EPC, pol);
+        for (int c = 0; c < CPL; ++c) v[u][c] = ld_row_keep(row + c * LPR * 16, pol);
     }
 #pragma unroll
     for (int u = 0; u < N; ++u)
@@ -523,7 +547,8 @@ __device__ __forceinline__ void pool_chunk(const BagParams& p, const Stage& S, i
     constexpr int UT = U >= 4 ? U / 2 : U;  // passes per masked tail step
     const int sub = lane / LPR, cl = lane % LPR;
     const int f = S.f, n = S.n;
-    const TT* __restrict__ table = static_cast<const TT*>(p.tables[f]);
+    const uint8_t* __restrict__ tlane = static_cast<const uint8_t*>(p.tables[f]) + cl * 16;
+    const uint8_t* zlane = reinterpret_cast<const uint8_t*>(g_zero_row) + cl * 16;
     const int64_t rows64 = p.rows[f];
     const uint32_t rows = rows64 < 0x7fffffff ? (uint32_t)rows64 : 0x7fffffffu;
     OT* out = static_cast<OT*>(PEER ? p.p_out[S.r] : p.out) + (int64_t)(p.out_foff + f) * p.D;
@@ -541,14 +566,14 @@ __device__ __forceinline__ void pool_chunk(const BagParams& p, const Stage& S, i
         }
         if (__all_sync(0xffffffffu, in_range)) {
             for (; j + RPP * U <= len; j += RPP * U)
-                gather_step<TT, LPR, CPL, U, false, false, PEER>(p, S, sk, j, len, table, rows, sub, cl, pol, acc);
+                gather_step<TT, LPR, CPL, U, false, false, PEER>(p, S, sk, j, len, tlane, rows, sub, zlane, pol, acc);
             for (; j < len; j += RPP * UT)
-                gather_step<TT, LPR, CPL, UT, true, false, PEER>(p, S, sk, j, len, table, rows, sub, cl, pol, acc);
+                gather_step<TT, LPR, CPL, UT, true, false, PEER>(p, S, sk, j, len, tlane, rows, sub, zlane, pol, acc);
         } else {
             for (; j + RPP * U <= len; j += RPP * U)
-                gather_step<TT, LPR, CPL, U, false, true, PEER>(p, S, sk, j, len, table, rows, sub, cl, pol, acc);
+                gather_step<TT, LPR, CPL, U, false, true, PEER>(p, S, sk, j, len, tlane, rows, sub, zlane, pol, acc);
             for (; j < len; j += RPP * UT)
-                gather_step<TT, LPR, CPL, UT, true, true, PEER>(p, S, sk, j, len, table, rows, sub, cl, pol, acc);
+                gather_step<TT, LPR, CPL, UT, true, true, PEER>(p, S, sk, j, len, tlane, rows, sub, zlane, pol, acc);
         }
         // fold the RPP row groups: lanes with equal cl end up with the full sum
 #pragma unroll
@@ -561,7 +586,7 @@ __device__ __forceinline__ void pool_chunk(const BagParams& p, const Stage& S, i
             for (int i = 0; i < CPL * EPC; ++i) ss += acc[i] * acc[i];
 #pragma unroll
             for (int o = 1; o < LPR; o <<= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-            const float inv = rsqrtf(ss / (float)p.D + 1e-6f);
+            const float inv = rsqrt_ftz(ss * (1.0f / (LPR * CPL * EPC)) + 1e-6f);  // as in direct::
 #pragma unroll
             for (int i = 0; i < CPL * EPC; ++i) acc[i] *= inv;
         }

@@ -21,11 +21,20 @@ rows = torch.full((n,), ROWS, dtype=torch.int64, device="cuda")
 off, ids = L.synth_bags(n, B, 40, ROWS, 0x1A78)
 dom = L.synth_domains(B, 4, 0x1A78)
 E = torch.empty((B, n, d), dtype=torch.bfloat16, device="cuda")
-pos = torch.randperm(B, device="cuda").to(torch.int32)
 logits = torch.empty((B, 6), device="cuda")
 s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
 net.forward(dom, off, ids, ptrs, rows, torch.bfloat16, logits=logits)  # X0 valid
 net.bucket(dom)
+import ctypes
+POS = os.environ.get("PROBE_POS", "net")
+if POS == "rand":
+    pos = torch.randperm(B, device="cuda").to(torch.int32)
+elif POS == "ident":
+    pos = torch.arange(B, device="cuda", dtype=torch.int32)
+else:
+    order = torch.argsort(dom.long(), stable=True)  # the network's domain-sorted rows (K6)
+    pos = torch.empty(B, dtype=torch.int32, device="cuda")
+    pos[order] = torch.arange(B, dtype=torch.int32, device="cuda")
 
 
 def dense(k):
@@ -55,7 +64,13 @@ def timed(fn):
 
 for _ in range(2):
     dense(2), emb(2)
-print("blocks/SM cap", os.environ.get("LATTICE_BAG_BLOCKS_PER_SM", "default"))
+print("pos", POS, "blocks/SM cap", os.environ.get("LATTICE_BAG_BLOCKS_PER_SM", "default"))
 print("dense alone  %.2f ms" % timed(lambda: dense(K)))
 print("bag alone    %.2f ms" % timed(lambda: emb(K)))
+def full(k):
+    for _ in range(k):
+        net.forward(dom, off, ids, ptrs, rows, torch.bfloat16, logits=logits)
+
+
+print("net forward  %.2f ms" % timed(lambda: full(K)))
 print("both         %.2f ms" % timed(lambda: (dense(K), emb(K))))
