@@ -242,6 +242,58 @@ lattice_status lattice_swish_rn_jvp(int64_t rows, int64_t width, double eps, con
                                     lattice_stream stream);
 
 /* ======================================================================================
+ * JSON-lines impression ingest -- replaces parse_jsonl_records +
+ * record_from_json (serde.hpp:129-166; format SPEC.md:283) for a whole file: content is the
+ * file's bytes in DEVICE memory (kept alive until lattice_jsonl_close). lattice_jsonl_open splits
+ * lines (getline semantics, blank lines skipped), validates every line as nlohmann::json::parse
+ * does, runs record_from_json's checks and sizes the columns (synchronises the stream). The
+ * first bad line (lowest number) -> DATA with "<source>:<line>: <json exception text>", as the
+ * reference's line loop throws (info->error_line / error_kind set; record-level texts are
+ * nlohmann's exactly, parse errors keep its code and column but not its wording). lattice_jsonl_extract writes the columns
+ * into caller buffers sized from info (any group may be null):
+ *   domain / user / ad   unescaped UTF-8 bytes + offsets [records + 1] (user / ad feed
+ *                        lattice_zipper_assign_labels directly)
+ *   ts                   impression_time_ms [records] (get<int64_t>), line [records] (1-based)
+ *   features             per-record entry offsets [records + 1]; per entry key bytes + key
+ *                        offsets [entries + 1] and value (get<double>)
+ *   conversions          the same with int64 values (get<TimestampMs>)
+ * Entries follow nlohmann items(): object members (a repeated key keeps its last value), array
+ * elements keyed "0", "1", ..., a primitive as one entry with the empty key, null as none.
+ * lattice_jsonl_task_columns maps conversion entries onto the zip tasks: conv[r][t] / present
+ * (the Zipper's label inputs, zip_dataset datasets.hpp:219-244).
+ * ==================================================================================== */
+typedef struct lattice_jsonl lattice_jsonl;
+typedef struct {
+    int64_t lines, records;
+    int64_t domain_bytes, user_bytes, ad_bytes;
+    int64_t feature_entries, feature_key_bytes;
+    int64_t conversion_entries, conversion_key_bytes;
+    int64_t error_line;  /* 0, or the 1-based line of the error */
+    int64_t error_kind;  /* 1: DataError ("<source>:<line>: ..."); 2: a number literal overflowing
+                            double -- nlohmann's out_of_range.406, which the reference lets escape
+                            as a plain json::exception (message without context) */
+} lattice_jsonl_info;
+typedef struct {
+    uint8_t* domain;  int64_t* domain_off;
+    uint8_t* user;    int64_t* user_off;
+    uint8_t* ad;      int64_t* ad_off;
+    int64_t* ts;      int64_t* line;
+    int64_t* feature_off;    uint8_t* feature_key;    int64_t* feature_key_off;    double* feature_val;
+    int64_t* conversion_off; uint8_t* conversion_key; int64_t* conversion_key_off; int64_t* conversion_val;
+} lattice_jsonl_columns;
+
+lattice_status lattice_jsonl_open(const uint8_t* content, int64_t bytes, const char* source,
+                                  lattice_jsonl** out, lattice_jsonl_info* info, lattice_stream stream);
+lattice_status lattice_jsonl_extract(lattice_jsonl* h, const lattice_jsonl_columns* columns,
+                                     lattice_stream stream);
+lattice_status lattice_jsonl_task_columns(int64_t records, const int64_t* conversion_off,
+                                          const uint8_t* conversion_key, const int64_t* conversion_key_off,
+                                          const int64_t* conversion_val, int32_t tasks,
+                                          const uint8_t* task_bytes, const int64_t* task_off,
+                                          int64_t* conv, uint8_t* present, lattice_stream stream);
+void lattice_jsonl_close(lattice_jsonl* h);
+
+/* ======================================================================================
  * Post-tower batch reductions. fp64, deterministic (fixed-order
  * per-block partials, no float atomics).
  * lattice_correlation_loss -- replaces lattice::correlation_loss (numerics.hpp:46-78) for

@@ -153,8 +153,36 @@ def load_ref():
                                             _I64, _D, _P, _P, _P]
         lib.ref_window_summary.restype = ctypes.c_int
         lib.ref_window_summary.argtypes = [_I64, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P, _P]
+        if hasattr(lib, "ref_parse_jsonl"):
+            lib.ref_parse_jsonl.restype = ctypes.c_int
+            lib.ref_parse_jsonl.argtypes = [ctypes.c_char_p, _SZ, ctypes.c_char_p, ctypes.POINTER(_P),
+                                            ctypes.POINTER(_SZ)]
+            lib.ref_free.restype = None
+            lib.ref_free.argtypes = [_P]
         _ref = lib
     return _ref
+
+
+def ref_parse_jsonl(content, source="records"):
+    """The reference's parse_jsonl_records (serde.hpp:158-170, via ref_shim) -> (records, None) or
+    (None, error text); the text of an exception that is not a DataError (nlohmann's
+    out_of_range.406 for a number literal overflowing double) is prefixed "exception: ". Records: dicts with domain / user_id / ad_id / impression_time_ms /
+    features {key: float} / conversions {key: int}."""
+    import json
+    import struct
+    lib = load_ref()
+    out, n = _P(), _SZ()
+    rc = lib.ref_parse_jsonl(content, len(content), source.encode(), ctypes.byref(out), ctypes.byref(n))
+    if rc != 0:
+        return None, ("exception: " if rc == 3 else "") + lib.ref_last_error().decode("utf-8", "replace")
+    try:
+        text = ctypes.string_at(out.value, n.value).decode("utf-8")
+    finally:
+        lib.ref_free(out)
+    recs = json.loads(text)
+    for r in recs:
+        r["features"] = {k: struct.unpack("<d", bytes.fromhex(v)[::-1])[0] for k, v in r["features"].items()}
+    return recs, None
 
 
 # ---- thin numpy conveniences ---------------------------------------------------------

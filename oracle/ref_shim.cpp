@@ -6,6 +6,8 @@
 // The reference headers are included under `#define lattice lattice_ref` so they cannot
 // collide with anything named lattice:: elsewhere ("verified by probe").
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -15,6 +17,7 @@
 #include "lattice/datasets.hpp"
 #include "lattice/ktap.hpp"
 #include "lattice/numerics.hpp"
+#include "lattice/serde.hpp"
 #undef lattice
 
 namespace {
@@ -35,6 +38,9 @@ int guarded(F&& f) {
     } catch (const lattice_ref::DataError& e) {
         g_err = e.what();
         return 2;
+    } catch (const std::exception& e) {  // e.g. nlohmann's out_of_range.406 (number overflow)
+        g_err = e.what();
+        return 3;
     }
 }
 }  // namespace
@@ -252,5 +258,40 @@ int ref_student_queries(int64_t entries, int dim, const double* emb, const doubl
         return 0;
     });
 }
+
+// parse_jsonl_records (serde.hpp:158-170) over `content` -> the records as JSON text: [{"domain",
+// "user_id", "ad_id", "impression_time_ms", "features": {key: "<16 hex digits of the double's
+// bits>"}, "conversions": {key: int}}], malloc'ed into *out (ref_free). Status 2 + the DataError
+// text on a bad file.
+int ref_parse_jsonl(const char* content, size_t len, const char* source, char** out, size_t* out_len) {
+    return guarded([&] {
+        const auto recs = lattice_ref::parse_jsonl_records(std::string(content, len), source);
+        nlohmann::json arr = nlohmann::json::array();
+        for (const auto& r : recs) {
+            nlohmann::json j;
+            j["domain"] = r.domain;
+            j["user_id"] = r.user_id;
+            j["ad_id"] = r.ad_id;
+            j["impression_time_ms"] = r.impression_time_ms;
+            j["features"] = nlohmann::json::object();
+            for (const auto& [k, v] : r.values) {
+                uint64_t bits;
+                std::memcpy(&bits, &v, 8);
+                char hex[17];
+                std::snprintf(hex, sizeof hex, "%016llx", (unsigned long long)bits);
+                j["features"][k] = hex;
+            }
+            j["conversions"] = nlohmann::json::object();
+            for (const auto& [k, v] : r.conversions) j["conversions"][k] = v;
+            arr.push_back(std::move(j));
+        }
+        const std::string s = arr.dump();
+        *out = static_cast<char*>(std::malloc(s.size() + 1));
+        std::memcpy(*out, s.data(), s.size() + 1);
+        *out_len = s.size();
+        return 0;
+    });
+}
+void ref_free(void* p) { std::free(p); }
 
 }  // extern "C"

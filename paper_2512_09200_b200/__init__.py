@@ -73,6 +73,19 @@ class PeerBagArgs(ctypes.Structure):
                 ("out_row_stride", _I64), ("normalize", _I32), ("check", _I32)]
 
 
+class JsonlInfo(ctypes.Structure):
+    _fields_ = [(k, _I64) for k in ("lines", "records", "domain_bytes", "user_bytes", "ad_bytes",
+                                    "feature_entries", "feature_key_bytes", "conversion_entries",
+                                    "conversion_key_bytes", "error_line", "error_kind")]
+
+
+class JsonlColumns(ctypes.Structure):
+    _fields_ = [(k, _P) for k in ("domain", "domain_off", "user", "user_off", "ad", "ad_off", "ts", "line",
+                                  "feature_off", "feature_key", "feature_key_off", "feature_val",
+                                  "conversion_off", "conversion_key", "conversion_key_off",
+                                  "conversion_val")]
+
+
 class ObjectiveArgs(ctypes.Structure):
     _fields_ = [("n", _I64), ("tasks", _I32), ("windows", _I32), ("logits", _P), ("window", _P),
                 ("labels", _P), ("eps", ctypes.c_double), ("routed", _P), ("corr", _P), ("counts", _P),
@@ -154,6 +167,12 @@ _sig("lattice_net_set_timing", ctypes.c_int, [_P, _I32])
 _sig("lattice_net_stage_times", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_float), _I32,
                                                ctypes.POINTER(_I32)])
 
+_sig("lattice_jsonl_open", ctypes.c_int, [_P, _I64, ctypes.c_char_p, ctypes.POINTER(_P),
+                                          ctypes.POINTER(JsonlInfo), _P])
+_sig("lattice_jsonl_extract", ctypes.c_int, [_P, ctypes.POINTER(JsonlColumns), _P])
+_sig("lattice_jsonl_task_columns", ctypes.c_int, [_I64, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P])
+_sig("lattice_jsonl_close", None, [_P])
+
 EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_version",
            "lattice_stable_hash", "lattice_zipper_validate", "lattice_zipper_assign_labels",
            "lattice_embedding_bag", "lattice_rownorm", "lattice_fill_tables",
@@ -166,7 +185,9 @@ EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_versio
            "lattice_ipc_open", "lattice_ipc_close", "lattice_peer_barrier", "lattice_net_bucket",
            "lattice_net_buffer", "lattice_correlation_loss", "lattice_window_summary",
            "lattice_routed_objectives", "lattice_merge_dense", "lattice_student_inputs",
-           "lattice_clip_features", "lattice_smooth_labels", "lattice_swish_rn_jvp"]
+           "lattice_clip_features", "lattice_smooth_labels", "lattice_swish_rn_jvp",
+           "lattice_jsonl_open", "lattice_jsonl_extract", "lattice_jsonl_task_columns",
+           "lattice_jsonl_close"]
 
 lib = _lib
 
@@ -387,6 +408,78 @@ def merge_dense(domain, values, src_col, out_width, out_dtype=None, check_errors
     check(_lib.lattice_merge_dense(n, G, md, _p(domain), _p(values), code[values.dtype], _p(src_col), out_width,
                                    code[odt], _p(out), 1 if check_errors else 0, _stream(stream)))
     return out
+
+
+def jsonl_columns(content, source="records", stream=None):
+    """parse_jsonl_records (serde.hpp:158-170) on the GPU: content = the JSONL file as bytes or a
+    uint8 CUDA tensor. Returns a dict of CUDA tensors: domain/user/ad (+ _off [records+1]), ts,
+    line, feature_off/feature_key/feature_key_off/feature_val, conversion_* (lattice_jsonl_extract).
+    A bad line raises DataError("<source>:<line>: ...")."""
+    import torch
+    if isinstance(content, (bytes, bytearray)):
+        buf = torch.frombuffer(bytearray(content), dtype=torch.uint8) if len(content) else torch.empty(0, dtype=torch.uint8)
+        content = buf.cuda()
+    dev = content.device
+    h = _P()
+    info = JsonlInfo()
+    check(_lib.lattice_jsonl_open(_p(content) if content.numel() else None, content.numel(), source.encode(),
+                                  ctypes.byref(h), ctypes.byref(info), _stream(stream)))
+    try:
+        N = info.records
+        u8 = lambda n: torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+        i64 = lambda n: torch.empty(n, dtype=torch.int64, device=dev)
+        out = {"domain": u8(info.domain_bytes), "domain_off": i64(N + 1), "user": u8(info.user_bytes),
+               "user_off": i64(N + 1), "ad": u8(info.ad_bytes), "ad_off": i64(N + 1), "ts": i64(max(N, 1)),
+               "line": i64(max(N, 1)), "feature_off": i64(N + 1), "feature_key": u8(info.feature_key_bytes),
+               "feature_key_off": i64(info.feature_entries + 1),
+               "feature_val": torch.empty(max(info.feature_entries, 1), dtype=torch.float64, device=dev),
+               "conversion_off": i64(N + 1), "conversion_key": u8(info.conversion_key_bytes),
+               "conversion_key_off": i64(info.conversion_entries + 1),
+               "conversion_val": i64(max(info.conversion_entries, 1))}
+        cols = JsonlColumns(**{k: _p(v) for k, v in out.items()})
+        check(_lib.lattice_jsonl_extract(h, ctypes.byref(cols), _stream(stream)))
+    finally:
+        _lib.lattice_jsonl_close(h)
+    out["records"], out["lines"] = N, info.lines
+    return out
+
+
+def jsonl_task_columns(cols, tasks, stream=None):
+    """Conversion entries -> the Zipper's label inputs for `tasks` (names): conv int64 [N, T],
+    present uint8 [N, T] (lattice_jsonl_task_columns)."""
+    import torch
+    N, dev = cols["records"], cols["ts"].device
+    tb = b"".join(t.encode() for t in tasks)
+    toff = [0]
+    for t in tasks:
+        toff.append(toff[-1] + len(t.encode()))
+    tbytes = torch.tensor(list(tb) or [0], dtype=torch.uint8, device=dev)
+    toff = torch.tensor(toff, dtype=torch.int64, device=dev)
+    conv = torch.zeros((max(N, 1), len(tasks)), dtype=torch.int64, device=dev)
+    pres = torch.zeros((max(N, 1), len(tasks)), dtype=torch.uint8, device=dev)
+    check(_lib.lattice_jsonl_task_columns(N, _p(cols["conversion_off"]), _p(cols["conversion_key"]),
+                                          _p(cols["conversion_key_off"]), _p(cols["conversion_val"]), len(tasks),
+                                          _p(tbytes), _p(toff), _p(conv), _p(pres), _stream(stream)))
+    return conv[:N], pres[:N]
+
+
+def jsonl_records(content, source="records"):
+    """parse_jsonl_records as Python records (dicts with the reference's DomainRecord fields;
+    strings decoded as UTF-8), for tests and small files."""
+    c = {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in jsonl_columns(content, source).items()}
+    s = lambda buf, off, i: bytes(buf[off[i]:off[i + 1]]).decode("utf-8")
+    recs = []
+    for r in range(c["records"]):
+        feats = {}
+        for e in range(c["feature_off"][r], c["feature_off"][r + 1]):
+            feats[s(c["feature_key"], c["feature_key_off"], e)] = float(c["feature_val"][e])
+        convs = {}
+        for e in range(c["conversion_off"][r], c["conversion_off"][r + 1]):
+            convs[s(c["conversion_key"], c["conversion_key_off"], e)] = int(c["conversion_val"][e])
+        recs.append({"domain": s(c["domain"], c["domain_off"], r), "user_id": s(c["user"], c["user_off"], r),
+                     "ad_id": s(c["ad"], c["ad_off"], r), "impression_time_ms": int(c["ts"][r]),
+                     "features": feats, "conversions": convs, "line": int(c["line"][r])})
+    return recs
 
 
 def union_schema(declared):
