@@ -259,6 +259,8 @@ lattice_status lattice_swish_rn_jvp(int64_t rows, int64_t width, double eps, con
  *   conversions          the same with int64 values (get<TimestampMs>)
  * Entries follow nlohmann items(): object members (a repeated key keeps its last value), array
  * elements keyed "0", "1", ..., a primitive as one entry with the empty key, null as none.
+ * The handle's workspaces are stream-ordered on the open call's stream: extract on that stream
+ * (or after it), close frees them on it.
  * lattice_jsonl_task_columns maps conversion entries onto the zip tasks: conv[r][t] / present
  * (the Zipper's label inputs, zip_dataset datasets.hpp:219-244).
  * ==================================================================================== */

@@ -784,6 +784,7 @@ struct lattice_jsonl {
     int64_t* rec_line = nullptr;
     int64_t* ts = nullptr;
     int64_t* off[7] = {};  // exclusive-scan offsets [records + 1]: domain, user, ad, fcnt, fkey, ccnt, ckey
+    cudaStream_t stream = nullptr;  // the open call's stream: allocations are ordered on it
     std::vector<void*> allocs;
 };
 
@@ -791,10 +792,12 @@ namespace {
 
 using lat::set_error;
 
+// stream-ordered pool allocations: an ingest call allocates ~30 arrays, and plain cudaMalloc /
+// cudaFree (which synchronises the device) cost more than the kernels themselves
 template <typename T>
 lattice_status jl_alloc(lattice_jsonl* h, T** p, int64_t count) {
     void* q = nullptr;
-    LAT_CUDA(cudaMalloc(&q, (size_t)(count > 0 ? count : 1) * sizeof(T)));
+    LAT_CUDA(cudaMallocAsync(&q, (size_t)(count > 0 ? count : 1) * sizeof(T), h->stream));
     h->allocs.push_back(q);
     *p = static_cast<T*>(q);
     return LATTICE_OK;
@@ -866,6 +869,7 @@ lattice_status lattice_jsonl_open(const uint8_t* content, int64_t bytes, const c
     *info = lattice_jsonl_info{};
     cudaStream_t st = (cudaStream_t)stream;
     lattice_jsonl* h = new lattice_jsonl();
+    h->stream = st;
     h->content = content;
     h->bytes = bytes;
     auto fail = [&](lattice_status s) {
@@ -1078,7 +1082,7 @@ lattice_status lattice_jsonl_task_columns(int64_t records, const int64_t* conver
 
 void lattice_jsonl_close(lattice_jsonl* h) {
     if (!h) return;
-    for (void* p : h->allocs) cudaFree(p);
+    for (void* p : h->allocs) cudaFreeAsync(p, h->stream);
     delete h;
 }
 

@@ -11,6 +11,7 @@
 #include "lattice/datasets.hpp"
 #include "lattice/network.hpp"
 #include "lattice/numerics.hpp"
+#include "lattice/serde.hpp"
 
 using namespace lattice;
 
@@ -263,6 +264,38 @@ static void network_smoke() {
     CHECK_THROWS_AS(Network{bad}, UsageError);
 }
 
+// serde.hpp:158 parse_jsonl_records through the GPU parser: the SPEC.md:283 record format, then
+// zip_dataset on the parsed records (the CLI's run_zip path, lattice_cli.cpp:115-139)
+static void jsonl_examples() {
+    const std::string file =
+        "{\"domain\":\"shop\",\"user_id\":\"u1\",\"ad_id\":\"a1\",\"impression_time_ms\":0,"
+        "\"features\":{\"age\":31,\"ctr\":0.0125},\"conversions\":{\"cvr\":7200000}}\n"
+        "\n"
+        "{\"domain\":\"shop\",\"user_id\":\"u\\u00e9\",\"ad_id\":\"a2\",\"impression_time_ms\":5,"
+        "\"features\":{\"age\":1,\"age\":2}}\r\n";
+    const auto recs = parse_jsonl_records(file, "log.jsonl");
+    CHECK(recs.size() == 2);
+    CHECK(recs[0].domain == "shop" && recs[0].user_id == "u1" && recs[0].impression_time_ms == 0);
+    CHECK(recs[0].values.at("age") == 31.0 && recs[0].values.at("ctr") == 0.0125);
+    CHECK(recs[0].conversions.at("cvr") == 7200000);
+    CHECK(recs[1].user_id == "u\xc3\xa9" && recs[1].values.size() == 1 && recs[1].values.at("age") == 2.0);
+    const auto cfg = ZipperConfig::create({{"90min", 5400000}, {"1d", 86400000}}, {0.5, 0.5}, Seed{7});
+    const auto z = zip_dataset(recs, {"cvr"}, cfg);
+    CHECK(z.records[0].label(0, 0, 2) == 0 && z.records[0].label(0, 1, 2) == 1);
+    CHECK_THROWS_AS(parse_jsonl_records("{\"domain\":1}\n", "x"), DataError);
+    CHECK_THROWS_AS(parse_jsonl_records("{}\n{oops\n", "x"), DataError);
+    CHECK_THROWS_AS(parse_jsonl_records("[1e999]\n", "x"), JsonOutOfRange);
+    try {
+        parse_jsonl_records("{\"domain\":\"d\",\"user_id\":\"u\",\"ad_id\":\"a\",\"impression_time_ms\":1}\n"
+                            "{\"domain\":\"d\",\"ad_id\":\"a\",\"impression_time_ms\":1}\n",
+                            "log.jsonl");
+        CHECK(false && "expected DataError");
+    } catch (const DataError& e) {
+        CHECK(std::string(e.what()) == "log.jsonl:2: [json.exception.out_of_range.403] key 'user_id' not found");
+    }
+    CHECK(parse_jsonl_records("", "empty").empty());
+}
+
 int main() {
     core_goldens();
     numerics_examples();
@@ -270,6 +303,7 @@ int main() {
     numerics_more();
     merge_and_summary();
     network_smoke();
+    jsonl_examples();
     std::printf("drop-in: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail;
 }
