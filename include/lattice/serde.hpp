@@ -7,10 +7,12 @@
 // a number literal that overflows double throws the reference's un-wrapped
 // "[json.exception.out_of_range.406] ..." text as JsonOutOfRange (not a DataError, as in the
 // reference, where nlohmann's out_of_range escapes parse_json's parse_error catch).
-// parse_jsonl_columns is the columnar form the Zipper consumes without building records.
+// parse_jsonl_columns is the columnar form the Zipper consumes without building records;
+// dataset_from_records (:172-194) groups one file's records into a DomainDataset.
 
 #include <cstdint>
 #include <map>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -107,6 +109,28 @@ inline std::vector<DomainRecord> parse_jsonl_records(const std::string& content,
                 c.conversion_val[static_cast<std::size_t>(e)];
     }
     return records;
+}
+
+// serde.hpp:172-194 -- one JSONL file = one domain's dataset: every record carries the first
+// record's domain tag; the schema is the first-seen union of feature names (records in file
+// order, names in each record's map order). Host-side string work on the parsed records.
+inline DomainDataset dataset_from_records(std::vector<DomainRecord> records, const std::string& source) {
+    if (records.empty()) throw DataError(source + ": no records");
+    const std::string& dom = records.front().domain;
+    std::vector<FeatureId> names;
+    std::set<FeatureId> known;
+    for (const DomainRecord& r : records) {
+        if (r.domain != dom)
+            throw DataError(source + ": mixed domains '" + dom + "' and '" + r.domain + "' in one file");
+        for (const auto& kv : r.values)
+            if (known.insert(kv.first).second) names.push_back(kv.first);
+    }
+    try {
+        DatasetSchema schema = DatasetSchema::create(dom, std::move(names));
+        return DomainDataset{std::move(schema), std::move(records)};
+    } catch (const UsageError& e) {  // the values came from a file: a data error (serde.hpp:54)
+        throw DataError(source + ": " + e.what());
+    }
 }
 
 }  // namespace lattice

@@ -286,6 +286,8 @@ __device__ bool scan_literal(const uint8_t* s, uint32_t n, uint32_t& i, uint8_t&
 }
 
 // Validates one value from s[i] (after whitespace); i ends after it. Returns 0 or a P_* reason.
+// OVF: also reject float literals that overflow (pass 1; later passes walk validated lines).
+template <bool OVF = true>
 __device__ int skip_value(const uint8_t* s, uint32_t n, uint32_t& i, uint8_t& type) {
     uint32_t stk[kMaxDepth / 32];  // bit per level: 1 = object
     int depth = 0;
@@ -315,7 +317,7 @@ __device__ int skip_value(const uint8_t* s, uint32_t n, uint32_t& i, uint8_t& ty
             if (!scan_number(s, n, i, t)) return P_NUMBER;
             // nlohmann's parser rejects a float literal that overflows (the SAX number_float
             // callback, before anything after the token is looked at); i is left at the token
-            if (t == T_FLT && isinf(dec::parse_double(s + tok, s + i))) {
+            if (OVF && t == T_FLT && isinf(dec::parse_double(s + tok, s + i))) {
                 i = tok;
                 return P_OVERFLOW;
             }
@@ -544,7 +546,7 @@ __device__ void for_entries(const uint8_t* s, uint32_t n, uint32_t vpos, Fn&& fn
         }
         const uint32_t vs = i;
         uint8_t vt;
-        skip_value(s, n, i, vt);
+        skip_value<false>(s, n, i, vt);
         bool last = true;
         if (t == T_OBJ) {  // a later member with the same key replaces this one
             uint32_t j = i;
@@ -562,7 +564,7 @@ __device__ void for_entries(const uint8_t* s, uint32_t n, uint32_t vpos, Fn&& fn
                 while (is_ws(s[j])) ++j;
                 ++j;
                 uint8_t t2;
-                skip_value(s, n, j, t2);
+                skip_value<false>(s, n, j, t2);
             }
         }
         if (last) fn(t == T_OBJ ? 0 : 1, kq, idx, vs);
@@ -868,6 +870,19 @@ lattice_status lattice_jsonl_open(const uint8_t* content, int64_t bytes, const c
     *out = nullptr;
     *info = lattice_jsonl_info{};
     cudaStream_t st = (cudaStream_t)stream;
+    {  // keep freed pool memory for the next call (the default threshold 0 returns it to the
+       // driver at every synchronisation, and re-allocating costs like cudaMalloc)
+        static bool pool_set = false;
+        if (!pool_set) {
+            int dev = 0;
+            cudaMemPool_t pool;
+            if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t keep = 1ull << 32;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            pool_set = true;
+        }
+    }
     lattice_jsonl* h = new lattice_jsonl();
     h->stream = st;
     h->content = content;

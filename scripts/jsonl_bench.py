@@ -24,7 +24,7 @@ dev = host.cuda()
 for _ in range(2):
     L.jsonl_columns(dev)
 torch.cuda.synchronize()
-K = 5
+K = 10
 t0 = time.perf_counter()
 for _ in range(K):
     cols = L.jsonl_columns(dev)

@@ -294,6 +294,12 @@ static void jsonl_examples() {
         CHECK(std::string(e.what()) == "log.jsonl:2: [json.exception.out_of_range.403] key 'user_id' not found");
     }
     CHECK(parse_jsonl_records("", "empty").empty());
+    const auto ds = dataset_from_records(recs, "log.jsonl");
+    CHECK(ds.schema.domain == "shop" && ds.schema.features == std::vector<FeatureId>({"age", "ctr"}));
+    auto mixed = recs;
+    mixed[1].domain = "news";
+    CHECK_THROWS_AS(dataset_from_records(mixed, "log.jsonl"), DataError);
+    CHECK_THROWS_AS(dataset_from_records({}, "log.jsonl"), DataError);
 }
 
 int main() {
