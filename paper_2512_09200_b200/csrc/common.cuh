@@ -118,6 +118,22 @@ __host__ __device__ __forceinline__ int weight_shift(int64_t fan_in) {
     return 7 + lg / 2;
 }
 
+// ---- 32-byte global accesses (sm_100: LDG/STG .ENL2.256) ----------------------------------
+// Epilogues where a thread owns an output row put consecutive lanes 32 rows apart, so each
+// 16-byte access fills half an L2 sector; 32 bytes per lane move whole sectors with half the
+// instructions. Callers check 32-byte alignment.
+__device__ __forceinline__ bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
+__device__ __forceinline__ void st_global_256(void* p, uint4 a, uint4 b) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+                 "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                 : "memory");
+}
+__device__ __forceinline__ void ld_global_256(const void* p, uint4& a, uint4& b) {
+    asm volatile("ld.global.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                 : "l"(p));
+}
+
 // ---- numeric helpers ----------------------------------------------------------------------
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -60,6 +60,19 @@ struct Store<__nv_bfloat16> {
         *reinterpret_cast<uint4*>(dst) = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
                                                     pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
     }
+    // 16 consecutive values -> one 32-byte store when aligned (a whole L2 sector per lane)
+    __device__ static void row16(__nv_bfloat16* dst, const float* v) {
+        const uint4 a = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                                   pack_bf16x2(v[6], v[7]));
+        const uint4 b = make_uint4(pack_bf16x2(v[8], v[9]), pack_bf16x2(v[10], v[11]), pack_bf16x2(v[12], v[13]),
+                                   pack_bf16x2(v[14], v[15]));
+        if (aligned32(dst)) {
+            st_global_256(dst, a, b);
+        } else {
+            reinterpret_cast<uint4*>(dst)[0] = a;
+            reinterpret_cast<uint4*>(dst)[1] = b;
+        }
+    }
     __device__ static void one(__nv_bfloat16* dst, float v) { *dst = __float2bfloat16_rn(v); }
     // unpack 8 residual values starting at element e of a packed row held in uint4 res[]
     __device__ static void unpack8(const uint4* res, int e, float* out) {
@@ -77,6 +90,10 @@ struct Store<float> {
     __device__ static void row8(float* dst, const float* v) {
         reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
         reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+    __device__ static void row16(float* dst, const float* v) {
+        row8(dst, v);
+        row8(dst + 8, v + 8);
     }
     __device__ static void one(float* dst, float v) { *dst = v; }
     __device__ static void unpack8(const uint4* res, int e, float* out) {
@@ -337,12 +354,13 @@ __global__ void __launch_bounds__(kResThreads, 1)
                     float v[32];
                     tc::tmem_ld32(t_L + c_lo + c, v);
 #pragma unroll
-                    for (int j = 0; j < 32; j += 8) {
-                        float r8[8];
-                        Store<T>::unpack8(res, c + j, r8);
+                    for (int j = 0; j < 32; j += 16) {  // 16 values: one 32-byte store (bf16)
+                        float r16[16];
+                        Store<T>::unpack8(res, c + j, r16);
+                        Store<T>::unpack8(res, c + j + 8, r16 + 8);
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) r8[i] = (v[j + i] + r8[i]) * inv;
-                        if (live) Store<T>::row8(dst + c + j, r8);
+                        for (int i = 0; i < 16; ++i) r16[i] = (v[j + i] + r16[i]) * inv;
+                        if (live) Store<T>::row16(dst + c + j, r16);
                     }
                 }
             }
@@ -401,7 +419,17 @@ __global__ void __launch_bounds__(kResThreads, 1)
                         if (!small_k) tc::tmem_ld32(t_F + mt * kpad + c0, v[mt]);
                         if (r >= p.n) continue;
                         T* dst = static_cast<T*>(p.Fout) + b * (int64_t)p.n * p.k + (int64_t)r * p.k + c0;
-                        if ((p.k & 7) == 0) {
+                        if ((p.k & 15) == 0) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 16) {
+                                if (c0 + j < p.k) {
+                                    float o[16];
+#pragma unroll
+                                    for (int i = 0; i < 16; ++i) o[i] = v[mt][j + i] * inv;
+                                    Store<T>::row16(dst + j, o);
+                                }
+                            }
+                        } else if ((p.k & 7) == 0) {
 #pragma unroll
                             for (int j = 0; j < 32; j += 8) {
                                 if (c0 + j < p.k) {

@@ -17,6 +17,8 @@
 namespace lat {
 namespace gemm {
 
+__device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
+
 constexpr int BN = 256;
 constexpr int kRasterGroup = 16;
 
@@ -26,7 +28,15 @@ constexpr int kRasterGroup = 16;
 __device__ __forceinline__ void store_row32(const Params& p, int64_t m, int n, const float* v) {
     if (p.out_bf16) {
         __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.C) + m * p.ldc + n;
-        if (n + 32 <= p.N) {
+        if (n + 32 <= p.N && aligned32(dst)) {  // whole sectors: two 32-byte stores
+#pragma unroll
+            for (int j = 0; j < 32; j += 16)
+                st_global_256(dst + j,
+                              make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
+                                         pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7])),
+                              make_uint4(pack_bf16x2(v[j + 8], v[j + 9]), pack_bf16x2(v[j + 10], v[j + 11]),
+                                         pack_bf16x2(v[j + 12], v[j + 13]), pack_bf16x2(v[j + 14], v[j + 15])));
+        } else if (n + 32 <= p.N) {
 #pragma unroll
             for (int j = 0; j < 32; j += 8)
                 *reinterpret_cast<uint4*>(dst + j) =
@@ -39,7 +49,12 @@ __device__ __forceinline__ void store_row32(const Params& p, int64_t m, int n, c
         }
     } else {
         float* dst = static_cast<float*>(p.C) + m * p.ldc + n;
-        if (n + 32 <= p.N) {
+        if (n + 32 <= p.N && aligned32(dst)) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8)
+                st_global_256(dst + j, make_uint4(f2u(v[j]), f2u(v[j + 1]), f2u(v[j + 2]), f2u(v[j + 3])),
+                              make_uint4(f2u(v[j + 4]), f2u(v[j + 5]), f2u(v[j + 6]), f2u(v[j + 7])));
+        } else if (n + 32 <= p.N) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4)
                 *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
@@ -84,12 +99,19 @@ __device__ __forceinline__ void resid_norm_group(const Params& p, uint32_t taddr
     if (!valid) return;
     if (p.out_bf16) {
         const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(p.resid) + m * p.ldr + n;
+        const bool wide = aligned32(r);  // 32-byte loads: whole sectors per lane
 #pragma unroll
-        for (int c = 0; c < GROUP; c += 8) {
-            const uint4 q = *reinterpret_cast<const uint4*>(r + c);
-            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        for (int c = 0; c < GROUP; c += 16) {
+            uint4 q0, q1;
+            if (wide) {
+                ld_global_256(r + c, q0, q1);
+            } else {
+                q0 = *reinterpret_cast<const uint4*>(r + c);
+                q1 = *reinterpret_cast<const uint4*>(r + c + 8);
+            }
+            const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < 8; ++i) {
                 v[c + 2 * i] += bf16_lo(w[i]);
                 v[c + 2 * i + 1] += bf16_hi(w[i]);
             }
