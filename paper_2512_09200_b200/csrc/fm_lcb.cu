@@ -648,16 +648,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc::tmem_ld32(t_L + c, v);
                     if (live) {
 #pragma unroll
-                        for (int j = 0; j < 32; j += 8) {
-                            const uint4 r = *reinterpret_cast<const uint4*>(sX + ((c + j) / 64) * g.xpanel +
-                                                                            swz<2>(xr, (c + j) & 63));
-                            const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-                            uint32_t o[4];
+                        for (int j = 0; j < 32; j += 16) {  // 16 values per 32-byte store
+                            uint32_t o[8];
 #pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                o[k] = pack_bf16x2((v[j + 2 * k] + bf16_lo(w[k])) * inv,
-                                                   (v[j + 2 * k + 1] + bf16_hi(w[k])) * inv);
-                            *reinterpret_cast<uint4*>(dst + c + j) = make_uint4(o[0], o[1], o[2], o[3]);
+                            for (int hh = 0; hh < 2; ++hh) {
+                                const int jj = j + 8 * hh;
+                                const uint4 r = *reinterpret_cast<const uint4*>(sX + ((c + jj) / 64) * g.xpanel +
+                                                                                swz<2>(xr, (c + jj) & 63));
+                                const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    o[4 * hh + k] = pack_bf16x2((v[jj + 2 * k] + bf16_lo(w[k])) * inv,
+                                                                (v[jj + 2 * k + 1] + bf16_hi(w[k])) * inv);
+                            }
+                            st_global_256(dst + c + j, make_uint4(o[0], o[1], o[2], o[3]),
+                                          make_uint4(o[4], o[5], o[6], o[7]));
                         }
                     }
                 }
@@ -704,13 +709,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.Fout) + b * (int64_t)p.n * p.k +
                                              (int64_t)r * p.k + c0;
                         if ((p.k & 15) == 0) {
-                            float o[8];
+                            float o[16];
 #pragma unroll
-                            for (int j = 0; j < 16; j += 8) {
-#pragma unroll
-                                for (int k = 0; k < 8; ++k) o[k] = v[j + k] * inv;
-                                Store<__nv_bfloat16>::row8(dst + j, o);
-                            }
+                            for (int k = 0; k < 16; ++k) o[k] = v[k] * inv;
+                            Store<__nv_bfloat16>::row16(dst, o);
                         } else {
 #pragma unroll
                             for (int j = 0; j < 16; ++j)
