@@ -1,4 +1,4 @@
-"""World-size-2/3 gloo test (CPU) of the peer-memory sharded embedding host logic
+"""World-size-2/3/8 gloo test (CPU) of the peer-memory sharded embedding host logic
 (paper_2512_09200_b200/peer.py): every shared buffer is exported once per rank, the pointer
 table a rank hands to the owner kernel holds its own pointer at its own index and the peers'
 IPC-mapped pointers elsewhere, and one step issues bucket -> barrier -> owner kernel ->
@@ -91,7 +91,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_peer_exchange_pointer_tables(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
