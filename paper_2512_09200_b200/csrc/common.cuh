@@ -25,6 +25,12 @@ lattice_status check_cuda(cudaError_t e, const char* what);
         if (!(cond)) return ::lat::set_error(LATTICE_USAGE, (msg));                 \
     } while (0)
 
+// embedding_bag.cu: the stable domain bucketing behind lattice_domain_bucket, with a caller-owned
+// workspace of bucket_workspace(B, G) int32 (lattice_net keeps one: no allocation per step)
+int64_t bucket_workspace(int64_t B, int G);
+lattice_status bucket_ws(int64_t B, int G, const int32_t* dom, int32_t* pos, int32_t* order, int32_t* seg,
+                         int32_t* ws, cudaStream_t stream);
+
 inline int num_sms() {
     static int n = 0;
     if (!n) {

@@ -837,64 +837,84 @@ __global__ void synth_dom_kernel(int64_t n, int G, uint64_t seed, int32_t* dom) 
 constexpr int kBucketThreads = 1024;
 constexpr int kMaxDomains = 32;
 
-__global__ void __launch_bounds__(kBucketThreads) bucket_kernel(int64_t B, int G,
-                                                                const int32_t* __restrict__ dom,
-                                                                int32_t* __restrict__ pos,
-                                                                int32_t* __restrict__ order,
-                                                                int32_t* __restrict__ seg) {
-    extern __shared__ int32_t cnt[];  // [G][1024]
+// Stable counting sort of the batch by domain in three short kernels (coalesced, one thread per
+// sample): per-block domain histograms -> one block scans them into per-(block, domain) bases and
+// the segment starts -> every sample's rank among the earlier same-domain samples of its block
+// (warp match + per-warp prefix). A domain outside [0, G) counts as domain 0.
+__device__ __forceinline__ int bucket_domain(const int32_t* __restrict__ dom, int64_t B, int G, int64_t b) {
+    if (b >= B) return G;  // padding lane: a class of its own, never stored
+    const int g = dom[b];
+    return g >= 0 && g < G ? g : 0;
+}
+
+__global__ void __launch_bounds__(kBucketThreads) bucket_hist_kernel(int64_t B, int G, const int32_t* __restrict__ dom,
+                                                                     int32_t* __restrict__ hist) {
+    __shared__ int32_t h[kMaxDomains];
+    if (threadIdx.x < kMaxDomains) h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t b = (int64_t)blockIdx.x * kBucketThreads + threadIdx.x;
+    const int g = bucket_domain(dom, B, G, b);
+    // one atomic per (warp, domain)
+    const unsigned same = __match_any_sync(0xffffffffu, g);
+    if (g < G && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&h[g], __popc(same));
+    __syncthreads();
+    if (threadIdx.x < G) hist[(int64_t)blockIdx.x * G + threadIdx.x] = h[threadIdx.x];
+}
+
+// one block: base[blk][g] = samples of domain g in blocks < blk; seg[g] = first row of domain g
+__global__ void __launch_bounds__(kBucketThreads) bucket_scan_kernel(int64_t nblk, int G, const int32_t* __restrict__ hist,
+                                                                     int32_t* __restrict__ base, int32_t* __restrict__ seg) {
     __shared__ int32_t tot[kMaxDomains + 1];
-    __shared__ int32_t warp_tot[32];
-    const int t = threadIdx.x;
-    const int64_t per = (B + kBucketThreads - 1) / kBucketThreads;
-    const int64_t lo = (int64_t)t * per < B ? (int64_t)t * per : B;
-    const int64_t hi = lo + per < B ? lo + per : B;
-    for (int g = 0; g < G; ++g) cnt[g * kBucketThreads + t] = 0;
-    for (int64_t b = lo; b < hi; ++b) {
-        const int g = dom[b];
-        cnt[(g >= 0 && g < G ? g : 0) * kBucketThreads + t]++;
+    const int g = threadIdx.x;
+    if (g < G) {
+        int run = 0;
+        for (int64_t k = 0; k < nblk; ++k) {
+            const int c = hist[k * G + g];
+            base[k * G + g] = run;
+            run += c;
+        }
+        tot[g] = run;
     }
     __syncthreads();
-    // exclusive scan of cnt[g][*] for every g
-    for (int g = 0; g < G; ++g) {
-        int v = cnt[g * kBucketThreads + t];
-        int incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int n = __shfl_up_sync(0xffffffffu, incl, o);
-            if ((t & 31) >= o) incl += n;
-        }
-        if ((t & 31) == 31) warp_tot[t >> 5] = incl;
-        __syncthreads();
-        if (t < 32) {
-            int w = warp_tot[t], wi = w;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int n = __shfl_up_sync(0xffffffffu, wi, o);
-                if (t >= o) wi += n;
-            }
-            warp_tot[t] = wi - w;
-            if (t == 31) tot[g] = wi;
-        }
-        __syncthreads();
-        cnt[g * kBucketThreads + t] = incl - v + warp_tot[t >> 5];
-        __syncthreads();
-    }
-    if (t == 0) {
+    if (threadIdx.x == 0) {
         int run = 0;
-        for (int g = 0; g < G; ++g) {
-            const int c = tot[g];
-            tot[g] = run;
-            seg[g] = run;
+        for (int q = 0; q < G; ++q) {
+            const int c = tot[q];
+            seg[q] = run;
+            tot[q] = run;
             run += c;
         }
         seg[G] = run;
     }
+}
+
+__global__ void __launch_bounds__(kBucketThreads) bucket_rank_kernel(int64_t B, int G, const int32_t* __restrict__ dom,
+                                                                     const int32_t* __restrict__ base,
+                                                                     const int32_t* __restrict__ seg,
+                                                                     int32_t* __restrict__ pos, int32_t* __restrict__ order) {
+    __shared__ int32_t wcnt[kMaxDomains][32];  // [domain][warp] -> exclusive prefix over warps
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < kMaxDomains * 32; i += kBucketThreads) (&wcnt[0][0])[i] = 0;
     __syncthreads();
-    for (int64_t b = lo; b < hi; ++b) {
-        int g = dom[b];
-        g = (g >= 0 && g < G) ? g : 0;
-        const int p = tot[g] + cnt[g * kBucketThreads + t]++;
+    const int64_t b = (int64_t)blockIdx.x * kBucketThreads + threadIdx.x;
+    const int g = bucket_domain(dom, B, G, b);
+    const unsigned same = __match_any_sync(0xffffffffu, g);
+    const int rank = __popc(same & ((1u << lane) - 1u));
+    if (g < G && lane == __ffs(same) - 1) wcnt[g][warp] = __popc(same);
+    __syncthreads();
+    if (warp < G) {  // warp q scans domain q's 32 per-warp counts
+        const int v = wcnt[warp][lane];
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int n = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += n;
+        }
+        wcnt[warp][lane] = incl - v;
+    }
+    __syncthreads();
+    if (g < G) {
+        const int p = seg[g] + base[(int64_t)blockIdx.x * G + g] + wcnt[g][warp] + rank;
         pos[b] = p;
         order[p] = (int32_t)b;
     }
@@ -939,6 +959,20 @@ lattice_status sync_err(unsigned long long* err, cudaStream_t st, unsigned long 
 }
 
 }  // namespace
+// lattice_domain_bucket with a caller-owned workspace of bucket_workspace(B, G) int32
+// (hist | base per block); lattice_net keeps one so a step does no allocation
+int64_t bucket_workspace(int64_t B, int G) { return 2 * ((B + kBucketThreads - 1) / kBucketThreads) * G; }
+
+lattice_status bucket_ws(int64_t B, int G, const int32_t* dom, int32_t* pos, int32_t* order, int32_t* seg,
+                         int32_t* ws, cudaStream_t stream) {
+    const int64_t nblk = (B + kBucketThreads - 1) / kBucketThreads;
+    bucket_hist_kernel<<<(unsigned)nblk, kBucketThreads, 0, stream>>>(B, G, dom, ws);
+    bucket_scan_kernel<<<1, kBucketThreads, 0, stream>>>(nblk, G, ws, ws + nblk * G, seg);
+    bucket_rank_kernel<<<(unsigned)nblk, kBucketThreads, 0, stream>>>(B, G, dom, ws + nblk * G, seg, pos, order);
+    LAT_CUDA(cudaGetLastError());
+    return LATTICE_OK;
+}
+
 }  // namespace lat
 
 extern "C" {
@@ -1145,17 +1179,15 @@ lattice_status lattice_domain_bucket(int64_t B, int32_t G, const int32_t* dom, i
     using namespace lat;
     LAT_REQUIRE(B >= 0 && B < (1ll << 31) && G > 0 && G <= kMaxDomains, "domain_bucket: bad sizes");
     LAT_REQUIRE(dom && pos && order && seg, "domain_bucket: null pointer");
-    const size_t smem = sizeof(int32_t) * G * kBucketThreads;
-    static bool attr = false;
-    if (!attr) {
-        LAT_CUDA(cudaFuncSetAttribute(bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(sizeof(int32_t) * kMaxDomains * kBucketThreads)));
-        attr = true;
+    if (B == 0) {
+        LAT_CUDA(cudaMemsetAsync(seg, 0, sizeof(int32_t) * (G + 1), stream));
+        return LATTICE_OK;
     }
-    LAT_REQUIRE(smem <= 227 * 1024, "domain_bucket: too many domains");
-    bucket_kernel<<<1, kBucketThreads, smem, stream>>>(B, G, dom, pos, order, seg);
-    LAT_CUDA(cudaGetLastError());
-    return LATTICE_OK;
+    int32_t* ws = nullptr;
+    LAT_CUDA(cudaMallocAsync(&ws, sizeof(int32_t) * bucket_workspace(B, G), stream));
+    const lattice_status st = bucket_ws(B, G, dom, pos, order, seg, ws, stream);
+    cudaFreeAsync(ws, stream);
+    return st;
 }
 
 lattice_status lattice_rownorm(int32_t mode, int64_t rows, int64_t width, double eps, const float* x,

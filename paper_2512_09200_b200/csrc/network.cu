@@ -119,7 +119,7 @@ struct lattice_net {
     float* rowpart = nullptr;  // swish GEMMs (CTA-pair kernel): row-statistics exchange
     int* rowcnt = nullptr;
     // workspace
-    int32_t *pos = nullptr, *order = nullptr, *seg = nullptr;
+    int32_t *pos = nullptr, *order = nullptr, *seg = nullptr, *bucket_ws = nullptr;
     int4* tiles = nullptr;
     int* n_tiles = nullptr;
     void* X[2] = {nullptr, nullptr};
@@ -390,6 +390,7 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
     NET_TRY(dalloc(net, &net->pos, (size_t)Bm));
     NET_TRY(dalloc(net, &net->order, (size_t)Bm));
     NET_TRY(dalloc(net, &net->seg, (size_t)c.domains + 1));
+    NET_TRY(dalloc(net, &net->bucket_ws, (size_t)lat::bucket_workspace(Bm, c.domains)));
     NET_TRY(dalloc(net, &net->tiles, (size_t)((Bm + 127) / 128 + c.domains)));
     NET_TRY(dalloc(net, &net->n_tiles, 1));
     NET_TRY(dalloc_bytes(net, &net->X[0], es * (size_t)Bm * nd));
@@ -460,7 +461,8 @@ lattice_status lattice_net_bucket(lattice_net* net, int64_t batch, const int32_t
     LAT_REQUIRE(net != nullptr && domain != nullptr, "lattice_net_bucket: null argument");
     LAT_REQUIRE(batch >= 0 && batch <= net->cfg.max_batch, "lattice_net_bucket: batch exceeds max_batch");
     if (batch == 0) return LATTICE_OK;
-    lattice_status s = lattice_domain_bucket(batch, net->cfg.domains, domain, net->pos, net->order, net->seg, stream);
+    lattice_status s = bucket_ws(batch, net->cfg.domains, domain, net->pos, net->order, net->seg, net->bucket_ws,
+                                 (cudaStream_t)stream);
     if (s != LATTICE_OK) return s;
     tiles_kernel<<<1, 256, 0, stream>>>(net->seg, net->cfg.domains, net->tiles, net->n_tiles);
     LAT_CUDA(cudaGetLastError());

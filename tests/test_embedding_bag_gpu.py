@@ -127,7 +127,7 @@ def test_long_bags_and_empty_batch():
 
 def test_domain_bucket_is_stable_sort():
     import paper_2512_09200_b200 as L
-    for B, G in [(1, 1), (1000, 4), (65536, 16), (32768, 3)]:
+    for B, G in [(1, 1), (1000, 4), (65536, 16), (32768, 3), (5000, 32), (1 << 20, 7), (1023, 2), (1025, 2)]:
         dom = L.synth_domains(B, G, 99)
         pos, order, seg = L.domain_bucket(dom, G)
         d = dom.cpu().numpy()
