@@ -530,7 +530,9 @@ def run_mid(args, rank, world, local):
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
 
-    launches = 3 + c["blocks"] * (1 + len(c["mlp"]) - 1) + 1
+    # per step: domain bucketing (histogram, block scan, ranks) + tiles + bag, then per block the
+    # FM/LCB kernel and one GEMM per MLP layer, then the grouped tower
+    launches = 5 + c["blocks"] * (1 + len(c["mlp"]) - 1) + 1
     if peer:
         pb.check()
         launches += 2  # two barrier kernels (the bag slot above is the owner kernel)
