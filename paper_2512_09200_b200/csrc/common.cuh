@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "../../include/lattice_b200.h"
@@ -30,6 +31,18 @@ lattice_status check_cuda(cudaError_t e, const char* what);
 int64_t bucket_workspace(int64_t B, int G);
 lattice_status bucket_ws(int64_t B, int G, const int32_t* dom, int32_t* pos, int32_t* order, int32_t* seg,
                          int32_t* ws, cudaStream_t stream);
+
+// Programmatic dependent launch for the dense chain (FM/LCB and GEMM kernels); LATTICE_PDL=0
+// launches them with plain stream ordering (A/B runs). The kernels call griddepcontrol.wait
+// either way, which is a no-op without the launch attribute.
+inline bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("LATTICE_PDL");
+        v = e ? (std::atoi(e) != 0) : 1;
+    }
+    return v == 1;
+}
 
 inline int num_sms() {
     static int n = 0;

@@ -192,6 +192,10 @@ __global__ void __launch_bounds__(kResThreads, 1)
     tc::fence_after();
     const uint32_t tmem = *tmem_slot;
     const int m_tiles = (npad + 127) / 128;
+    // PDL: barriers, TMEM and the resident weights are set up while the preceding kernel drains;
+    // X, Fout and Xout are touched only after griddep_wait
+    if (!(warp == 0 && lane == 0)) tc::griddep_wait();
+    tc::griddep_launch_dependents();
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer
@@ -200,6 +204,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
                 tc::tma_load_2d(sWL + pn * g.wlpanel, &tmWL, w_full, pn * EP, 0);
                 tc::tma_load_2d(sYT + pn * g.ytpanel, &tmYT, w_full, pn * EP, 0);
             }
+            tc::griddep_wait();
             int it = 0;
             for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
                 const int st = it & 1;
@@ -529,11 +534,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t t_Pb = tmem, t_Lb = tmem + 64, t_Fb = tmem + 64 + 128 * 2;
+    if (!(warp == 0 && lane == 0)) tc::griddep_wait();  // PDL, as in fm_lcb_kernel
+    tc::griddep_launch_dependents();
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer: X (4 boxes), then the W_L panel stream
             tc::mbar_expect_tx(w_full, g.ytpanel * g.panels_n);
             for (int pn = 0; pn < g.panels_n; ++pn) tc::tma_load_2d(sYT + pn * g.ytpanel, &tmYT, w_full, pn * 64, 0);
+            tc::griddep_wait();
             int it = 0, gw = 0;
             for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
                 tc::mbar_wait(x_empty, (it & 1) ^ 1);
@@ -812,9 +820,25 @@ lattice_status launch_t(const Plan& pl, cudaStream_t st) {
     }
     const int grid = (int)(pl.p.B < num_sms() ? pl.p.B : num_sms());
     if (grid <= 0) return LATTICE_OK;
-    fm_lcb_kernel<T><<<grid, kResThreads, smem_bytes(pl.p), st>>>(pl.tmX, pl.tmWL, pl.tmYT, pl.p);
+    LAT_CUDA(launch_pdl(fm_lcb_kernel<T>, grid, kResThreads, smem_bytes(pl.p), st, pl));
     LAT_CUDA(cudaGetLastError());
     return LATTICE_OK;
+}
+
+// programmatic stream serialization unless LATTICE_PDL=0 (see tc::griddep_wait)
+template <typename K>
+cudaError_t launch_pdl(K kernel, int grid, int threads, size_t smem, cudaStream_t st, const Plan& pl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(threads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, pl.tmX, pl.tmWL, pl.tmYT, pl.p);
 }
 
 lattice_status launch(const Plan& pl, cudaStream_t st) {
@@ -826,7 +850,7 @@ lattice_status launch(const Plan& pl, cudaStream_t st) {
         }
         const int grid = (int)(pl.p.B < num_sms() ? pl.p.B : num_sms());
         if (grid <= 0) return LATTICE_OK;
-        fm_lcb_large_kernel<<<grid, kThreads, smem_bytes(pl.p), st>>>(pl.tmX, pl.tmWL, pl.tmYT, pl.p);
+        LAT_CUDA(launch_pdl(fm_lcb_large_kernel, grid, kThreads, smem_bytes(pl.p), st, pl));
         LAT_CUDA(cudaGetLastError());
         return LATTICE_OK;
     }

@@ -204,6 +204,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int C = p.cluster;
     const int rank = C > 1 ? (int)tc::cluster_rank() : 0;
+    // PDL: the tile count and every operand may come from the preceding kernel
+    tc::griddep_wait();
+    tc::griddep_launch_dependents();
 
     Sched s;
     s.nt = (p.N + BN - 1) / BN;
@@ -489,6 +492,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::fence_after();
     tc::cluster_sync();
     const uint32_t tmem = *tmem_slot;
+    // PDL: set up while the preceding kernel drains; its outputs are read only after this
+    tc::griddep_wait();
+    tc::griddep_launch_dependents();
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer (both CTAs), completions on the leader's barrier
@@ -651,13 +657,15 @@ lattice_status launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Para
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = C;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     // persistent grid = the clusters that can be co-resident (GPC sizes limit clusters of 8 to
     // 16 per B200); a larger grid would serialise whole clusters behind the first wave
     static int max_clusters[kMaxCluster + 1] = {0};
@@ -691,13 +699,15 @@ lattice_status launch_2cta(const CUtensorMap& ta, const CUtensorMap& tb, const P
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     static int max_pairs = 0;
     if (!max_pairs) {
         cfg.gridDim = dim3(2 * (num_sms() / 2), 1, 1);
@@ -707,7 +717,7 @@ lattice_status launch_2cta(const CUtensorMap& ta, const CUtensorMap& tb, const P
         max_pairs = mc;
     }
     const int units = ((p.M + 2 * BM - 1) / (2 * BM)) * ((p.N + BN - 1) / BN);
-    if (p.epi == kSwish || p.epi == kSwishHard)
+    if ((p.epi == kSwish || p.epi == kSwishHard) && !p.rowcnt_zeroed)
         LAT_CUDA(cudaMemsetAsync(p.rowcnt, 0, sizeof(int) * 2 * ((p.M + 2 * BM - 1) / (2 * BM)), st));
     int pairs = max_pairs < units ? max_pairs : units;
     if (pairs < 1) pairs = 1;

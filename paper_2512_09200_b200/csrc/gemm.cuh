@@ -51,6 +51,7 @@ struct Params {
     // and per (256-row block, CTA half) arrival counters, exchanged through global memory
     float* rowpart;
     int* rowcnt;
+    int rowcnt_zeroed;   // 1: the caller zeroed rowcnt for this launch (no memset between kernels)
     // grouped
     const int4* tiles;   // {group, row0, row_end, 0}; nullptr = dense
     const int* n_tiles;

@@ -117,7 +117,8 @@ struct lattice_net {
     void* D2 = nullptr;          // [dense_features*d][dense_hidden]
     void *Din = nullptr, *Hd = nullptr, *Od = nullptr;  // dense input copy, hidden, output rows
     float* rowpart = nullptr;  // swish GEMMs (CTA-pair kernel): row-statistics exchange
-    int* rowcnt = nullptr;
+    int* rowcnt = nullptr;     // [swish GEMMs][rowcnt_stride] arrival counters, zeroed once per forward
+    size_t rowcnt_stride = 0, rowcnt_total = 0;
     // workspace
     int32_t *pos = nullptr, *order = nullptr, *seg = nullptr, *bucket_ws = nullptr;
     int4* tiles = nullptr;
@@ -251,7 +252,8 @@ lattice_status build_plans(lattice_net* net) {
                 p.epi = c.hard ? gemm::kSwishHard : gemm::kSwish;
                 p.cluster = (out + 255) / 256;
                 p.rowpart = net->rowpart;
-                p.rowcnt = net->rowcnt;
+                p.rowcnt = net->rowcnt + (size_t)(blk * (c.n_mlp - 1) + li) * net->rowcnt_stride;
+                p.rowcnt_zeroed = 1;  // one memset per forward for every swish GEMM's counters
             } else {
                 p.C = Xn;
                 p.ldc = nd;
@@ -277,7 +279,8 @@ lattice_status build_plans(lattice_net* net) {
         d1.epi = c.hard ? gemm::kSwishHard : gemm::kSwish;
         d1.cluster = (c.dense_hidden + 255) / 256;
         d1.rowpart = net->rowpart;
-        d1.rowcnt = net->rowcnt;
+        d1.rowcnt = net->rowcnt + (size_t)c.blocks * (c.n_mlp - 1) * net->rowcnt_stride;
+        d1.rowcnt_zeroed = 1;
         lattice_status s = gemm::plan(&net->dense_plans[0], net->Din, c.dense_in, Bm, net->D1, c.dense_in,
                                       c.dense_hidden, d1, (int)((Bm + 127) / 128), net->f32);
         if (s != LATTICE_OK) return s;
@@ -385,7 +388,9 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
     {  // row-statistics exchange of the swish GEMMs: [rows][<= 8 N-tiles] + counters
         const size_t rows = (size_t)((Bm + 255) / 256) * 256;
         NET_TRY(dalloc(net, &net->rowpart, rows * 8));
-        NET_TRY(dalloc(net, &net->rowcnt, rows / 128 + 16));
+        net->rowcnt_stride = rows / 128 + 16;
+        net->rowcnt_total = net->rowcnt_stride * ((size_t)c.blocks * (c.n_mlp - 1) + 1);
+        NET_TRY(dalloc(net, &net->rowcnt, net->rowcnt_total));
     }
     NET_TRY(dalloc(net, &net->pos, (size_t)Bm));
     NET_TRY(dalloc(net, &net->order, (size_t)Bm));
@@ -556,6 +561,9 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
         }
         LAT_CUDA(cudaGetLastError());
     }
+    // every swish GEMM of this forward counts row-statistics arrivals in its own zeroed slot,
+    // so no memset sits between the dense-chain kernels (they overlap through PDL)
+    LAT_CUDA(cudaMemsetAsync(net->rowcnt, 0, sizeof(int) * net->rowcnt_total, stream));
     if (c.dense_features > 0) {  // dense processor -> rows [nc, n) of X0
         LAT_REQUIRE(batch->dense != nullptr, "lattice_net_forward: the network has dense features; batch.dense is null");
         LAT_CUDA(cudaMemcpyAsync(net->Din, batch->dense, net->es * (size_t)B * c.dense_in, cudaMemcpyDeviceToDevice,

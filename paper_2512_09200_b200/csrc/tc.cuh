@@ -291,5 +291,15 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Programmatic dependent launch (PDL): kernels of the dense chain are launched with
+// programmatic stream serialization, so the next kernel's CTAs can be resident (prologue done:
+// barriers, TMEM, weight loads) while this kernel's last CTAs drain. griddep_wait() blocks until
+// every preceding grid has completed and its memory is visible (a no-op for a normal launch);
+// griddep_launch_dependents() lets the next grid be scheduled early.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace tc
 }  // namespace lat
