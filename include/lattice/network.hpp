@@ -95,6 +95,7 @@ public:
         lb.rows = d_rows.get();
         lb.offsets = d_off.get();
         lb.ids = d_ids.get();
+        lb.check = 1;  // host-vector call: synchronous anyway, so bad ids throw DataError
         device::throw_status(lattice_net_forward(net_, &lb, d_logits.get(), nullptr));
         return d_logits.download();
     }

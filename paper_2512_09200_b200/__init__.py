@@ -116,7 +116,7 @@ class NetConfig(ctypes.Structure):
 class Batch(ctypes.Structure):
     _fields_ = [("batch", _I64), ("domain", _P), ("table_dtype", _I32), ("tables", _P),
                 ("rows", _P), ("offsets", _P), ("ids", _P), ("pooled", _P),
-                ("pooled_layout", _I32), ("shards", _I32), ("dense", _P)]
+                ("pooled_layout", _I32), ("shards", _I32), ("dense", _P), ("check", _I32)]
 
 
 def _sig(name, res, args):
@@ -696,9 +696,11 @@ class Network:
             pass
 
     def forward(self, domain, offsets=None, ids=None, table_ptrs=None, rows=None,
-                table_dtype=None, pooled=None, logits=None, stream=None, shards=0, dense=None):
+                table_dtype=None, pooled=None, logits=None, stream=None, shards=0, dense=None,
+                check_errors=False):
         """shards > 0: `pooled` is the table-wise sharded, owner-normalised bf16 layout
-        [S][B][n/S][d] received from the pooled all-to-all."""
+        [S][B][n/S][d] received from the pooled all-to-all. check_errors: synchronise after the
+        embedding stage and raise DataError for an id outside its table (lattice_batch.check)."""
         import torch
         B = domain.shape[0]
         if logits is None:
@@ -715,6 +717,7 @@ class Network:
             b.table_dtype = F32 if table_dtype == torch.float32 else BF16
             b.tables, b.rows, b.offsets, b.ids = _p(table_ptrs), _p(rows), _p(offsets), _p(ids)
         b.dense = _p(dense)
+        b.check = 1 if check_errors else 0
         check(_lib.lattice_net_forward(self._h, ctypes.byref(b), _p(logits), _stream(stream)))
         return logits
 

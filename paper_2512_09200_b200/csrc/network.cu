@@ -527,7 +527,7 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
         a.out_feature_offset = 0;
         a.sample_pos = net->pos;
         a.normalize = 1;
-        a.check = 0;
+        a.check = batch->check ? 1 : 0;
         a.sources = 1;
         FWD_TRY(lattice_embedding_bag(&a, stream));
     } else {

@@ -259,6 +259,9 @@ static void network_smoke() {
     CHECK(finite);
     const auto again = net.forward(b, ts);
     CHECK(again == logits);  // deterministic
+    SparseBatch oob = b;  // an id outside its table: DataError, as embedding_bag reports it
+    oob.ids[oob.ids.size() / 2] = rows + 3;
+    CHECK_THROWS_AS(net.forward(oob, ts), DataError);
     NetworkConfig bad = c;
     bad.nL = 3;
     CHECK_THROWS_AS(Network{bad}, UsageError);

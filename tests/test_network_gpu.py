@@ -194,6 +194,30 @@ def test_domain_routing_uses_untied_towers():
     assert torch.equal(mixed[torch.from_numpy(d == 2).cuda()], b[torch.from_numpy(d == 2).cuda()])
 
 
+def test_out_of_range_id_reported_when_checked():
+    """An id outside its table: with check_errors the forward raises DataError naming the first
+    offending position in ids (the oracle's semantics, lattice_embedding_bag's message); unchecked
+    (graph / pipelined use) the bag pools it as a zero row and the logits stay finite."""
+    import torch
+    import paper_2512_09200_b200 as L
+    cfg, B, rows = SMALL, 256, 3000
+    net, tab, ptrs, rws, offsets, ids, dom = build(cfg, B, rows)
+    bad = ids.clone()
+    nz = torch.nonzero(offsets[1:] > offsets[:-1]).flatten()
+    pos = int(offsets[int(nz[len(nz) // 2])])  # the first id of some non-empty bag
+    bad[pos] = rows + 5
+    last = int(offsets[-1]) - 1
+    if last > pos:
+        bad[last] = -1  # a later offender: the error still names the first
+    with pytest.raises(L.DataError) as e:
+        net.forward(dom, offsets, bad, ptrs, rws, torch.bfloat16, check_errors=True)
+    assert e.value.index == pos and f"position {pos} " in str(e.value)
+    out = net.forward(dom, offsets, bad, ptrs, rws, torch.bfloat16)
+    assert torch.isfinite(out).all()
+    ok = net.forward(dom, offsets, ids, ptrs, rws, torch.bfloat16, check_errors=True)
+    assert torch.isfinite(ok).all()
+
+
 def test_config_contract():
     import paper_2512_09200_b200 as L
     bad = dict(SMALL)
