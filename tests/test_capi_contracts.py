@@ -1,0 +1,84 @@
+"""C-ABI contract checks that need no GPU: every entry validates its arguments before touching
+CUDA and reports a violation as LATTICE_USAGE (the reference's UsageError, core.hpp:20-22) with
+a message naming the rule -- the same behaviour on a CPU-only host as on a B200."""
+import ctypes
+
+import pytest
+
+import paper_2512_09200_b200 as L
+
+
+def usage(rc, fragment):
+    assert rc == L.USAGE, rc
+    msg = L.lib.lattice_last_error().decode()
+    assert fragment in msg, msg
+
+
+def bag_args(**kw):
+    a = L.BagArgs()
+    a.features, a.batch, a.dim = 4, 8, 128
+    a.table_dtype = a.out_dtype = L.BF16
+    a.tables = a.rows = a.offsets = a.ids = a.out = ctypes.c_void_p(16)
+    a.out_row_stride = 4 * 128
+    for k, v in kw.items():
+        setattr(a, k, v)
+    return a
+
+
+def test_embedding_bag_contracts():
+    usage(L.lib.lattice_embedding_bag(None, None), "null args")
+    usage(L.lib.lattice_embedding_bag(ctypes.byref(bag_args(out_row_stride=3 * 128)), None),
+          "out_row_stride too small")
+    usage(L.lib.lattice_embedding_bag(ctypes.byref(bag_args(features=1 << 16, batch=1 << 15,
+                                                            out_row_stride=(1 << 16) * 128)), None),
+          "must be < 2^31")
+    usage(L.lib.lattice_embedding_bag(ctypes.byref(bag_args(tables=None)), None), "null pointer")
+    usage(L.lib.lattice_embedding_bag(ctypes.byref(bag_args(table_dtype=9)), None), "table dtype")
+
+
+def net_config(**kw):
+    kw = dict(kw)
+    c = L.NetConfig()
+    base = dict(n=8, d=64, blocks=2, nF=4, nL=4, k=4, n_mlp=2, domains=2, heads=2, tower_hidden=64,
+                max_batch=512, dtype=L.BF16)
+    mlp = kw.pop("mlp", None)
+    base.update(kw)
+    for k, v in base.items():
+        setattr(c, k, v)
+    mlp = mlp or [base["n"] * base["k"], 64, base["nF"] * base["d"]]
+    for i, w in enumerate(mlp):
+        c.mlp[i] = w
+    return c
+
+
+@pytest.mark.parametrize("kw,fragment", [
+    (dict(nL=3), "nF + nL == n"),
+    (dict(n=600, nF=300, nL=300), "n must be in [1, 512]"),
+    (dict(k=65), "k must be in [1, 64]"),
+    (dict(mlp=[31, 64, 256]), "mlp[0] must equal n*k"),
+    (dict(mlp=[32, 4096, 256]), "hidden widths above 2048"),
+    (dict(domains=33), "domains must be in [1, 32]"),
+    (dict(heads=17), "heads must be in [1, 16]"),
+    (dict(tower_hidden=12), "tower_hidden must be a multiple of 8"),
+    (dict(d=96), "d must be 64 or 128"),
+    (dict(dtype=L.F32, d=128), "fp32 needs d = 64"),
+    (dict(dense_features=8), "dense_features must be in [0, n)"),
+])
+def test_network_config_contracts(kw, fragment):
+    h = ctypes.c_void_p()
+    usage(L.lib.lattice_net_create(ctypes.byref(net_config(**kw)), ctypes.byref(h)), fragment)
+    assert not h.value
+
+
+def test_bucket_rownorm_jsonl_contracts():
+    p = ctypes.c_void_p(16)
+    usage(L.lib.lattice_domain_bucket(10, 33, p, p, p, p, None), "domain_bucket: bad sizes")
+    usage(L.lib.lattice_domain_bucket(-1, 2, p, p, p, p, None), "domain_bucket: bad sizes")
+    usage(L.lib.lattice_rownorm(0, 4, 8, 0.0, p, p, 1, None), "eps must be > 0")
+    usage(L.lib.lattice_rownorm(0, 4, 0, 1e-6, p, p, 1, None), "empty input")  # numerics.hpp:83
+    info = L.JsonlInfo()
+    h = ctypes.c_void_p()
+    usage(L.lib.lattice_jsonl_open(p, 1 << 31, b"big.jsonl", ctypes.byref(h), ctypes.byref(info), None),
+          "< 2 GiB")
+    usage(L.lib.lattice_jsonl_open(p, 10, b"x", None, ctypes.byref(info), None), "null argument")
+    usage(L.lib.lattice_jsonl_task_columns(-1, p, p, p, p, 1, p, p, p, p, None), "bad sizes")
