@@ -50,6 +50,7 @@ struct BagParams {
     const int32_t* const* p_pos;  // [R] output row of each source sample
     void* const* p_out;           // [R] each source's [B][.][D] output
     int32_t src_foff;
+    uint32_t mC, sC, mR, sR;  // fast division by the staged kernel's chunks per segment and by R
 };
 
 // Table rows with an L2 evict_last policy: rows of the table being pooled are re-read by
@@ -436,14 +437,14 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 template <bool PEER>
 __device__ __forceinline__ void locate(const BagParams& p, uint32_t c, uint32_t cps, int& f, int& r, uint32_t& b0,
                                        int& n) {
-    const uint32_t seg = c / cps;
+    const uint32_t seg = fdiv(c, p.mC, p.sC);  // c / cps
     b0 = (c - seg * cps) * kChunk;
     n = (uint32_t)p.B - b0 < (uint32_t)kChunk ? (int)((uint32_t)p.B - b0) : kChunk;
     if (PEER) {
-        f = (int)(seg / (uint32_t)p.R);
+        f = (int)fdiv(seg, p.mR, p.sR);
         r = (int)(seg - (uint32_t)f * (uint32_t)p.R);
     } else {
-        r = (int)(seg / (uint32_t)p.F);
+        r = (int)fdiv(seg, p.mF, p.sF);
         f = (int)(seg - (uint32_t)r * (uint32_t)p.F);
     }
 }
@@ -1007,6 +1008,8 @@ lattice_status lattice_embedding_bag(const lattice_bag_args* a, lattice_stream s
                 bag_l2keep(), 0, 0, 0, 0, 0, nullptr, nullptr, nullptr, nullptr, 0};
     fastdiv((uint32_t)p.B, &p.mB, &p.sB);
     fastdiv((uint32_t)p.F, &p.mF, &p.sF);
+    fastdiv((uint32_t)((p.B + staged::kChunk - 1) / staged::kChunk), &p.mC, &p.sC);  // chunks per segment
+    fastdiv((uint32_t)p.R, &p.mR, &p.sR);
     lattice_status st;
     if (a->table_dtype == LATTICE_F32)
         st = a->out_dtype == LATTICE_F32 ? launch_bag<float, float>(p, row_bytes, stream)
@@ -1067,6 +1070,8 @@ lattice_status lattice_peer_embedding_bag(const lattice_peer_bag_args* a, lattic
                 bag_l2keep(), 0, 0, 0, 0, 1, a->offsets, a->ids, a->sample_pos, a->out, a->feature_base};
     fastdiv((uint32_t)p.B, &p.mB, &p.sB);
     fastdiv((uint32_t)p.F, &p.mF, &p.sF);
+    fastdiv((uint32_t)((p.B + staged::kChunk - 1) / staged::kChunk), &p.mC, &p.sC);  // chunks per segment
+    fastdiv((uint32_t)p.R, &p.mR, &p.sR);
     lattice_status st;
     if (a->table_dtype == LATTICE_F32)
         st = a->out_dtype == LATTICE_F32 ? launch_bag<float, float>(p, row_bytes, stream)
