@@ -99,3 +99,31 @@ def test_zip_from_jsonl_matches_reference_zip_dataset():
     assert np.array_equal(w.cpu().numpy(), rw)
     assert np.array_equal(lab.cpu().numpy(), rl)
     torch.cuda.synchronize()
+
+
+def test_wide_records_with_duplicates_match_reference():
+    """Records with hundreds of feature keys, repeated keys (the last occurrence wins), escaped
+    spellings of the same key and 17-digit values: the per-object duplicate scan at width."""
+    import json
+    import random
+
+    import paper_2512_09200_b200 as L
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = random.Random(11)
+    lines = []
+    for i in range(300):
+        items = []
+        for k in range(rng.randint(100, 300)):
+            key = f"f{rng.randint(0, 150)}"
+            if rng.random() < 0.1:
+                key = key.replace("f", "\\u0066", 1)  # the same key, escaped
+            items.append(f'"{key}":{rng.uniform(-1e6, 1e6)!r}')
+        conv = ",".join(f'"t{rng.randint(0, 5)}":{1700000000000 + rng.randint(0, 10**9)}' for _ in range(10))
+        lines.append('{"domain":"w","user_id":"u%d","ad_id":"a","impression_time_ms":%d,"features":{%s},'
+                     '"conversions":{%s}}' % (i, 1700000000000 + i, ",".join(items), conv))
+    content = ("\n".join(lines) + "\n").encode()
+    recs, err = oracle.ref_parse_jsonl(content, "wide.jsonl")
+    assert err is None, err
+    assert _bits(L.jsonl_records(content, "wide.jsonl")) == _bits(recs)
+
