@@ -459,10 +459,12 @@ typedef struct {
     int32_t shards;
     const void* dense;           /* DEVICE [B][dense_in] in the net dtype (caller order) when
                                     cfg.dense_features > 0 (e.g. lattice_merge_dense output) */
-    int32_t check;               /* tables != NULL only. 1: synchronise after the embedding stage
-                                    and return DATA naming the first id outside its table (its
-                                    position in ids), as lattice_embedding_bag does; 0 (graphs,
-                                    pipelines): such ids pool as zero rows, unreported */
+    int32_t check;               /* 1: synchronise after the bucketing / embedding stage and
+                                    return DATA naming the first sample whose domain is outside
+                                    [0, domains) or (tables != NULL) the first id outside its table
+                                    (its position in ids, as lattice_embedding_bag); 0 (graphs,
+                                    pipelines): bad domains count as domain 0 and bad ids pool as
+                                    zero rows, unreported */
 } lattice_batch;
 
 /* Domain bucketing of a batch ahead of the forward (pooled_layout 2): writes the

@@ -29,8 +29,10 @@ lattice_status check_cuda(cudaError_t e, const char* what);
 // embedding_bag.cu: the stable domain bucketing behind lattice_domain_bucket, with a caller-owned
 // workspace of bucket_workspace(B, G) int32 (lattice_net keeps one: no allocation per step)
 int64_t bucket_workspace(int64_t B, int G);
+// (bad != nullptr: the lowest sample index whose domain is outside [0, G) is atomicMin'ed into
+// *bad, initialised by the caller to ~0; such samples count as domain 0 either way)
 lattice_status bucket_ws(int64_t B, int G, const int32_t* dom, int32_t* pos, int32_t* order, int32_t* seg,
-                         int32_t* ws, cudaStream_t stream);
+                         int32_t* ws, cudaStream_t stream, unsigned long long* bad = nullptr);
 
 // Programmatic dependent launch for the dense chain (FM/LCB and GEMM kernels); LATTICE_PDL=0
 // launches them with plain stream ordering (A/B runs). The kernels call griddepcontrol.wait

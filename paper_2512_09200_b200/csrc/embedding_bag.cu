@@ -849,11 +849,13 @@ __device__ __forceinline__ int bucket_domain(const int32_t* __restrict__ dom, in
 }
 
 __global__ void __launch_bounds__(kBucketThreads) bucket_hist_kernel(int64_t B, int G, const int32_t* __restrict__ dom,
-                                                                     int32_t* __restrict__ hist) {
+                                                                     int32_t* __restrict__ hist,
+                                                                     unsigned long long* bad) {
     __shared__ int32_t h[kMaxDomains];
     if (threadIdx.x < kMaxDomains) h[threadIdx.x] = 0;
     __syncthreads();
     const int64_t b = (int64_t)blockIdx.x * kBucketThreads + threadIdx.x;
+    if (bad && b < B && (dom[b] < 0 || dom[b] >= G)) atomicMin(bad, (unsigned long long)b);  // first offender
     const int g = bucket_domain(dom, B, G, b);
     // one atomic per (warp, domain)
     const unsigned same = __match_any_sync(0xffffffffu, g);
@@ -965,9 +967,9 @@ lattice_status sync_err(unsigned long long* err, cudaStream_t st, unsigned long 
 int64_t bucket_workspace(int64_t B, int G) { return 2 * ((B + kBucketThreads - 1) / kBucketThreads) * G; }
 
 lattice_status bucket_ws(int64_t B, int G, const int32_t* dom, int32_t* pos, int32_t* order, int32_t* seg,
-                         int32_t* ws, cudaStream_t stream) {
+                         int32_t* ws, cudaStream_t stream, unsigned long long* bad) {
     const int64_t nblk = (B + kBucketThreads - 1) / kBucketThreads;
-    bucket_hist_kernel<<<(unsigned)nblk, kBucketThreads, 0, stream>>>(B, G, dom, ws);
+    bucket_hist_kernel<<<(unsigned)nblk, kBucketThreads, 0, stream>>>(B, G, dom, ws, bad);
     bucket_scan_kernel<<<1, kBucketThreads, 0, stream>>>(nblk, G, ws, ws + nblk * G, seg);
     bucket_rank_kernel<<<(unsigned)nblk, kBucketThreads, 0, stream>>>(B, G, dom, ws + nblk * G, seg, pos, order);
     LAT_CUDA(cudaGetLastError());

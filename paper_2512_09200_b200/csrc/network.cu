@@ -121,6 +121,7 @@ struct lattice_net {
     size_t rowcnt_stride = 0, rowcnt_total = 0;
     // workspace
     int32_t *pos = nullptr, *order = nullptr, *seg = nullptr, *bucket_ws = nullptr;
+    unsigned long long* bad_domain = nullptr;  // checked forwards: first sample with a bad domain
     int4* tiles = nullptr;
     int* n_tiles = nullptr;
     void* X[2] = {nullptr, nullptr};
@@ -396,6 +397,7 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
     NET_TRY(dalloc(net, &net->order, (size_t)Bm));
     NET_TRY(dalloc(net, &net->seg, (size_t)c.domains + 1));
     NET_TRY(dalloc(net, &net->bucket_ws, (size_t)lat::bucket_workspace(Bm, c.domains)));
+    NET_TRY(dalloc(net, &net->bad_domain, 1));
     NET_TRY(dalloc(net, &net->tiles, (size_t)((Bm + 127) / 128 + c.domains)));
     NET_TRY(dalloc(net, &net->n_tiles, 1));
     NET_TRY(dalloc_bytes(net, &net->X[0], es * (size_t)Bm * nd));
@@ -507,7 +509,23 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
     const bool in_place = !batch->tables && batch->pooled_layout == 2;  // X0 written by peers
     const int nc = c.n - c.dense_features;  // sparse (table-pooled) embeddings come first
     FWD_TRY(mark());
-    if (!in_place) FWD_TRY(lattice_net_bucket(net, B, batch->domain, stream));
+    if (!in_place && batch->check) {  // checked: a domain outside [0, domains) is a DataError
+        LAT_CUDA(cudaMemsetAsync(net->bad_domain, 0xff, sizeof(*net->bad_domain), stream));
+        FWD_TRY(bucket_ws(B, c.domains, batch->domain, net->pos, net->order, net->seg, net->bucket_ws,
+                          (cudaStream_t)stream, net->bad_domain));
+        tiles_kernel<<<1, 256, 0, stream>>>(net->seg, c.domains, net->tiles, net->n_tiles);
+        LAT_CUDA(cudaGetLastError());
+        unsigned long long bad = ~0ull;
+        LAT_CUDA(cudaMemcpyAsync(&bad, net->bad_domain, sizeof(bad), cudaMemcpyDeviceToHost, stream));
+        LAT_CUDA(cudaStreamSynchronize(stream));
+        if (bad != ~0ull)
+            return set_error(LATTICE_DATA,
+                             "network: sample " + std::to_string(bad) + " has a domain outside [0, " +
+                                 std::to_string(c.domains) + ")",
+                             (int64_t)bad);
+    } else if (!in_place) {
+        FWD_TRY(lattice_net_bucket(net, B, batch->domain, stream));
+    }
     FWD_TRY(mark());
     if (in_place) {
         // lattice_net_bucket ran for this batch and lattice_peer_embedding_bag filled X0

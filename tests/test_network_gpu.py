@@ -195,9 +195,10 @@ def test_domain_routing_uses_untied_towers():
 
 
 def test_out_of_range_id_reported_when_checked():
-    """An id outside its table: with check_errors the forward raises DataError naming the first
-    offending position in ids (the oracle's semantics, lattice_embedding_bag's message); unchecked
-    (graph / pipelined use) the bag pools it as a zero row and the logits stay finite."""
+    """An id outside its table (or a domain outside [0, domains)): with check_errors the forward
+    raises DataError naming the first offender (the oracle's semantics, lattice_embedding_bag's
+    message); unchecked (graph / pipelined use) the bag pools a zero row / the sample takes
+    domain 0, and the logits stay finite."""
     import torch
     import paper_2512_09200_b200 as L
     cfg, B, rows = SMALL, 256, 3000
@@ -216,6 +217,14 @@ def test_out_of_range_id_reported_when_checked():
     assert torch.isfinite(out).all()
     ok = net.forward(dom, offsets, ids, ptrs, rws, torch.bfloat16, check_errors=True)
     assert torch.isfinite(ok).all()
+    # a domain outside [0, domains): DataError naming the first such sample when checked
+    bad_dom = dom.clone()
+    bad_dom[7] = cfg["domains"]
+    bad_dom[100] = -1
+    with pytest.raises(L.DataError) as e:
+        net.forward(bad_dom, offsets, ids, ptrs, rws, torch.bfloat16, check_errors=True)
+    assert e.value.index == 7 and "sample 7 " in str(e.value)
+    assert torch.isfinite(net.forward(bad_dom, offsets, ids, ptrs, rws, torch.bfloat16)).all()
 
 
 def test_config_contract():
