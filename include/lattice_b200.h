@@ -399,6 +399,28 @@ typedef struct {
 lattice_status lattice_gemm(const lattice_gemm_args* args, lattice_stream stream);
 
 /* ======================================================================================
+ * K2 on its own: the interaction half of one DWFB block (DESIGN.md section 3
+ * step 3), per sample b with X_b [n][d]:
+ *   P = q(X_b^T . Y)  (d x k),  F = X_b . P  (n x k),  Fin[b] = q(rms_norm(flatten F))  (n*k)
+ *   Xout[b][nF+i] = q(rms_norm_d((W_L . X_b)_i + X_b[nF+i])), i < nL  (LCB half of X')
+ * q() = round to the storage dtype. Rows [0, nF) of Xout are not written (the FMB MLP's
+ * residual-norm epilogue fills them). The network runs the same kernel in every block; this
+ * entry exists for kernel-level tests and callers composing their own blocks.
+ * ==================================================================================== */
+typedef struct {
+    int64_t batch;
+    int32_t n, d, k, nF, nL;   /* n <= 512 (n > 256: bf16, d = 128, k <= 48), k <= 64, nF + nL == n */
+    int32_t dtype;             /* LATTICE_BF16, or LATTICE_F32 (kind::tf32; d = 64, n <= 64) */
+    const void* X;             /* DEVICE [B][n][d] */
+    const void* YT;            /* DEVICE [k][n]  (Y transposed) */
+    const void* WL;            /* DEVICE [nL][n] */
+    void* Fin;                 /* DEVICE out [B][n*k] */
+    void* Xout;                /* DEVICE out [B][n][d], rows [nF, n) */
+} lattice_fm_lcb_args;
+
+lattice_status lattice_fm_lcb(const lattice_fm_lcb_args* args, lattice_stream stream);
+
+/* ======================================================================================
  * Network (K1 -> K2/K3 blocks -> K4 towers). No reference code; the
  * arithmetic is DESIGN.md section 3 and oracle/lattice_oracle.c lo_net_forward.
  * ==================================================================================== */
@@ -435,6 +457,14 @@ void lattice_net_destroy(lattice_net* net);
  * [G][heads][tower_hidden], 6 dense D1 [dense_hidden][dense_in], 7 dense D2
  * [dense_features*d][dense_hidden]. block ignored for 4-7. */
 const void* lattice_net_weight(lattice_net* net, int32_t block, int32_t kind, int32_t index);
+/* Load caller-owned weights (a trained model) into one of the tensors above, replacing the
+ * generated values. src: DEVICE, unpadded, row-major in the layout listed for `kind` (kind 4/5:
+ * all G domains stacked), in src_dtype: LATTICE_F32 (rounded to the net dtype with RNE; kind 5 is
+ * kept fp32) or the net dtype itself (copied bit for bit). The net's zero padding is kept. Ordered
+ * on `stream`; the forward passes queued after it on that stream see the new values. Non-finite
+ * values are not checked. */
+lattice_status lattice_net_set_weight(lattice_net* net, int32_t block, int32_t kind, int32_t index,
+                                      const void* src, int32_t src_dtype, lattice_stream stream);
 
 typedef struct {
     int64_t batch;
@@ -471,8 +501,12 @@ typedef struct {
  * domain-sorted row of every sample, readable through lattice_net_buffer(net, 1). */
 lattice_status lattice_net_bucket(lattice_net* net, int64_t batch, const int32_t* domain,
                                   lattice_stream stream);
-/* Workspace pointers for peer export: 0 = X0 [max_batch][n][d] (net dtype, the embedding
- * stage's output), 1 = sample_pos int32 [max_batch]. NULL for an unknown index. */
+/* Workspace pointers: 0 = X0 [max_batch][n][d] (net dtype, the embedding stage's output; peer
+ * export), 1 = sample_pos int32 [max_batch] (row of sample b in the domain-sorted activations),
+ * 2 = the second activation buffer. Blocks ping-pong: block l reads buffer (l & 1 ? 2 : 0) and
+ * writes the other, so after a forward buffer (blocks & 1 ? 2 : 0) holds the last block's output
+ * X_L (the towers' input) and the other X_{L-1} (inspection / stage-wise tests). NULL for an
+ * unknown index. */
 void* lattice_net_buffer(lattice_net* net, int32_t which);
 
 /* logits: DEVICE fp32 [B][heads] in the caller's sample order. */

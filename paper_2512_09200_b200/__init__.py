@@ -105,6 +105,11 @@ class GemmArgs(ctypes.Structure):
                 ("resid", _P), ("ldr", _I64), ("group", _I32), ("in_dtype", _I32)]
 
 
+class FmLcbArgs(ctypes.Structure):
+    _fields_ = [("batch", _I64), ("n", _I32), ("d", _I32), ("k", _I32), ("nF", _I32), ("nL", _I32),
+                ("dtype", _I32), ("X", _P), ("YT", _P), ("WL", _P), ("Fin", _P), ("Xout", _P)]
+
+
 class NetConfig(ctypes.Structure):
     _fields_ = [("n", _I32), ("d", _I32), ("blocks", _I32), ("nF", _I32), ("nL", _I32),
                 ("k", _I32), ("n_mlp", _I32), ("mlp", _I32 * 6), ("domains", _I32),
@@ -162,6 +167,8 @@ _sig("lattice_gemm", ctypes.c_int, [ctypes.POINTER(GemmArgs), _P])
 _sig("lattice_net_create", ctypes.c_int, [ctypes.POINTER(NetConfig), ctypes.POINTER(_P)])
 _sig("lattice_net_destroy", None, [_P])
 _sig("lattice_net_weight", _P, [_P, _I32, _I32, _I32])
+_sig("lattice_net_set_weight", ctypes.c_int, [_P, _I32, _I32, _I32, _P, _I32, _P])
+_sig("lattice_fm_lcb", ctypes.c_int, [ctypes.POINTER(FmLcbArgs), _P])
 _sig("lattice_net_forward", ctypes.c_int, [_P, ctypes.POINTER(Batch), _P, _P])
 _sig("lattice_net_set_timing", ctypes.c_int, [_P, _I32])
 _sig("lattice_net_stage_times", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_float), _I32,
@@ -187,7 +194,7 @@ EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_versio
            "lattice_routed_objectives", "lattice_merge_dense", "lattice_student_inputs",
            "lattice_clip_features", "lattice_smooth_labels", "lattice_swish_rn_jvp",
            "lattice_jsonl_open", "lattice_jsonl_extract", "lattice_jsonl_task_columns",
-           "lattice_jsonl_close"]
+           "lattice_jsonl_close", "lattice_net_set_weight", "lattice_fm_lcb"]
 
 lib = _lib
 
@@ -637,6 +644,22 @@ def gemm(A, B, epilogue=EPI_STORE, out_dtype=None, resid=None, group=128, out=No
     return out
 
 
+def fm_lcb(X, YT, WL, nF, Fin=None, Xout=None, stream=None):
+    """K2 alone (lattice_fm_lcb): X [B, n, d], YT [k, n], WL [nL, n], all bf16 (or all fp32).
+    Returns (Fin [B, n*k], Xout [B, n, d] with rows [nF, n) written)."""
+    import torch
+    B, n, d = X.shape
+    k, nL = YT.shape[0], WL.shape[0]
+    if Fin is None:
+        Fin = torch.empty((B, n * k), dtype=X.dtype, device=X.device)
+    if Xout is None:
+        Xout = torch.zeros_like(X)
+    a = FmLcbArgs(B, n, d, k, nF, nL, F32 if X.dtype == torch.float32 else BF16, _p(X), _p(YT),
+                  _p(WL) if nL else None, _p(Fin), _p(Xout))
+    check(_lib.lattice_fm_lcb(ctypes.byref(a), _stream(stream)))
+    return Fin, Xout
+
+
 # ---- network -------------------------------------------------------------------------------------
 
 class _CAI:
@@ -726,11 +749,24 @@ class Network:
         check(_lib.lattice_net_bucket(self._h, domain.shape[0], _p(domain), _stream(stream)))
 
     def buffer(self, which):
-        """Device pointer of a workspace buffer: 0 = X0, 1 = sample_pos (lattice_net_buffer)."""
+        """Device pointer of a workspace buffer (lattice_net_buffer): 0 = X0 / even blocks'
+        input, 1 = sample_pos, 2 = odd blocks' input."""
         p = _lib.lattice_net_buffer(self._h, which)
         if not p:
             raise UsageError(f"lattice_net_buffer: unknown buffer {which}")
         return p
+
+    def activations(self, layer, batch):
+        """X_layer of the last forward in the caller's sample order, [batch, n, d] (a copy):
+        layer = blocks (the towers' input) or blocks - 1 (the last block's input)."""
+        import torch
+        c = self.cfg
+        if layer not in (c["blocks"], c["blocks"] - 1):
+            raise UsageError("activations: only X_L and X_{L-1} survive a forward")
+        dt = torch.float32 if c["dtype"] in ("f32", "fp32", "float32") else torch.bfloat16
+        X = _view(self.buffer(2 if layer & 1 else 0), (batch, c["n"], c["d"]), dt)
+        pos = torch.as_tensor(_CAI(self.buffer(1), (batch,), "<i4"), device="cuda").long()
+        return X[pos].clone()
 
     def forward_in_place(self, domain, logits=None, stream=None, dense=None):
         """Forward over an X0 already filled by lattice_peer_embedding_bag (pooled_layout 2)."""
@@ -755,6 +791,15 @@ class Network:
         n = _I32()
         check(_lib.lattice_net_stage_times(self._h, buf, 64, ctypes.byref(n)))
         return [buf[i] for i in range(n.value)]
+
+    def set_weight(self, kind, src, block=0, index=0, stream=None):
+        """Load caller-owned weights (lattice_net_set_weight): src a CUDA tensor, fp32 or the net
+        dtype, unpadded, in the layout weights() returns (kind 1 YT, 2 WL, 3 MLP layer `index`,
+        4 T1 [G, th, n*d], 5 T2 [G, heads, th], 6 D1, 7 D2)."""
+        import torch
+        src = src.contiguous()
+        dt = F32 if src.dtype == torch.float32 else BF16
+        check(_lib.lattice_net_set_weight(self._h, block, kind, index, _p(src), dt, _stream(stream)))
 
     def weights(self):
         """Host fp32 copies of every weight, unpadded, in the oracle's layout."""

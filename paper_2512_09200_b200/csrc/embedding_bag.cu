@@ -215,11 +215,17 @@ __device__ __forceinline__ void bag_range(const BagParams& p, uint32_t bag, cons
     } else {
         s = p.offsets[bag];
         e = p.offsets[bag + 1];
-        len = (int)(e - s);
         if (p.slice_cap > 0) {
+            // source r's ids sit in the fixed slice [r*cap, (r+1)*cap): a slice the sender had to
+            // truncate (it set the overflow flag) pools only what arrived, never the next slice
             const int64_t r = bag / ((int64_t)p.F * p.B);
-            s += r * p.slice_cap - p.offsets[r * p.F * p.B];
+            const int64_t base = p.offsets[r * p.F * p.B];
+            s = min(s - base, p.slice_cap);
+            e = min(e - base, p.slice_cap);
+            s += r * p.slice_cap;
+            e += r * p.slice_cap;
         }
+        len = (int)(e - s);
         idp = p.ids + s;
         return;
     }
@@ -457,7 +463,12 @@ __device__ __forceinline__ int64_t chunk_offsets(const BagParams& p, uint32_t c,
     locate<PEER>(p, c, cps, f, r, b0, n);
     if (lane > n) return 0;
     if (PEER) return p.p_off[r][(int64_t)(p.src_foff + f) * p.B + b0 + lane];
-    return p.offsets[((int64_t)r * p.F + f) * p.B + b0 + lane];
+    const int64_t o = p.offsets[((int64_t)r * p.F + f) * p.B + b0 + lane];
+    if (p.slice_cap > 0) {  // clamp into source r's fixed slice (see direct::bag_range)
+        const int64_t base = p.offsets[(int64_t)r * p.F * p.B];
+        return base + min(o - base, p.slice_cap);
+    }
+    return o;
 }
 
 // Fill stage S for chunk c whose offsets are `o` (per lane, from chunk_offsets): header and

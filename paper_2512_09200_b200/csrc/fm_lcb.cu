@@ -861,3 +861,54 @@ int wl_rows(const Params& p) { return p.nL > 128 ? 256 : 128; }
 
 }  // namespace fm
 }  // namespace lat
+
+// ---------------------------------------------------------------------------------------------
+// lattice_fm_lcb: K2 on its own (tests and callers composing their own blocks). Y^T and W_L come
+// unpadded from the caller and are copied into the zero-padded layout the tensor maps expect.
+// ---------------------------------------------------------------------------------------------
+extern "C" lattice_status lattice_fm_lcb(const lattice_fm_lcb_args* a, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(a != nullptr, "lattice_fm_lcb: null args");
+    LAT_REQUIRE(a->batch >= 0 && a->batch < (1ll << 31), "lattice_fm_lcb: bad batch");
+    LAT_REQUIRE(a->dtype == LATTICE_BF16 || a->dtype == LATTICE_F32, "lattice_fm_lcb: dtype must be bf16 or f32");
+    LAT_REQUIRE(a->n >= 1 && a->n <= 512 && a->k >= 1 && a->k <= 64 && a->nF >= 1 && a->nL >= 0 &&
+                    a->nF + a->nL == a->n,
+                "lattice_fm_lcb: need 1 <= n <= 512, 1 <= k <= 64, nF >= 1, nF + nL == n");
+    if (a->batch == 0) return LATTICE_OK;
+    LAT_REQUIRE(a->X && a->YT && a->Fin && a->Xout && (a->nL == 0 || a->WL), "lattice_fm_lcb: null pointer");
+    const cudaStream_t st = (cudaStream_t)stream;
+    fm::Plan pl = {};
+    fm::Params& p = pl.p;
+    p.B = a->batch;
+    p.n = a->n;
+    p.d = a->d;
+    p.k = a->k;
+    p.nF = a->nF;
+    p.nL = a->nL;
+    p.n_pad = a->n > 256 ? (a->n + 255) / 256 * 256 : (a->n + 15) / 16 * 16;
+    p.k_pad = (a->k + 15) / 16 * 16;
+    p.tmem_cols = 512;
+    p.f32 = a->dtype == LATTICE_F32 ? 1 : 0;
+    p.Fout = a->Fin;
+    p.Xout = a->Xout;
+    lattice_status s = fm::check(p);
+    if (s != LATTICE_OK) return s;
+    const size_t es = p.f32 ? 4 : 2;
+    const int wr = fm::wl_rows(p);
+    const size_t yt_bytes = es * (size_t)p.k_pad * p.n_pad, wl_bytes = es * (size_t)wr * p.n_pad;
+    uint8_t* ws = nullptr;
+    LAT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), yt_bytes + wl_bytes, st));
+    auto body = [&]() -> lattice_status {
+        LAT_CUDA(cudaMemsetAsync(ws, 0, yt_bytes + wl_bytes, st));
+        LAT_CUDA(cudaMemcpy2DAsync(ws, es * p.n_pad, a->YT, es * p.n, es * p.n, p.k, cudaMemcpyDeviceToDevice, st));
+        if (p.nL > 0)
+            LAT_CUDA(cudaMemcpy2DAsync(ws + yt_bytes, es * p.n_pad, a->WL, es * p.n, es * p.n, p.nL,
+                                       cudaMemcpyDeviceToDevice, st));
+        lattice_status r = fm::make_maps(&pl, a->X, ws + yt_bytes, ws);
+        if (r != LATTICE_OK) return r;
+        return fm::launch(pl, st);
+    };
+    s = body();
+    cudaFreeAsync(ws, st);
+    return s;
+}

@@ -99,6 +99,17 @@ __global__ void shard_gather_kernel(int64_t B, int n, int d, int es, int S, cons
 
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+// fp32 [rows][cols] -> dst rows of stride ld in the net dtype (RNE), for lattice_net_set_weight
+template <typename TO>
+__global__ void load_rows_kernel(int64_t rows, int64_t cols, const float* __restrict__ src, TO* __restrict__ dst,
+                                 int64_t ld) {
+    const int64_t n = rows * cols;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / cols;
+        put(dst + r * ld + (i - r * cols), src[i]);
+    }
+}
+
 }  // namespace
 }  // namespace lat
 
@@ -437,6 +448,44 @@ const void* lattice_net_weight(lattice_net* net, int32_t block, int32_t kind, in
     }
 }
 
+lattice_status lattice_net_set_weight(lattice_net* net, int32_t block, int32_t kind, int32_t index,
+                                      const void* src, int32_t src_dtype, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(net != nullptr && src != nullptr, "lattice_net_set_weight: null argument");
+    const lattice_net_config& c = net->cfg;
+    void* dst = const_cast<void*>(lattice_net_weight(net, block, kind, index));
+    LAT_REQUIRE(dst != nullptr, "lattice_net_set_weight: no such weight (block / kind / index)");
+    // unpadded [rows][cols] and the row stride of the net's (possibly padded) buffer
+    int64_t rows = 0, cols = 0, ld = 0;
+    switch (kind) {
+        case 1: rows = c.k, cols = c.n, ld = net->n_pad; break;
+        case 2: rows = c.nL, cols = c.n, ld = net->n_pad; break;
+        case 3: rows = c.mlp[index + 1], cols = c.mlp[index], ld = cols; break;
+        case 4: rows = (int64_t)c.domains * c.tower_hidden, cols = (int64_t)c.n * c.d, ld = cols; break;
+        case 5: rows = (int64_t)c.domains * c.heads, cols = c.tower_hidden, ld = cols; break;
+        case 6: rows = c.dense_hidden, cols = c.dense_in, ld = cols; break;
+        case 7: rows = (int64_t)c.dense_features * c.d, cols = c.dense_hidden, ld = cols; break;
+        default: break;
+    }
+    LAT_REQUIRE(rows > 0 && cols > 0, "lattice_net_set_weight: the network has no such weight");
+    const bool fp32_dst = kind == 5 || net->f32;
+    const int dst_dtype = fp32_dst ? LATTICE_F32 : LATTICE_BF16;
+    LAT_REQUIRE(src_dtype == LATTICE_F32 || src_dtype == dst_dtype,
+                "lattice_net_set_weight: src_dtype must be f32 or the net's dtype");
+    const cudaStream_t st = (cudaStream_t)stream;
+    const size_t des = fp32_dst ? 4 : 2;
+    if (src_dtype == dst_dtype) {
+        LAT_CUDA(cudaMemcpy2DAsync(dst, des * ld, src, des * cols, des * cols, rows, cudaMemcpyDeviceToDevice, st));
+        return LATTICE_OK;
+    }
+    const int64_t n = rows * cols;
+    const unsigned grid = (unsigned)((n + 255) / 256 < 148 * 32 ? (n + 255) / 256 : 148 * 32);
+    load_rows_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(rows, cols, static_cast<const float*>(src),
+                                                          static_cast<__nv_bfloat16*>(dst), ld);
+    LAT_CUDA(cudaGetLastError());
+    return LATTICE_OK;
+}
+
 lattice_status lattice_net_set_timing(lattice_net* net, int32_t enable) {
     LAT_REQUIRE(net != nullptr, "lattice_net_set_timing: null net");
     net->timing = enable != 0;
@@ -481,6 +530,7 @@ void* lattice_net_buffer(lattice_net* net, int32_t which) {
     switch (which) {
         case 0: return net->X[0];
         case 1: return net->pos;
+        case 2: return net->X[1];
         default: return nullptr;
     }
 }

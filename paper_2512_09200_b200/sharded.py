@@ -110,7 +110,13 @@ class ShardedBags:
         dist.all_to_all_single(recv.view(-1), send.view(-1), group=self.group)
         return recv
 
-    def forward_embeddings(self, offsets, ids, tables, table_ptrs, rows, send=None, recv=None):
+    def forward_embeddings(self, offsets, ids, tables, table_ptrs, rows, send=None, recv=None,
+                           check_errors=False):
+        """check_errors: synchronise after the ids exchange and raise if a slice exceeded the
+        static capacity (the owners then pool only the ids that fit: truncation, never a read
+        outside the slice). Unchecked (graphs, pipelines): call check_overflow() later."""
         recv_off, recv_ids, cap = self.exchange_ids(offsets, ids)
+        if check_errors:
+            self.check_overflow()
         send = self.pool(recv_off, recv_ids, cap, tables, table_ptrs, rows, out=send)
         return self.exchange_pooled(send, recv)

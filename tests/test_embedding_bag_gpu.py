@@ -4,6 +4,8 @@ With the synthetic value scheme (k * 2^-10, |k| <= 128) every fp32 bag sum is ex
 GPU output must equal the oracle bit for bit (fp32 out) or equal the one RNE rounding of the
 exact sum (bf16 out). Edge cases: empty bags, bad ids (first offender), permuted output rows,
 strided/offset output (sharding), D in {64, 128, 256}, fp32 and bf16 tables."""
+import os
+
 import numpy as np
 import pytest
 
@@ -183,3 +185,15 @@ def test_full_micro_config_sampled_and_checksum():
     n = int(o_cpu[-1])
     gathered = tab.view(F * rows, D)[feat * rows + ids[:n].long()].double().sum(0)
     assert torch.equal(out.double().sum((0, 1)), gathered)
+
+
+@pytest.mark.parametrize("kernel", ["direct", "staged"])
+def test_static_slice_overflow_truncates_inside_the_slice(kernel):
+    """an overflowing source slice is truncated, not read past (both bag kernels)."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, os.path.join(here, "bag_truncation_check.py")],
+                       env=dict(os.environ, LATTICE_BAG_KERNEL=kernel), capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
