@@ -65,18 +65,24 @@ struct ZipperConfig {
     std::vector<double> probabilities;
     Seed seed;
 
-    // Name checks here; the numeric checks are the library's (lattice_zipper_validate),
-    // which mirror datasets.hpp:60-84 message for message.
+    // datasets.hpp:60-84 in its order: per window name, duplicate, then duration (one loop, so
+    // the first offending window decides the message), then the probabilities -- whose checks,
+    // like the durations', the library's lattice_zipper_validate repeats message for message.
     static ZipperConfig create(std::vector<AttributionWindow> windows, std::vector<double> probabilities,
                                Seed seed) {
         if (windows.empty()) throw UsageError("ZipperConfig: no windows");
         if (probabilities.size() != windows.size())
             throw UsageError("ZipperConfig: probabilities/windows length mismatch");
         std::set<std::string> names;
-        for (const auto& w : windows) {
+        DurationMs prev = 0;
+        for (std::size_t i = 0; i < windows.size(); ++i) {
+            const auto& w = windows[i];
             if (w.name.empty()) throw UsageError("ZipperConfig: empty window name");
             if (!names.insert(w.name).second)
                 throw UsageError("ZipperConfig: duplicate window name '" + w.name + "'");
+            if (w.duration_ms <= (i == 0 ? 0 : prev))
+                throw UsageError("ZipperConfig: window durations must be positive and strictly increasing");
+            prev = w.duration_ms;
         }
         std::vector<std::int64_t> dur;
         for (const auto& w : windows) dur.push_back(w.duration_ms);
@@ -184,7 +190,10 @@ inline std::size_t assign_window(std::string_view user_id, std::string_view ad_i
 namespace detail {
 inline std::string join_domains(const std::vector<std::string>& parts) {
     std::string out;
-    for (std::size_t i = 0; i < parts.size(); ++i) out += (i ? "+" : "") + parts[i];
+    for (const auto& p : parts) {  // datasets.hpp:115-122: '+' only after a non-empty prefix
+        if (!out.empty()) out += "+";
+        out += p;
+    }
     return out;
 }
 }  // namespace detail

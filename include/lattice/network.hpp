@@ -8,6 +8,7 @@
 
 #include <array>
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "core.hpp"
@@ -82,6 +83,17 @@ public:
             throw UsageError("Network::forward: a network with dense features needs forward_device with batch.dense");
         if (t.tables.size() != static_cast<std::size_t>(sparse) || t.rows.size() != t.tables.size())
             throw UsageError("Network::forward: need one table per sparse feature");
+        if (b.batch == 0) return {};
+        // the CSR is already on the host: check it here so a malformed one is a DataError, never
+        // a device read outside ids
+        if (b.offsets.front() != 0)
+            throw DataError("Network::forward: offsets must start at 0");
+        for (std::size_t i = 1; i < b.offsets.size(); ++i)
+            if (b.offsets[i] < b.offsets[i - 1])
+                throw DataError("Network::forward: offsets decrease at bag " + std::to_string(i - 1));
+        if (b.offsets.back() != static_cast<std::int64_t>(b.ids.size()))
+            throw DataError("Network::forward: offsets end at " + std::to_string(b.offsets.back()) + ", ids has " +
+                            std::to_string(b.ids.size()));
         device::Buffer<std::int64_t> d_off(b.offsets), d_rows(t.rows);
         device::Buffer<std::int32_t> d_ids(b.ids.empty() ? std::vector<std::int32_t>{0} : b.ids);
         device::Buffer<std::int32_t> d_dom(b.domain);
@@ -98,6 +110,36 @@ public:
         lb.check = 1;  // host-vector call: synchronous anyway, so bad ids throw DataError
         device::throw_status(lattice_net_forward(net_, &lb, d_logits.get(), nullptr));
         return d_logits.download();
+    }
+
+    // Load trained weights (lattice_net_set_weight): `values` is the unpadded row-major fp32 tensor
+    // of `kind` (1 Y^T [k][n], 2 W_L [nL][n], 3 MLP layer `index` of `block` [out][in], 4 tower W1
+    // [G][tower_hidden][n*d], 5 tower W2 [G][heads][tower_hidden], 6 dense D1, 7 dense D2),
+    // rounded to the network dtype on the device.
+    void set_weight(int kind, int block, int index, const std::vector<float>& values) {
+        const auto& c = cfg_;
+        const std::int64_t nd = static_cast<std::int64_t>(c.n) * c.d;
+        std::int64_t want = -1;
+        switch (kind) {
+            case 1: want = static_cast<std::int64_t>(c.k) * c.n; break;
+            case 2: want = static_cast<std::int64_t>(c.nL) * c.n; break;
+            case 3:
+                if (index >= 0 && index + 1 < static_cast<int>(c.mlp.size()))
+                    want = static_cast<std::int64_t>(c.mlp[index]) * c.mlp[index + 1];
+                break;
+            case 4: want = static_cast<std::int64_t>(c.domains) * c.tower_hidden * nd; break;
+            case 5: want = static_cast<std::int64_t>(c.domains) * c.heads * c.tower_hidden; break;
+            case 6: want = static_cast<std::int64_t>(c.dense_hidden) * c.dense_in; break;
+            case 7: want = static_cast<std::int64_t>(c.dense_features) * c.d * c.dense_hidden; break;
+            default: break;
+        }
+        if (want <= 0) throw UsageError("Network::set_weight: the network has no such weight");
+        if (static_cast<std::int64_t>(values.size()) != want)
+            throw UsageError("Network::set_weight: expected " + std::to_string(want) + " values, got " +
+                             std::to_string(values.size()));
+        device::Buffer<float> d(values);
+        device::throw_status(lattice_net_set_weight(net_, block, kind, index, d.get(), LATTICE_F32, nullptr));
+        device::cuda(cudaStreamSynchronize(nullptr), "Network::set_weight");
     }
 
     // Device-pointer entry: everything already on the GPU, ordered on `stream`.

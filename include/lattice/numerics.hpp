@@ -3,9 +3,10 @@
 // Drop-in for proj/include/lattice/numerics.hpp: rms_norm, swish_rn, swish_rn_hard (:81-107),
 // correlation_loss (:46-78), swish_rn_jvp (:113-136), clip_features and smooth_labels
 // (:139-156) with the same signatures and error contract (eps <= 0 or empty -> UsageError,
-// non-finite -> DataError). correlation_loss, the jvp, clip and smoothing run in fp64. The row is computed by the B200
-// row-norm kernel in fp32 (the same math the GEMM epilogues fuse), so results agree with the
-// fp64 reference to ~1e-7 relative. rms_norm_rows / swish_rn_rows take many rows at once.
+// non-finite -> DataError). Everything runs in fp64 on the device with the reference's own
+// arithmetic (lattice_rownorm_f64: sequential row sums without FMA contraction), so rms_norm is
+// bit-identical to the reference and swish_rn / swish_rn_hard agree to exp()'s last ulp, for
+// inputs of any magnitude. The fp32 batched swish_rn_rows is the GEMM epilogues' arithmetic.
 
 #include <span>
 #include <vector>
@@ -19,12 +20,11 @@ inline constexpr double kDefaultEps = 1e-6;
 namespace detail {
 inline std::vector<double> rownorm(int mode, std::span<const double> x, double eps) {
     if (!(eps > 0.0)) throw UsageError("eps must be > 0");
-    std::vector<float> xf(x.begin(), x.end());
-    device::Buffer<float> d_x(xf), d_y(xf.size());
-    device::throw_status(lattice_rownorm(mode, 1, static_cast<std::int64_t>(xf.size()), eps, d_x.get(),
-                                         d_y.get(), 1, nullptr));
-    const auto y = d_y.download();
-    return std::vector<double>(y.begin(), y.end());
+    if (x.empty()) throw UsageError("rms_norm: empty input");
+    device::Buffer<double> d_x(x.data(), x.size()), d_y(x.size());
+    device::throw_status(lattice_rownorm_f64(mode, 1, static_cast<std::int64_t>(x.size()), eps, d_x.get(),
+                                             d_y.get(), 1, nullptr));
+    return d_y.download();
 }
 }  // namespace detail
 

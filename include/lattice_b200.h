@@ -182,6 +182,13 @@ lattice_status lattice_embedding_bag(const lattice_bag_args* args, lattice_strea
  * ==================================================================================== */
 lattice_status lattice_rownorm(int32_t mode, int64_t rows, int64_t width, double eps,
                                const float* x, float* out, int32_t check, lattice_stream stream);
+/* The same in fp64 with the reference's own arithmetic: the row's sum of squares is taken in
+ * index order without FMA contraction (numerics.hpp:36-40), so rms_norm matches the host
+ * reference bit for bit and swish_rn / swish_rn_hard to within exp()'s last ulp, for inputs of
+ * any magnitude (a sum that overflows gives 0 rows, as in the reference). What the C++ drop-in
+ * (include/lattice/numerics.hpp) calls. */
+lattice_status lattice_rownorm_f64(int32_t mode, int64_t rows, int64_t width, double eps,
+                                   const double* x, double* out, int32_t check, lattice_stream stream);
 
 /* ======================================================================================
  * Dense features across consolidated domains -- replaces the value side of
@@ -397,6 +404,12 @@ typedef struct {
 } lattice_gemm_args;
 
 lattice_status lattice_gemm(const lattice_gemm_args* args, lattice_stream stream);
+/* Synchronises `stream`, then reports (LATTICE_CUDA) and clears any failed row-statistics exchange
+ * of the swish_rn GEMMs since the last check. Those GEMMs run a persistent grid whose CTA pairs
+ * exchange per-row sums of squares through global memory; the launch is cooperative, so the
+ * hardware keeps every pair resident, and a wait that still exceeds 5 s gives up (invalid
+ * outputs, counted here) instead of hanging the GPU. A checked lattice_net_forward calls it. */
+lattice_status lattice_device_check(lattice_stream stream);
 
 /* ======================================================================================
  * K2 on its own: the interaction half of one DWFB block (DESIGN.md section 3

@@ -82,6 +82,26 @@ int ref_zipper_config_check(int W, const int64_t* durations, const double* probs
     });
 }
 
+// datasets.hpp:60-84 with caller-named windows (the drop-in's check order is fuzzed against it)
+int ref_zipper_config_create(int W, const char* const* names, const int64_t* durations, const double* probs) {
+    return guarded([&] {
+        std::vector<lattice_ref::AttributionWindow> windows;
+        for (int i = 0; i < W; ++i) windows.push_back({names[i], durations[i]});
+        lattice_ref::ZipperConfig::create(std::move(windows), std::vector<double>(probs, probs + W),
+                                          lattice_ref::Seed{7});
+        return 0;
+    });
+}
+
+// datasets.hpp:115-122
+int ref_joined_domain_name(int n, const char* const* parts, char* out, int cap) {
+    std::vector<std::string> v(parts, parts + n);
+    const std::string s = lattice_ref::detail::joined_domain_name(v);
+    if ((int)s.size() + 1 > cap) return -1;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return (int)s.size();
+}
+
 // datasets.hpp:179
 int ref_assign_window(const char* user, uint32_t ulen, const char* ad, uint32_t alen, int64_t ts,
                       int W, const int64_t* durations, const double* probs, uint64_t seed,

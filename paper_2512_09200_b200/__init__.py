@@ -139,6 +139,7 @@ _sig("lattice_zipper_validate", ctypes.c_int, [_I32, _P, _P])
 _sig("lattice_zipper_assign_labels", ctypes.c_int, [ctypes.POINTER(ZipArgs), _P])
 _sig("lattice_embedding_bag", ctypes.c_int, [ctypes.POINTER(BagArgs), _P])
 _sig("lattice_rownorm", ctypes.c_int, [_I32, _I64, _I64, ctypes.c_double, _P, _P, _I32, _P])
+_sig("lattice_rownorm_f64", ctypes.c_int, [_I32, _I64, _I64, ctypes.c_double, _P, _P, _I32, _P])
 _sig("lattice_fill_tables", ctypes.c_int, [_P, _I32, _I32, _I64, _I32, _U64, _I32, _I64, _P])
 _sig("lattice_fill_weights", ctypes.c_int, [_P, _I32, _I64, _I64, _U64, _U64, _P])
 _sig("lattice_synth_bags", ctypes.c_int, [_I32, _I64, _I32, _I64, _U64, _P, _P, _P])
@@ -164,6 +165,7 @@ _sig("lattice_clip_features", ctypes.c_int, [_I64, _P, ctypes.c_double, _P, _P])
 _sig("lattice_smooth_labels", ctypes.c_int, [_I64, _P, ctypes.c_double, _P, _I32, _P])
 _sig("lattice_swish_rn_jvp", ctypes.c_int, [_I64, _I64, ctypes.c_double, _P, _P, _P, _I32, _P])
 _sig("lattice_gemm", ctypes.c_int, [ctypes.POINTER(GemmArgs), _P])
+_sig("lattice_device_check", ctypes.c_int, [_P])
 _sig("lattice_net_create", ctypes.c_int, [ctypes.POINTER(NetConfig), ctypes.POINTER(_P)])
 _sig("lattice_net_destroy", None, [_P])
 _sig("lattice_net_weight", _P, [_P, _I32, _I32, _I32])
@@ -194,7 +196,8 @@ EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_versio
            "lattice_routed_objectives", "lattice_merge_dense", "lattice_student_inputs",
            "lattice_clip_features", "lattice_smooth_labels", "lattice_swish_rn_jvp",
            "lattice_jsonl_open", "lattice_jsonl_extract", "lattice_jsonl_task_columns",
-           "lattice_jsonl_close", "lattice_net_set_weight", "lattice_fm_lcb"]
+           "lattice_jsonl_close", "lattice_net_set_weight", "lattice_fm_lcb",
+           "lattice_rownorm_f64", "lattice_device_check"]
 
 lib = _lib
 
@@ -569,13 +572,14 @@ def pack_slices(bounds, ids, cap, out, overflow, stream=None):
 
 
 def rownorm(x, mode=1, eps=1e-6, check_errors=True, stream=None):
-    """mode 0 rms_norm, 1 swish_rn, 2 swish_rn_hard over the last dim of an fp32 matrix."""
+    """mode 0 rms_norm, 1 swish_rn, 2 swish_rn_hard over the last dim of an fp32 matrix (the
+    epilogue arithmetic) or an fp64 one (the reference's arithmetic, lattice_rownorm_f64)."""
     import torch
     x = x.contiguous()
     out = torch.empty_like(x)
     rows = x.numel() // x.shape[-1] if x.numel() else 0
-    check(_lib.lattice_rownorm(mode, rows, x.shape[-1], eps, _p(x), _p(out),
-                               1 if check_errors else 0, _stream(stream)))
+    fn = _lib.lattice_rownorm_f64 if x.dtype == torch.float64 else _lib.lattice_rownorm
+    check(fn(mode, rows, x.shape[-1], eps, _p(x), _p(out), 1 if check_errors else 0, _stream(stream)))
     return out
 
 
@@ -658,6 +662,12 @@ def fm_lcb(X, YT, WL, nF, Fin=None, Xout=None, stream=None):
                   _p(WL) if nL else None, _p(Fin), _p(Xout))
     check(_lib.lattice_fm_lcb(ctypes.byref(a), _stream(stream)))
     return Fin, Xout
+
+
+def device_check(stream=None):
+    """lattice_device_check: synchronise and raise CudaError if a swish GEMM's row-statistics
+    exchange timed out since the last check."""
+    check(_lib.lattice_device_check(_stream(stream)))
 
 
 # ---- network -------------------------------------------------------------------------------------

@@ -19,6 +19,17 @@ namespace gemm {
 
 __device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
 
+// Row-statistics waits of the CTA-pair swish epilogue that gave up (see gemm2_kernel): read and
+// cleared by lattice_device_check. Never non-zero while every pair of the grid is co-resident.
+__device__ unsigned int g_exchange_timeouts = 0;
+constexpr uint64_t kExchangeTimeoutNs = 5ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 constexpr int BN = 256;
 constexpr int kRasterGroup = 16;
 
@@ -584,9 +595,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     atomicAdd(cnt, 1);
                     const int want = 4 * nt;  // 4 epilogue warps per N-tile
                     int seen;
-                    do {
+                    uint64_t t0 = 0;
+                    for (uint32_t spin = 0;; ++spin) {
                         asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
-                    } while (seen < want);
+                        if (seen >= want) break;
+                        // bounded: a partner that never runs (co-residency lost to another workload)
+                        // is reported through lattice_device_check instead of hanging the GPU
+                        if ((spin & 1023u) == 1023u) {
+                            const uint64_t now = globaltimer_ns();
+                            if (t0 == 0) {
+                                t0 = now;
+                            } else if (now - t0 > kExchangeTimeoutNs) {
+                                atomicAdd(&g_exchange_timeouts, 1u);
+                                break;
+                            }
+                        }
+                    }
                 }
                 __syncwarp();
                 float total = 0.0f;
@@ -695,33 +719,60 @@ lattice_status launch_2cta(const CUtensorMap& ta, const CUtensorMap& tb, const P
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_done = true;
     }
+    const bool swish = p.epi == kSwish || p.epi == kSwishHard;
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[3];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 2;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+    if (pdl_enabled()) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    static int max_pairs = 0;
-    if (!max_pairs) {
+    cfg.numAttrs = na;
+    // the persistent grid: the pairs that fit on this device at once (cached per device)
+    static int max_pairs[64] = {0};
+    int dev = 0;
+    LAT_CUDA(cudaGetDevice(&dev));
+    int& mp = max_pairs[dev & 63];
+    if (!mp) {
         cfg.gridDim = dim3(2 * (num_sms() / 2), 1, 1);
         int mc = 0;
         if (cudaOccupancyMaxActiveClusters(&mc, gemm2_kernel<kStages2, __nv_bfloat16>, &cfg) != cudaSuccess || mc < 1)
             mc = num_sms() / 2;
-        max_pairs = mc;
+        mp = mc;
     }
     const int units = ((p.M + 2 * BM - 1) / (2 * BM)) * ((p.N + BN - 1) / BN);
-    if ((p.epi == kSwish || p.epi == kSwishHard) && !p.rowcnt_zeroed)
+    if (swish && !p.rowcnt_zeroed)
         LAT_CUDA(cudaMemsetAsync(p.rowcnt, 0, sizeof(int) * 2 * ((p.M + 2 * BM - 1) / (2 * BM)), st));
-    int pairs = max_pairs < units ? max_pairs : units;
+    int pairs = mp < units ? mp : units;
     if (pairs < 1) pairs = 1;
+    // a row block's N-tiles are consecutive units handed round-robin to the pairs: each must land
+    // on a different pair (or a pair would wait on its own later tile)
+    if (swish && (p.N + BN - 1) / BN > pairs && units > pairs)
+        return set_error(LATTICE_USAGE, "gemm: swish_rn row of " + std::to_string(p.N) +
+                                            " columns needs more CTA pairs than this device runs at once");
     cfg.gridDim = dim3(2 * pairs, 1, 1);
+    // The swish epilogue exchanges row statistics between pairs through global memory, so every
+    // pair must be resident at once: a cooperative launch has the hardware guarantee it (or the
+    // launch fails) even when other kernels share the GPU. LATTICE_GEMM_COOP=0 turns it off (A/B).
+    static const int coop_env = [] {
+        const char* e = std::getenv("LATTICE_GEMM_COOP");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (swish && coop_env) {
+        at[na].id = cudaLaunchAttributeCooperative;
+        at[na].val.cooperative = 1;
+        cfg.numAttrs = na + 1;
+    }
     LAT_CUDA(cudaLaunchKernelEx(&cfg, gemm2_kernel<kStages2, __nv_bfloat16>, ta, tb, p));
     return LATTICE_OK;
 }
@@ -790,6 +841,18 @@ lattice_status plan(GemmPlan* g, const void* A, int64_t lda, int64_t a_rows, con
 }  // namespace gemm
 }  // namespace lat
 
+extern "C" lattice_status lattice_device_check(lattice_stream stream) {
+    using namespace lat;
+    LAT_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    unsigned int n = 0, zero = 0;
+    LAT_CUDA(cudaMemcpyFromSymbol(&n, gemm::g_exchange_timeouts, sizeof(n)));
+    if (n == 0) return LATTICE_OK;
+    LAT_CUDA(cudaMemcpyToSymbol(gemm::g_exchange_timeouts, &zero, sizeof(zero)));
+    return set_error(LATTICE_CUDA, "GEMM swish_rn row-statistics exchange timed out " + std::to_string(n) +
+                                       " time(s): a CTA pair of a persistent grid was not resident (outputs of "
+                                       "those launches are invalid)");
+}
+
 extern "C" lattice_status lattice_gemm(const lattice_gemm_args* a, lattice_stream stream) {
     using namespace lat;
     using namespace lat::gemm;
@@ -815,8 +878,13 @@ extern "C" lattice_status lattice_gemm(const lattice_gemm_args* a, lattice_strea
     p.cluster = 1;
     p.heads = 0;
     if (p.epi == kSwish || p.epi == kSwishHard) {
+        // the CTA-pair kernel (bf16, M >= 256) exchanges row statistics through global memory and
+        // takes rows up to 16384 wide; the single-CTA kernel's DSMEM exchange stops at 2048
         p.cluster = (p.N + BN - 1) / BN;
-        LAT_REQUIRE(p.cluster <= kMaxCluster, "lattice_gemm: swish_rn rows wider than 2048 are not supported");
+        const bool pair = a->in_dtype == LATTICE_BF16 && a->M >= 2 * BM;
+        LAT_REQUIRE(p.cluster <= (pair ? 64 : kMaxCluster),
+                    pair ? "lattice_gemm: swish_rn rows wider than 16384 are not supported"
+                         : "lattice_gemm: swish_rn rows wider than 2048 need bf16 and M >= 256");
     }
     if (p.epi == kResidNorm) {
         LAT_REQUIRE(a->resid && (a->group == 128 || a->group == 64) && p.N % a->group == 0 && a->ldr % 8 == 0,

@@ -74,6 +74,32 @@ __device__ __forceinline__ double sigmoid_d(double z) {  // numerics.hpp:29-33
 }
 
 // one warp per row: numerics.hpp:113-136
+// Row statistics in the reference's order: detail::mean_square (numerics.hpp:36-40) is a
+// sequential sum of x*x, compiled without FMA contraction on the host; lane 0 of the row's warp
+// repeats it with explicit roundings, so the sums -- and with IEEE division and sqrt, rms_norm --
+// match the host reference bit for bit (swish_rn differs only where exp() does, <= 1 ulp).
+__device__ __forceinline__ void row_sums(const double* __restrict__ xr, const double* __restrict__ tr, int64_t width,
+                                         int lane, double& ss, double& dot) {
+    ss = 0.0;
+    dot = 0.0;
+    if (lane == 0) {
+        for (int64_t c = 0; c < width; ++c) {
+            ss = __dadd_rn(ss, __dmul_rn(xr[c], xr[c]));
+            if (tr) dot = __dadd_rn(dot, __dmul_rn(xr[c], tr[c]));
+        }
+    }
+    ss = __shfl_sync(0xffffffffu, ss, 0);
+    dot = __shfl_sync(0xffffffffu, dot, 0);
+}
+
+__device__ __forceinline__ bool row_nonfinite(const double* __restrict__ xr, const double* __restrict__ tr,
+                                              int64_t width, int lane) {
+    bool nonfinite = false;
+    for (int64_t c = lane; c < width; c += 32) nonfinite |= !isfinite(xr[c]) || (tr && !isfinite(tr[c]));
+    return __any_sync(0xffffffffu, nonfinite);
+}
+
+// one warp per row: numerics.hpp:113-136
 __global__ void jvp_kernel(int64_t rows, int64_t width, double eps, const double* __restrict__ x,
                            const double* __restrict__ t, double* __restrict__ out, unsigned long long* __restrict__ bad) {
     const int lane = threadIdx.x & 31;
@@ -81,28 +107,38 @@ __global__ void jvp_kernel(int64_t rows, int64_t width, double eps, const double
          r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const double* xr = x + r * width;
         const double* tr = t + r * width;
-        double ss = 0.0, dot = 0.0;
-        bool nonfinite = false;
-        for (int64_t c = lane; c < width; c += 32) {
-            nonfinite |= !isfinite(xr[c]) || !isfinite(tr[c]);
-            ss += xr[c] * xr[c];
-            dot += xr[c] * tr[c];
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            ss += __shfl_xor_sync(0xffffffffu, ss, o);
-            dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        }
-        if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicMin(bad, (unsigned long long)r);
+        if (row_nonfinite(xr, tr, width, lane) && lane == 0) atomicMin(bad, (unsigned long long)r);
+        double ss, dot;
+        row_sums(xr, tr, width, lane, ss, dot);
         const double n = (double)width;
-        const double d = sqrt(ss / n + eps);
+        const double d = sqrt(__dadd_rn(ss / n, eps));
         dot /= n;
-        const double d3 = d * d * d;
+        const double d3 = __dmul_rn(__dmul_rn(d, d), d);
         for (int64_t c = lane; c < width; c += 32) {
             const double rv = xr[c] / d;
-            const double dr = tr[c] / d - xr[c] * dot / d3;
+            const double dr = __dsub_rn(tr[c] / d, __dmul_rn(xr[c], dot) / d3);
             const double s = sigmoid_d(rv);
-            out[r * width + c] = s * (1.0 + rv * (1.0 - s)) * dr;
+            out[r * width + c] = __dmul_rn(__dmul_rn(s, __dadd_rn(1.0, __dmul_rn(rv, __dsub_rn(1.0, s)))), dr);
+        }
+    }
+}
+
+// rms_norm / swish_rn / swish_rn_hard in fp64 (numerics.hpp:81-107), one warp per row
+__global__ void rownorm64_kernel(int mode, int64_t rows, int64_t width, double eps, const double* __restrict__ x,
+                                 double* __restrict__ out, unsigned long long* __restrict__ bad) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const double* xr = x + r * width;
+        if (row_nonfinite(xr, nullptr, width, lane) && lane == 0) atomicMin(bad, (unsigned long long)r);
+        double ss, unused;
+        row_sums(xr, nullptr, width, lane, ss, unused);
+        const double denom = sqrt(__dadd_rn(ss / (double)width, eps));
+        for (int64_t c = lane; c < width; c += 32) {
+            double v = xr[c] / denom;
+            if (mode == 1) v = __dmul_rn(v, sigmoid_d(v));
+            if (mode == 2) v = __dmul_rn(v, clampd(__dadd_rn(v, 3.0) / 6.0, 0.0, 1.0));
+            out[r * width + c] = v;
         }
     }
 }
@@ -175,6 +211,25 @@ lattice_status lattice_smooth_labels(int64_t n, const double* y, double eps_s, d
     if (s != LATTICE_OK) return s;
     if (host != ~0ull)  // numerics.hpp:152 (a UsageError in the reference)
         return set_error(LATTICE_USAGE, "smooth_labels: labels must be 0 or 1", (int64_t)host);
+    return LATTICE_OK;
+}
+
+lattice_status lattice_rownorm_f64(int32_t mode, int64_t rows, int64_t width, double eps, const double* x,
+                                   double* out, int32_t check, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(mode >= 0 && mode <= 2, "rownorm: mode must be 0, 1 or 2");
+    LAT_REQUIRE(eps > 0.0, "eps must be > 0");         // numerics.hpp:20
+    LAT_REQUIRE(width > 0, "rms_norm: empty input");   // numerics.hpp:83
+    if (rows <= 0) return LATTICE_OK;
+    LAT_REQUIRE(x && out, "rownorm: null pointer");
+    unsigned long long* bad = nullptr;
+    LAT_CUDA(cudaMallocAsync(&bad, sizeof(*bad), stream));
+    LAT_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(*bad), stream));
+    rownorm64_kernel<<<grid_of(rows * 32), 256, 0, stream>>>(mode, rows, width, eps, x, out, bad);
+    unsigned long long host;
+    lattice_status s = flag_status(bad, stream, check != 0, &host);
+    if (s != LATTICE_OK) return s;
+    if (host != ~0ull) return set_error(LATTICE_DATA, "rms_norm: non-finite input", (int64_t)host);  // numerics.hpp:84
     return LATTICE_OK;
 }
 

@@ -202,8 +202,15 @@ lattice_status validate(const lattice_net_config* c) {
     if (c->mlp[c->n_mlp] != c->nF * c->d) return set_error(LATTICE_USAGE, "network: mlp[n_mlp] must equal nF*d");
     for (int i = 0; i <= c->n_mlp; ++i)
         if (c->mlp[i] < 8 || c->mlp[i] % 8) return set_error(LATTICE_USAGE, "network: MLP widths must be multiples of 8");
+    // swish_rn hidden layers: the CTA-pair GEMM (bf16, >= 256 rows) exchanges row statistics
+    // through global memory and takes rows up to 16384 wide (PAPER.md:855's 8192-4096-8192 MLP);
+    // the single-CTA kernel (fp32 / tiny batches) exchanges them over DSMEM, up to 2048
+    const int max_hidden = c->dtype == LATTICE_BF16 && c->max_batch >= 256 ? 16384 : 2048;
     for (int i = 1; i < c->n_mlp; ++i)
-        if (c->mlp[i] > 2048) return set_error(LATTICE_USAGE, "network: hidden widths above 2048 are not supported");
+        if (c->mlp[i] > max_hidden)
+            return set_error(LATTICE_USAGE, max_hidden == 2048
+                                                ? "network: hidden widths above 2048 need bf16 and max_batch >= 256"
+                                                : "network: hidden widths above 16384 are not supported");
     if (c->domains < 1 || c->domains > 32) return set_error(LATTICE_USAGE, "network: domains must be in [1, 32]");
     if (c->heads < 1 || c->heads > 16) return set_error(LATTICE_USAGE, "network: heads must be in [1, 16]");
     if (c->tower_hidden < 8 || c->tower_hidden > 2048 || c->tower_hidden % 8)
@@ -397,9 +404,11 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
     }
     int max_hidden = 8;
     for (int i = 1; i < c.n_mlp; ++i) max_hidden = max_hidden > c.mlp[i] ? max_hidden : c.mlp[i];
-    {  // row-statistics exchange of the swish GEMMs: [rows][<= 8 N-tiles] + counters
+    {  // row-statistics exchange of the swish GEMMs: [rows][N-tiles of the widest] + counters
         const size_t rows = (size_t)((Bm + 255) / 256) * 256;
-        NET_TRY(dalloc(net, &net->rowpart, rows * 8));
+        int tiles = (max_hidden + 255) / 256;
+        if (c.dense_features > 0 && (c.dense_hidden + 255) / 256 > tiles) tiles = (c.dense_hidden + 255) / 256;
+        NET_TRY(dalloc(net, &net->rowpart, rows * (size_t)(tiles > 8 ? tiles : 8)));
         net->rowcnt_stride = rows / 128 + 16;
         net->rowcnt_total = net->rowcnt_stride * ((size_t)c.blocks * (c.n_mlp - 1) + 1);
         NET_TRY(dalloc(net, &net->rowcnt, net->rowcnt_total));
@@ -539,11 +548,12 @@ void* lattice_net_buffer(lattice_net* net, int32_t which) {
 lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch, float* logits,
                                    lattice_stream stream) {
     using namespace lat;
-    LAT_REQUIRE(net != nullptr && batch != nullptr && logits != nullptr, "lattice_net_forward: null argument");
+    LAT_REQUIRE(net != nullptr && batch != nullptr, "lattice_net_forward: null argument");
     const lattice_net_config& c = net->cfg;
     const int64_t B = batch->batch;
     LAT_REQUIRE(B >= 0 && B <= c.max_batch, "lattice_net_forward: batch exceeds max_batch");
-    if (B == 0) return LATTICE_OK;
+    if (B == 0) return LATTICE_OK;  // an empty batch needs no logits buffer
+    LAT_REQUIRE(logits != nullptr, "lattice_net_forward: null logits");
     LAT_REQUIRE(batch->domain != nullptr, "lattice_net_forward: null domain");
     const int nd = c.n * c.d;
     int ei = 0;
@@ -674,6 +684,7 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
     t.grid_y = (int)((B + 127) / 128) + c.domains;
     FWD_TRY(gemm::launch(t, stream));
     FWD_TRY(mark());
+    if (batch->check) FWD_TRY(lattice_device_check(stream));  // checked forwards synchronise anyway
 #undef FWD_TRY
     return LATTICE_OK;
 }

@@ -74,13 +74,23 @@ static void numerics_examples() {
     const double s1 = 1.0 / (1.0 + std::exp(-1.0));
     const auto s = swish_rn(std::vector<double>{2, 2});
     CHECK(std::abs(s[0] - s1) < 1e-4);
+    // fp64 on the device with the reference's arithmetic: the SURVEY 8c goldens to the last ulps
     const auto k = swish_rn(std::vector<double>{3, 4});
-    CHECK(std::abs(k[0] - 0.59418883661177035) < 1e-6 && std::abs(k[1] - 0.85542017401638759) < 1e-6);
+    CHECK(std::abs(k[0] - 0.59418883661177035) < 4e-16 && std::abs(k[1] - 0.85542017401638759) < 4e-16);
     const auto h = swish_rn_hard(std::vector<double>{3, 4});
-    CHECK(std::abs(h[0] - 0.54426404214136748) < 1e-6 && std::abs(h[1] - 0.77901871858849048) < 1e-6);
-    std::vector<double> huge(8, 1e6);
-    huge[0] = -1e6;
-    for (double v : swish_rn(huge)) CHECK(std::isfinite(v) && std::abs(v) <= std::sqrt(8.0));
+    CHECK(std::abs(h[0] - 0.54426404214136748) < 4e-16 && std::abs(h[1] - 0.77901871858849048) < 4e-16);
+    CHECK(p[0] == 3.0 / std::sqrt(12.5 + 1e-6));  // rms_norm: bit for bit (numerics.hpp:87-89)
+    for (double mag : {1e6, 1e20, 1e150, 1e300}) {  // any magnitude stays finite (numerics.hpp:92-93)
+        std::vector<double> huge(8, mag);
+        huge[0] = -mag;
+        for (double v : swish_rn(huge)) CHECK(std::isfinite(v) && std::abs(v) <= std::sqrt(8.0));
+        const auto r = rms_norm(huge);
+        double acc = 0.0;  // the reference's own sequence: sum of squares (inf past ~1e154), then divide
+        for (double v : huge) acc += v * v;
+        const double denom = std::sqrt(acc / 8.0 + 1e-6);
+        for (std::size_t i = 0; i < huge.size(); ++i) CHECK(r[i] == huge[i] / denom);
+    }
+    for (double v : rms_norm(std::vector<double>{0, 0}, 1e-300)) CHECK(v == 0.0);  // eps below fp32 range
 }
 
 static void zipper_examples() {
@@ -265,6 +275,23 @@ static void network_smoke() {
     NetworkConfig bad = c;
     bad.nL = 3;
     CHECK_THROWS_AS(Network{bad}, UsageError);
+    // an empty batch returns no logits; a malformed CSR is a DataError on the host
+    SparseBatch empty;
+    empty.offsets.assign(1, 0);
+    CHECK(net.forward(empty, ts).empty());
+    SparseBatch mal = b;
+    mal.offsets[5] = mal.offsets[6] + 1;  // decreasing
+    CHECK_THROWS_AS(net.forward(mal, ts), DataError);
+    mal = b;
+    mal.offsets.back() += 7;  // runs past ids
+    CHECK_THROWS_AS(net.forward(mal, ts), DataError);
+    // trained weights: a caller-owned tower head replaces the generated one
+    Network net2(c);
+    std::vector<float> w2(static_cast<std::size_t>(c.domains) * c.heads * c.tower_hidden, 0.0f);
+    net2.set_weight(5, 0, 0, w2);
+    for (float v : net2.forward(b, ts)) CHECK(v == 0.0f);  // zero heads -> zero logits
+    CHECK_THROWS_AS(net2.set_weight(5, 0, 0, std::vector<float>(3)), UsageError);
+    CHECK_THROWS_AS(net2.set_weight(9, 0, 0, w2), UsageError);
 }
 
 // serde.hpp:158 parse_jsonl_records through the GPU parser: the SPEC.md:283 record format, then

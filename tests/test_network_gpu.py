@@ -186,6 +186,16 @@ def test_large_backbone_real_widths():
     full_check("large_real_widths", LARGE, 512, 20000, oracle_samples=4, chunk=128)
 
 
+# the paper's internal MLP widths 8192 and 4096 (hidden swish_rn rows wider than
+# 2048, VERDICT r01 missing 8); widths arranged so the last layer is nF*d
+WIDE_HIDDEN = dict(n=64, d=128, blocks=2, nF=32, nL=32, k=16, mlp=[1024, 8192, 4096, 4096], domains=3, heads=4,
+                   tower_hidden=256)
+
+
+def test_hidden_widths_above_2048():
+    full_check("wide_hidden_8192_4096", WIDE_HIDDEN, 600, 4000, oracle_samples=16)
+
+
 def test_mid_config_matches_restatements():
     full_check("mid_B2048", MID, 2048, 20000, oracle_samples=64, chunk=1024)
 
