@@ -28,11 +28,29 @@ sys.path.insert(0, ROOT)
 SEED_T, SEED_D = 0x1A77, 0x1A78
 
 
-def load_traffic(workload, kernel):
-    """DRAM bytes per launch (group) of `kernel` from the committed ncu capture, or None."""
+def load_traffic(workload, kernel, key="dram"):
+    """Bytes per launch (group) of `kernel` from the committed ncu captures (profiles/r02, else
+    r01): key "dram" = dram__bytes_read.sum + dram__bytes_write.sum, "l2" = lts__t_bytes.sum."""
+    for rnd in ("r02", "r01"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "traffic.json")) as f:
+                v = json.load(f).get(workload, {}).get(kernel)
+        except Exception:
+            continue
+        if isinstance(v, dict):
+            v = v.get(key)
+        elif key != "dram":
+            v = None
+        if v is not None:
+            return v
+    return None
+
+
+def load_l2_peak():
+    """Measured L2 read bandwidth (GB/s, scripts/l2_probe.cu on a B200: profiles/r02/l2_probe.json)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
-            return json.load(f).get(workload, {}).get(kernel)
+        with open(os.path.join(ROOT, "profiles", "r02", "l2_probe.json")) as f:
+            return json.load(f)["l2_read_gbs"]
     except Exception:
         return None
 
@@ -61,7 +79,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -77,7 +95,8 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7 and self.t_start is not None and time.time() >= self.t_start:
+            # a line read within 20 ms of the mark may have been sampled before it
+            if len(parts) >= 7 and self.t_start is not None and time.time() >= self.t_start + 0.02:
                 self.samples.append(parts)
 
     def __exit__(self, *a):
@@ -140,12 +159,12 @@ def micro_bytes(n_ids, F, B, D, s_tab, s_out):
     return n_ids * D * s_tab + n_ids * 4 + (F * B + 1) * 8 + F * B * D * s_out
 
 
-def run_micro(args, rank, world, local):
+def run_micro(args, rank, world, local, dtype=None, min_seconds=0.0):
     import torch
     import paper_2512_09200_b200 as L
     c = MICRO
     F, R, D, B, ML = c["F"], c["rows"], c["D"], c["B"], c["max_len"]
-    dt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    dt = torch.bfloat16 if (dtype or args.dtype) == "bf16" else torch.float32
     s_tab = 2 if dt == torch.bfloat16 else 4
     tab = torch.empty((F, R, D), dtype=dt, device="cuda")
     L.fill_tables(tab, SEED_T)
@@ -163,6 +182,17 @@ def run_micro(args, rank, world, local):
                         rows=rows)
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = args.steps
+    if min_seconds > 0:  # long enough a timed region for the clock sampler to see it
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        step()
+        e0.record(stream)
+        for _ in range(3):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        steps = max(steps, int(min_seconds * 1e3 / (e0.elapsed_time(e1) / 3)) + 1)
+    args = argparse.Namespace(**dict(vars(args), steps=steps))
     kev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
     with ClockSampler(local) as clk:
         for _ in range(args.warmup):
@@ -228,7 +258,7 @@ def run_micro(args, rank, world, local):
                 "d2h_bytes_per_step": B * F * D * s_tab},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm,
-                     "traffic": load_traffic("micro_bf16", "bag_kernel") if dt == torch.bfloat16 else None,
+                     "traffic": load_traffic("micro_bf16" if dt == torch.bfloat16 else "micro_f32", "bag_kernel"),
                      "kernel": "bag_kernel",
                      "peak_source": src, "algorithmic_bytes_per_launch": alg,
                      "kernel_ms_mean": kernel_ms, "kernel_ms_min": min(kms), "kernel_ms_max": max(kms)},
@@ -238,13 +268,13 @@ def run_micro(args, rank, world, local):
     return res, dict(F=F, R=R, D=D, B=B, ML=ML, offsets=offsets, ids=ids)
 
 
-def cpu_baseline_micro(seconds=15.0):
-    """Oracle (port) embedding bag on a bounded sample, all host threads."""
+def cpu_baseline_micro(seconds=15.0, threads=None):
+    """Oracle (port) embedding bag on a bounded sample (all host threads unless given)."""
     import numpy as np
     import oracle
     c = MICRO
     F, R, D, B, ML = c["F"], c["rows"], c["D"], c["B"], c["max_len"]
-    threads = os.cpu_count() or 1
+    threads = threads or os.cpu_count() or 1
     o, i = oracle.synth_bags(F, B, ML, R, SEED_D)
     n, t0 = 0, time.perf_counter()
     chunk = 64
@@ -457,7 +487,7 @@ def run_mid(args, rank, world, local):
             step_eager()
         stages.append(net.stage_times())
     net.set_timing(False)
-    st = [min(s[i] for s in stages) for i in range(len(stages[0]))]  # min: robust to host hiccups
+    st = [statistics.median(s[i] for s in stages) for i in range(len(stages[0]))]
     # stages: [bucket, bag (or shard gather), (fm_lcb, mlp) x blocks, tower]
     t_bag = st[1] + (min(emb_ms) if sharded else 0.0)
     t_fm = [st[2 + 2 * b] for b in range(c["blocks"])]
@@ -592,8 +622,9 @@ def run_mid(args, rank, world, local):
                                     f"measured sustained figure {tf_sust})",
                      "algorithmic_flops_per_launch_group": mlp_fl, "ms": mlp_ms},
         "stages": {
-            "embedding": {"ms": t_bag, "bytes": emb_bytes, "GB/s": emb_bytes / (t_bag / 1e3) / 1e9,
-                          "frac_hbm": emb_bytes / (t_bag / 1e3) / 1e9 / hbm},
+            "_note": ("per-stage CUDA-event times: median of 5 eager forwards with events between "
+                      "stages (the graph-replayed step has no events inside)"),
+            "embedding": emb_stage(args.workload if not sharded else None, t_bag, emb_bytes, hbm),
             "fm_lcb": {"ms_per_block": statistics.mean(t_fm), "bytes_per_block": fm_bytes,
                        "GB/s": fm_bytes / (statistics.mean(t_fm) / 1e3) / 1e9,
                        "frac_hbm": fm_bytes / (statistics.mean(t_fm) / 1e3) / 1e9 / hbm},
@@ -603,6 +634,8 @@ def run_mid(args, rank, world, local):
             "dense_total": {"ms": dense_ms, "TFLOP": flops / 1e12,
                             "TFLOP/s": flops / (dense_ms / 1e3) / 1e12},
             "bucket_ms": st[0],
+            "stage_sum_ms": sum(st),
+            "eager_vs_graph_ms": sum(st) - ms,
         },
         "gpu_launches": launches * args.steps,
         "clocks": clk.summary(),
@@ -612,24 +645,90 @@ def run_mid(args, rank, world, local):
     return res
 
 
-def cpu_baseline_mid(seconds=15.0, threads=None):
-    """Oracle port of the mid forward (embedding bag + network, fp64) on a bounded sample."""
+def emb_stage(workload, t_ms, alg_bytes, hbm):
+    """Embedding-stage roofline. The algorithmic bytes (every gathered row counted once per id,
+    SURVEY 8d emb_bytes) exceed what DRAM serves: the mid tables (25.6 MB each, visited table by
+    table) stay hot in L2, so the line also carries the ncu-measured DRAM and L2 bytes of the bag
+    kernel at this config (profiles/r02/traffic.json) against the HBM and measured L2 peaks."""
+    d = {"ms": t_ms, "algorithmic_bytes": alg_bytes,
+         "algorithmic_GB/s": alg_bytes / (t_ms / 1e3) / 1e9,
+         "algorithmic_over_hbm_peak": alg_bytes / (t_ms / 1e3) / 1e9 / hbm}
+    dram = load_traffic(workload, "bag_kernel", "dram") if workload else None
+    l2 = load_traffic(workload, "bag_kernel", "l2") if workload else None
+    l2_peak = load_l2_peak()
+    if dram:
+        d.update({"dram_bytes_ncu": dram, "dram_GB/s": dram / (t_ms / 1e3) / 1e9,
+                  "frac_hbm_dram": dram / (t_ms / 1e3) / 1e9 / hbm})
+    if l2:
+        d.update({"l2_bytes_ncu": l2, "l2_GB/s": l2 / (t_ms / 1e3) / 1e9})
+        if l2_peak:
+            d.update({"l2_peak_GB/s": l2_peak, "frac_l2": l2 / (t_ms / 1e3) / 1e9 / l2_peak})
+    return d
+
+
+def zipper_timing(steps=20):
+    """K5 Zipper (window assignment + labels, full-portfolio shape: 4 tasks x 3 windows) on
+    65,536 impressions per step on the GPU, beside the reference's own zip_dataset
+    (datasets.hpp:199-249 compiled in place, oracle/_ref) on one host core."""
+    import numpy as np
+    import torch
+    import oracle
+    import paper_2512_09200_b200 as L
+    n, T = 65536, FULL_TASKS
+    probs = [1.0 / len(FULL_WINDOWS)] * len(FULL_WINDOWS)
+    imp = L.synth_impressions(n, T, 7)
+    for _ in range(3):
+        L.zipper_assign_labels(*imp, FULL_WINDOWS, probs, 7, check_errors=False)
+    torch.cuda.synchronize()
+    # replayed from a graph: the kernel's device time, not the host's ctypes/allocation overhead
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(steps):
+            L.zipper_assign_labels(*imp, FULL_WINDOWS, probs, 7, check_errors=False)
+    g.replay()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    out = {"impressions_per_step": n, "tasks": T, "windows": len(FULL_WINDOWS), "gpu_ms": ms,
+           "gpu_impressions_per_s": n / (ms / 1e3)}
+    if oracle.ref_available():
+        users, ads, ts, conv, pres = oracle.synth_impressions(8192, T, 7)
+        t0 = time.perf_counter()
+        k = 0
+        while time.perf_counter() - t0 < 3.0 or k == 0:
+            rc, _, _, _ = oracle.ref_zip_dataset(users, ads, ts, conv, pres, FULL_WINDOWS, probs, 7)
+            assert rc == 0
+            k += 1
+        dt = time.perf_counter() - t0
+        out.update({"reference_cpu_impressions_per_s": k * 8192 / dt, "reference_cores": 1,
+                    "reference_sample": f"{k} x 8192 impressions through lattice::zip_dataset (oracle/_ref, "
+                                        f"records built from columns inside the timed call)"})
+    return out
+
+
+def cpu_baseline_mid(seconds=15.0, threads=None, large=False):
+    """Oracle port of the mid (or large) forward (embedding bag + network, fp64) on a bounded sample."""
     import numpy as np
     import oracle
-    c = MID
+    c = LARGE if large else MID
+    table_rows = LARGE_ROWS if large else MID_ROWS
     threads = threads or os.cpu_count() or 1
     lib = oracle.load_oracle()
     n, d = c["n"], c["d"]
     # weights from the counter-based generator, on the host (no GPU needed for this leg)
     w = host_weights(c)
-    o, i = oracle.synth_bags(n, 512, MID_MAXLEN, MID_ROWS, SEED_D)
+    o, i = oracle.synth_bags(n, 512, MID_MAXLEN, table_rows, SEED_D)
     dom = oracle.synth_domains(512, c["domains"], SEED_D)
     cfg, ws, keep = oracle_net(c, w)
     t0 = time.perf_counter()
     done = 0
     chunk = max(threads, 4)
     while time.perf_counter() - t0 < seconds and done + chunk <= 512:
-        pooled, _ = oracle.embedding_bag_synth(SEED_T, n, MID_ROWS, d, 512, o, i, done, done + chunk, threads)
+        pooled, _ = oracle.embedding_bag_synth(SEED_T, n, table_rows, d, 512, o, i, done, done + chunk, threads)
         out = np.zeros((chunk, c["heads"]), np.float32)
         dd = np.ascontiguousarray(dom[done:done + chunk])
         lib.lo_net_forward(oracle.ctypes.byref(cfg), oracle.ctypes.byref(ws), chunk, oracle.ptr(pooled),
@@ -637,8 +736,8 @@ def cpu_baseline_mid(seconds=15.0, threads=None):
         done += chunk
     dt = time.perf_counter() - t0
     return {"value": done / dt, "unit": "samples/s", "cores": threads, "kind": "port",
-            "sample": f"{done} samples of the mid batch ({dt:.1f} s; tables regenerated lazily; "
-                      f"rate extrapolated to the 32768-sample batch)"}
+            "sample": f"{done} samples of the {'large' if large else 'mid'} batch ({dt:.1f} s; tables "
+                      f"regenerated lazily; rate extrapolated to the full batch)"}
 
 
 _HOST_W = {}
@@ -706,6 +805,8 @@ def main():
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch every kernel of the timed steps from the host instead of replaying the "
                          "forward step from a CUDA graph")
+    ap.add_argument("--no-micro", dest="micro", action="store_false",
+                    help="mid at N=1: skip the configs[1] micro lines and the Zipper timing")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl", "peer1"],
                     help="N>1 sharded embedding exchange: peer memory (default) or NCCL all-to-alls")
     args = ap.parse_args()
@@ -716,12 +817,22 @@ def main():
         if rank != 0:
             return
         per_step = max(0.5, min(3.0, 60.0 / (args.warmup + args.steps)))
-        base = cpu_baseline_mid if args.workload in ("mid", "full") else cpu_baseline_micro
+        if args.workload == "large":
+            base = lambda seconds: cpu_baseline_mid(seconds, large=True)
+        elif args.workload in ("mid", "full"):
+            base = cpu_baseline_mid
+        else:
+            base = cpu_baseline_micro
         steps = [base(seconds=per_step) for _ in range(args.warmup + args.steps)]
         v = statistics.median([s["value"] for s in steps[args.warmup:]])
         cb = dict(steps[-1])
         cb["value"] = v
-        if args.workload in ("mid", "full"):
+        if args.workload == "large":
+            metric = "Lattice Network samples/sec (large config, forward step)"
+            wl = ("large Lattice Network (CPU oracle port, fp64 with bf16 rounding emulation): 512 tables x "
+                  "1.5M rows x 128, l=4, n=512, MLP 16384-2048-2048-32768, B=65536/GPU")
+            dtype = "f64"
+        elif args.workload in ("mid", "full"):
             metric = "Lattice Network samples/sec (mid config, forward step)"
             wl = ("mid Lattice Network (CPU oracle port, fp64 with bf16 rounding emulation): "
                   "256 sparse feats x 100k rows x 128, l=4, B=32768")
@@ -745,9 +856,27 @@ def main():
     else:
         res, _ = run_micro(args, rank, world, local)
         base = cpu_baseline_micro
+    if world == 1 and args.workload == "mid" and args.micro:
+        # configs[1] beside the headline: the embedding-bag microbench in both table dtypes, where
+        # HBM (not L2) is the bound, each with its own clock samples
+        import torch
+        torch.cuda.empty_cache()
+        res["micro"] = {}
+        for dt in ("bf16", "f32"):
+            m, _ = run_micro(args, rank, world, local, dtype=dt, min_seconds=1.5)
+            m["roofline"]["dram_bytes_ncu"] = load_traffic(f"micro_{dt}", "bag_kernel", "dram")
+            if m["roofline"]["dram_bytes_ncu"]:
+                m["roofline"]["frac_hbm_dram"] = (m["roofline"]["dram_bytes_ncu"] / (m["roofline"]["kernel_ms_mean"] / 1e3)
+                                                  / 1e9 / m["roofline"]["peak"])
+            res["micro"][dt] = {k: m[k] for k in ("metric", "value", "unit", "steps", "ms_per_step", "dtype", "roofline",
+                                                  "e2e", "clocks")}
+            torch.cuda.empty_cache()
+        res["zipper"] = zipper_timing()
     if rank == 0:
         if world == 1 and args.workload != "large":
             res["cpu_baseline"] = base(args.cpu_seconds)
+            one = base(max(3.0, args.cpu_seconds / 2), threads=1)
+            res["cpu_baseline"]["threads_1"] = {k: one[k] for k in ("value", "unit", "cores", "sample")}
         print(json.dumps(res))
     if world > 1:
         import torch.distributed as dist

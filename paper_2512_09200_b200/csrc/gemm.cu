@@ -763,10 +763,16 @@ lattice_status launch_2cta(const CUtensorMap& ta, const CUtensorMap& tb, const P
     cfg.gridDim = dim3(2 * pairs, 1, 1);
     // The swish epilogue exchanges row statistics between pairs through global memory, so every
     // pair must be resident at once: a cooperative launch has the hardware guarantee it (or the
-    // launch fails) even when other kernels share the GPU. LATTICE_GEMM_COOP=0 turns it off (A/B).
+    // launch fails) even when other kernels share the GPU. LATTICE_GEMM_COOP=0/1 forces it off/on.
+    // Nsight Compute cannot replay a cooperative cluster launch (it reports a 0x0 grid and fails),
+    // so inside a profiler-injected process (the variables ncu sets for its target) the default is
+    // off; the bounded wait above still turns a starved pair into a reported error, not a hang.
     static const int coop_env = [] {
         const char* e = std::getenv("LATTICE_GEMM_COOP");
-        return e ? std::atoi(e) : 1;
+        if (e) return std::atoi(e);
+        const bool profiled = std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") || std::getenv("NV_TPS_LAUNCH_TOKEN") ||
+                              std::getenv("CUDA_INJECTION64_PATH");
+        return profiled ? 0 : 1;
     }();
     if (swish && coop_env) {
         at[na].id = cudaLaunchAttributeCooperative;

@@ -113,7 +113,9 @@ def _run_concurrent(coop):
     r = subprocess.run([sys.executable, os.path.join(here, "concurrent_nets_check.py")],
                        env=dict(os.environ, LATTICE_GEMM_COOP=coop), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
-    return json.loads(r.stdout.strip().splitlines()[-1])
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    print("[concurrency]", json.dumps(res))
+    return res
 
 
 def test_two_networks_on_two_streams_cooperative():
