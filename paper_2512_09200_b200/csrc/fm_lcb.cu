@@ -24,7 +24,9 @@
 // stage lands so the stage is recycled right after the MMAs.
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "fm_lcb.h"
@@ -34,10 +36,6 @@
 namespace lat {
 namespace fm {
 
-// large variant: 4 LCB + 4 FM epilogue warps
-constexpr int kEpiWarps = 8;
-constexpr int kEpiThreads = kEpiWarps * 32;
-constexpr int kThreads = 64 + kEpiThreads;
 // resident variant: 8 LCB warps (a warp pair per TMEM lane quarter, half of the d columns
 // each) + 4 FM warps, so the latency-bound LCB epilogue has two warps per sub-partition
 constexpr int kLcbWarps = 8;
@@ -464,68 +462,112 @@ __global__ void __launch_bounds__(kResThreads, 1)
 }
 
 // ---------------------------------------------------------------------------------------------
-// Large-n variant (256 < n <= 512, nL <= 256, d = 128, bf16): X_b (128 KB) fits only once, and
-// W_L (nL x n, up to 256 KB) cannot stay resident, so W_L streams from L2 through a TMA ring of
-// [128 x 64] panels (shared by every CTA, it stays L2-resident). Accumulators: P | L (2 M-tiles)
-// | F (4 M-tiles) in one TMEM region. Same warp roles as the resident variant.
+// Large-n variant (256 < n <= 512, nL <= 256, d = 128, bf16). X_b (n_pad x d = 128 KB) fits only
+// once and W_L (nL x n, up to 256 KB) cannot stay resident, so the kernel streams:
+//   * X_b in four 128-row chunks, each with its own full/empty barrier. Chunk c is released as
+//     soon as the F MMAs of M-tile c are done and the LCB threads whose residual rows it holds
+//     have read them, so the next sample's chunks load while this sample's F MMAs and epilogues
+//     run, and its P/L MMAs start on chunk 0 as it lands (the chunks holding LCB rows, read last,
+//     are needed last).
+//   * W_L in [128 x 64] panels (16 KB) through a deep TMA ring (4-5 stages; Y^T also streams, in
+//     [k_pad x 64] panels, so the ring gets its 32 KB), in K-outer order: for each 64-row K panel
+//     of X both L M-tiles and P advance, so P/L consume X chunk by chunk.
+// Warps: 0 X producer, 1 MMA issuer, 2 W_L / Y^T producer, 3..10 LCB group (8 warps: TMEM lane
+// quarter x L M-tile; the M-tile-0 warps also route P to the bf16 Pbuf), 11..14 FM group. TMEM:
+// P | L (2 M-tiles) | F (4 M-tiles) in one 512-column region, with separate "drained" barriers
+// for P+L (LCB group) and F (FM group), so this sample's FM epilogue overlaps the next sample's
+// P/L MMAs.
 // ---------------------------------------------------------------------------------------------
-constexpr int kWlStages = 3;
+// Wait-site profiling (LATTICE_FM_TRACE=1, lattice_fm_lcb only): cycles each role spends blocked
+// per barrier, summed per CTA -- the pipeline's critical path without a profiler.
+#define FM_WAIT(site, bar, parity)                                                \
+    do {                                                                          \
+        if (p.trace) {                                                            \
+            const long long _t0 = clock64();                                      \
+            tc::mbar_wait(bar, parity);                                           \
+            wt[site] += (unsigned long long)(clock64() - _t0);                    \
+        } else {                                                                  \
+            tc::mbar_wait(bar, parity);                                           \
+        }                                                                         \
+    } while (0)
+
+constexpr int kLargeWarps = 15;
+constexpr int kLargeThreads = kLargeWarps * 32;
+constexpr int kYtStages = 2;
 
 struct GeoL {
-    int panels_n, ml, mf;
-    uint32_t xpanel, ytpanel, ppanel, wlpanel;
+    int panels_n, ml, mf, chunks, wl_stages;
+    uint32_t xpanel, ytpanel, ppanel, wlpanel, pbytes;
     __host__ __device__ GeoL(const Params& p) {
         panels_n = p.n_pad / 64;
         ml = (p.nL + 127) / 128;
         mf = p.n_pad / 128;
+        chunks = p.n_pad / 128;
         xpanel = (uint32_t)p.n_pad * 128u;
         ytpanel = (uint32_t)p.k_pad * 128u;
         ppanel = (uint32_t)p.k_pad * 128u;
         wlpanel = 128u * 128u;
+        pbytes = (2 * ppanel + 1023u) & ~1023u;
+        // as many W_L stages as fit next to X, the Y^T ring and Pbuf (227 KB per CTA)
+        const int64_t left = 227 * 1024 - 1024 - 512 - 2 * (int64_t)xpanel - kYtStages * (int64_t)ytpanel - pbytes;
+        wl_stages = (int)(left / wlpanel);
+        if (wl_stages > 5) wl_stages = 5;
     }
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kLargeThreads, 1)
     fm_lcb_large_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWL,
                         const __grid_constant__ CUtensorMap tmYT, const Params p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-    const int npad = p.n_pad, kpad = p.k_pad;
+    const int kpad = p.k_pad;
     constexpr int d = 128;
     const GeoL g(p);
-    uint8_t* sX = smem;                                   // [2 panels][n_pad][64]
-    uint8_t* sWL = sX + 2 * g.xpanel;                     // ring [kWlStages][128][64]
-    uint8_t* sYT = sWL + kWlStages * g.wlpanel;           // [panels_n][k_pad][64]
-    uint8_t* sP = sYT + g.ytpanel * g.panels_n;           // [2 panels][k_pad][64]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + ((2 * g.ppanel + 1023u) & ~1023u));
-    uint64_t* x_full = bars;
-    uint64_t* x_empty = bars + 1;
-    uint64_t* pl_full = bars + 2;
-    uint64_t* f_full = bars + 3;
-    uint64_t* tmem_empty = bars + 4;
-    uint64_t* w_full = bars + 5;
-    uint64_t* pbuf_full = bars + 6;
-    uint64_t* wl_full = bars + 7;               // [kWlStages]
-    uint64_t* wl_empty = wl_full + kWlStages;   // [kWlStages]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wl_empty + kWlStages);
-    float* red_f = reinterpret_cast<float*>(wl_empty + kWlStages + 1);  // [2][4]
+    const int NW = g.wl_stages;
+    uint8_t* sX = smem;                                   // [2 d-panels][n_pad rows][128 B]
+    uint8_t* sWL = sX + 2 * g.xpanel;                     // ring [NW][128 rows][128 B]
+    uint8_t* sYT = sWL + NW * g.wlpanel;                  // ring [kYtStages][k_pad rows][128 B]
+    uint8_t* sP = sYT + kYtStages * g.ytpanel;            // [2 d-panels][k_pad][128 B]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + g.pbytes);
+    uint64_t* x_full = bars;                  // [4] chunk landed
+    uint64_t* x_empty = bars + 4;             // [4] chunk consumed (its F M-tile done)
+    uint64_t* wl_full = bars + 8;             // [NW <= 5]
+    uint64_t* wl_empty = bars + 13;           // [NW]
+    uint64_t* yt_full = bars + 18;            // [2]
+    uint64_t* yt_empty = bars + 20;           // [2]
+    uint64_t* pl_full = bars + 22;            // P and L accumulated
+    uint64_t* pbuf_full = bars + 23;          // P routed to Pbuf (bf16)
+    uint64_t* f_full = bars + 24;             // F accumulated
+    uint64_t* l_empty = bars + 25;            // P + L region drained (LCB group)
+    uint64_t* f_empty = bars + 26;            // F region drained (FM group)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 27);
+    float* red_f = reinterpret_cast<float*>(bars + 28);   // [2][4]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0 && lane == 0) {
         tc::tma_prefetch(&tmX);
         tc::tma_prefetch(&tmWL);
         tc::tma_prefetch(&tmYT);
-        tc::mbar_init(x_full, 1);
-        tc::mbar_init(x_empty, kEpiThreads);
-        tc::mbar_init(pl_full, 1);
-        tc::mbar_init(f_full, 1);
-        tc::mbar_init(tmem_empty, kEpiThreads);
-        tc::mbar_init(w_full, 1);
-        tc::mbar_init(pbuf_full, 128);
-        for (int i = 0; i < kWlStages; ++i) {
+        for (int c = 0; c < 4; ++c) {
+            // chunk c is released by its F M-tile's MMA commit and by the LCB threads whose
+            // residual row X[nF+i] lies in it (they pick it up into registers when it lands)
+            const int lo = max(128 * c, p.nF), hi = min(128 * c + 128, p.nF + p.nL);
+            tc::mbar_init(&x_full[c], 1);
+            tc::mbar_init(&x_empty[c], 1 + (hi > lo ? hi - lo : 0));
+        }
+        for (int i = 0; i < NW; ++i) {
             tc::mbar_init(&wl_full[i], 1);
             tc::mbar_init(&wl_empty[i], 1);
         }
+        for (int i = 0; i < kYtStages; ++i) {
+            tc::mbar_init(&yt_full[i], 1);
+            tc::mbar_init(&yt_empty[i], 1);
+        }
+        tc::mbar_init(pl_full, 1);
+        tc::mbar_init(pbuf_full, 128);
+        tc::mbar_init(f_full, 1);
+        tc::mbar_init(l_empty, 8 * 32);
+        tc::mbar_init(f_empty, 4 * 32);
         tc::fence_mbar_init();
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
@@ -533,54 +575,77 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t t_Pb = tmem, t_Lb = tmem + 64, t_Fb = tmem + 64 + 128 * 2;
-    if (!(warp == 0 && lane == 0)) tc::griddep_wait();  // PDL, as in fm_lcb_kernel
+    const uint32_t t_Pb = tmem, t_Lb = tmem + 64, t_Fb = tmem + 64 + 2 * 128;
+    // PDL: everything above overlaps the preceding kernel's tail; X (and the outputs) after this
+    tc::griddep_wait();
     tc::griddep_launch_dependents();
 
     if (warp == 0) {
-        if (lane == 0) {  // ---- TMA producer: X (4 boxes), then the W_L panel stream
-            tc::mbar_expect_tx(w_full, g.ytpanel * g.panels_n);
-            for (int pn = 0; pn < g.panels_n; ++pn) tc::tma_load_2d(sYT + pn * g.ytpanel, &tmYT, w_full, pn * 64, 0);
-            tc::griddep_wait();
-            int it = 0, gw = 0;
+        if (lane == 0) {  // ---- X producer: four 128-row chunks per sample, two d-panels each
+            unsigned long long wt[16] = {0};
+            int it = 0;
             for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
-                tc::mbar_wait(x_empty, (it & 1) ^ 1);
-                tc::mbar_expect_tx(x_full, (uint32_t)npad * 128u * 2u);
-                for (int pd = 0; pd < 2; ++pd)
-                    for (int h = 0; h < npad / 256; ++h)
-                        tc::tma_load_3d(sX + pd * g.xpanel + h * 256 * 128, &tmX, x_full, pd * 64, h * 256, (int)b);
-                for (int mt = 0; mt < g.ml; ++mt)
-                    for (int kp = 0; kp < g.panels_n; ++kp, ++gw) {
-                        const int s = gw % kWlStages;
-                        tc::mbar_wait(&wl_empty[s], ((gw / kWlStages) & 1) ^ 1);
+                for (int c = 0; c < g.chunks; ++c) {
+                    FM_WAIT(8, &x_empty[c], (it & 1) ^ 1);
+                    tc::mbar_expect_tx(&x_full[c], 2u * 128u * 128u);
+                    for (int pd = 0; pd < 2; ++pd)
+                        tc::tma_load_3d(sX + pd * g.xpanel + c * 16384, &tmX, &x_full[c], pd * 64, c * 128, (int)b);
+                }
+            }
+            if (p.trace) p.trace[blockIdx.x * 16 + 8] = wt[8];
+        }
+    } else if (warp == 2) {
+        if (lane == 0) {  // ---- W_L / Y^T producer, in the MMA's K-outer order
+            unsigned long long wt[16] = {0};
+            int gw = 0, gy = 0;
+            for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
+                for (int kp = 0; kp < g.panels_n; ++kp) {
+                    const int sy = gy % kYtStages;
+                    FM_WAIT(9, &yt_empty[sy], ((gy / kYtStages) & 1) ^ 1);
+                    tc::mbar_expect_tx(&yt_full[sy], g.ytpanel);
+                    tc::tma_load_2d(sYT + sy * g.ytpanel, &tmYT, &yt_full[sy], kp * 64, 0);
+                    ++gy;
+                    for (int mt = 0; mt < g.ml; ++mt, ++gw) {
+                        const int s = gw % NW;
+                        FM_WAIT(10, &wl_empty[s], ((gw / NW) & 1) ^ 1);
                         tc::mbar_expect_tx(&wl_full[s], g.wlpanel);
                         tc::tma_load_2d(sWL + s * g.wlpanel, &tmWL, &wl_full[s], kp * 64, mt * 128);
                     }
+                }
             }
+            if (p.trace) p.trace[blockIdx.x * 16 + 9] = wt[9], p.trace[blockIdx.x * 16 + 10] = wt[10];
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---- MMA issuer
             const uint32_t id_P = tc::idesc_bf16(128, kpad, 1, 0);
             const uint32_t id_L = tc::idesc_bf16(128, d, 0, 1);
             const uint32_t id_F = tc::idesc_bf16(128, kpad, 0, 0);
-            tc::mbar_wait(w_full, 0);
-            const uint32_t yt = tc::smem_u32(sYT), pb = tc::smem_u32(sP), xs = tc::smem_u32(sX);
-            const uint32_t wl0 = tc::smem_u32(sWL);
-            int it = 0, gw = 0;
+            const uint32_t pb = tc::smem_u32(sP), xs = tc::smem_u32(sX);
+            const uint32_t wl0 = tc::smem_u32(sWL), yt0 = tc::smem_u32(sYT);
+            int it = 0, gw = 0, gy = 0;
+            unsigned long long wt[16] = {0};
+            const long long t_start = clock64();
             for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
-                tc::mbar_wait(x_full, it & 1);
-                tc::mbar_wait(tmem_empty, (it & 1) ^ 1);
+                const uint32_t ph = it & 1;
+                FM_WAIT(0, l_empty, ph ^ 1);  // the previous sample's P and L are drained
                 tc::fence_after();
-                for (int kk = 0; kk < npad / 16; ++kk) {  // P = X^T Y
-                    const int k0 = kk * 16;
-                    const uint64_t a_xt = tc::sdesc(xs + k0 * 128, g.xpanel, 1024, 2);
-                    const uint64_t b_y = tc::sdesc(yt + (k0 / 64) * g.ytpanel + (k0 % 64) * 2, 16, 1024, 2);
-                    tc::mma_f16(t_Pb, a_xt, b_y, id_P, kk != 0);
-                }
-                for (int mt = 0; mt < g.ml; ++mt)  // L = W_L X, W_L streamed
-                    for (int kp = 0; kp < g.panels_n; ++kp, ++gw) {
-                        const int s = gw % kWlStages;
-                        tc::mbar_wait(&wl_full[s], (gw / kWlStages) & 1);
+                for (int kp = 0; kp < g.panels_n; ++kp) {
+                    if ((kp & 1) == 0) FM_WAIT(1, &x_full[kp >> 1], ph);
+                    const int sy = gy % kYtStages;
+                    FM_WAIT(2, &yt_full[sy], (gy / kYtStages) & 1);
+                    tc::fence_after();
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {  // P += X^T[:, k0:k0+16] . Y[k0:k0+16, :]
+                        const int k0 = kp * 64 + j * 16;
+                        const uint64_t a_xt = tc::sdesc(xs + k0 * 128, g.xpanel, 1024, 2);
+                        const uint64_t b_y = tc::sdesc(yt0 + sy * g.ytpanel + j * 32, 16, 1024, 2);
+                        tc::mma_f16(t_Pb, a_xt, b_y, id_P, (kp | j) != 0);
+                    }
+                    tc::mma_commit(&yt_empty[sy]);
+                    ++gy;
+                    for (int mt = 0; mt < g.ml; ++mt, ++gw) {  // L[mt] += W_L[mt, k0:k0+64] . X[k0:k0+64, :]
+                        const int s = gw % NW;
+                        FM_WAIT(3, &wl_full[s], (gw / NW) & 1);
                         tc::fence_after();
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
@@ -591,10 +656,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         tc::mma_commit(&wl_empty[s]);
                     }
+                }
                 tc::mma_commit(pl_full);
-                tc::mbar_wait(pbuf_full, it & 1);
+                FM_WAIT(4, pbuf_full, ph);
+                FM_WAIT(5, f_empty, ph ^ 1);  // the previous sample's F is drained
                 tc::fence_after();
-                for (int mt = 0; mt < g.mf; ++mt)  // F = X P
+                for (int mt = 0; mt < g.mf; ++mt) {  // F = X P, M-tile mt = X chunk mt
+#pragma unroll
                     for (int kk = 0; kk < d / 16; ++kk) {
                         const int k0 = kk * 16;
                         const uint32_t pan = (uint32_t)(k0 / 64), kin = (uint32_t)(k0 % 64) * 2;
@@ -602,86 +670,92 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint64_t b_p = tc::sdesc(pb + pan * g.ppanel + kin, 16, 1024, 2);
                         tc::mma_f16(t_Fb + mt * kpad, a_x, b_p, id_F, kk != 0);
                     }
+                    tc::mma_commit(&x_empty[mt]);  // every MMA reading chunk mt has completed
+                }
                 tc::mma_commit(f_full);
             }
+            if (p.trace) {
+                for (int i = 0; i < 6; ++i) p.trace[blockIdx.x * 16 + i] = wt[i];
+                p.trace[blockIdx.x * 16 + 6] = (unsigned long long)(clock64() - t_start);
+                p.trace[blockIdx.x * 16 + 7] = (unsigned long long)it;
+            }
         }
-    } else if (warp < 6) {  // ---- LCB group: P -> Pbuf, then the L rows (2 M-tiles)
+    } else if (warp < 11) {  // ---- LCB group, warps 3..10: lane quarter q, L M-tile mt
         const int q = warp & 3;
+        const int mt = (warp - 3) >> 2;
         const int row = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const float inv_d = 1.0f / (float)d;
+        const int i = mt * 128 + row;
+        const bool live = mt < g.ml && i < p.nL;
+        const int xr = p.nF + i;
+        const int cx = xr >> 7;  // the X chunk holding the residual row
+        const uint32_t t_L = t_Lb + lane_off + mt * 128;
         int it = 0;
         for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
             tc::mbar_wait(pl_full, it & 1);
             tc::fence_after();
-            for (int c0 = 0; c0 < kpad; c0 += 16) {
-                float pv[16];
-                tc::tmem_ld16(t_Pb + lane_off + c0, pv);
-                uint8_t* pan = sP + (row / 64) * g.ppanel;
+            if (mt == 0) {  // P row `row` (a d index) -> bf16 -> Pbuf[j][row], F's K-major B operand
+                for (int c0 = 0; c0 < kpad; c0 += 16) {
+                    float pv[16];
+                    tc::tmem_ld16(t_Pb + lane_off + c0, pv);
+                    uint8_t* pan = sP + (row / 64) * g.ppanel;
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    *reinterpret_cast<__nv_bfloat16*>(pan + swz<2>(c0 + j, row & 63)) = __float2bfloat16_rn(pv[j]);
+                    for (int j = 0; j < 16; ++j)
+                        *reinterpret_cast<__nv_bfloat16*>(pan + swz<2>(c0 + j, row & 63)) = __float2bfloat16_rn(pv[j]);
+                }
+                tc::fence_async_shared();
+                tc::mbar_arrive(pbuf_full);
             }
-            tc::fence_async_shared();
-            tc::mbar_arrive(pbuf_full);
-            for (int mt = 0; mt < g.ml; ++mt) {
-                const int i = mt * 128 + row;
-                const bool live = i < p.nL;
-                const int xr = p.nF + i;
-                const uint32_t t_L = t_Lb + lane_off + mt * 128;
-                float ss = 0.0f;
+            if (live) {  // X'[nF+i] = rms_norm_d(L[i] + X[nF+i]): sum of squares, then normalise + store;
+                         // the residual row is read from the X chunk in shared memory, which this
+                         // thread releases afterwards (the next sample's chunk loads behind it)
+                float ss4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                for (int c = 0; c < d; c += 32) {
-                    float v[32];
-                    tc::tmem_ld32(t_L + c, v);
-                    if (live) {
+                for (int c = 0; c < d; c += 16) {
+                    float v[16];
+                    tc::tmem_ld16(t_L + c, v);
 #pragma unroll
-                        for (int j = 0; j < 32; j += 8) {
-                            const uint4 r = *reinterpret_cast<const uint4*>(sX + ((c + j) / 64) * g.xpanel +
-                                                                            swz<2>(xr, (c + j) & 63));
-                            const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int e = c + 8 * hh;
+                        const uint4 r = *reinterpret_cast<const uint4*>(sX + (e / 64) * g.xpanel + swz<2>(xr, e & 63));
+                        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                const float a = v[j + 2 * k] + bf16_lo(w[k]), bb = v[j + 2 * k + 1] + bf16_hi(w[k]);
-                                ss += a * a + bb * bb;
-                            }
+                        for (int k = 0; k < 4; ++k) {
+                            const float a = v[8 * hh + 2 * k] + bf16_lo(w[k]), bb = v[8 * hh + 2 * k + 1] + bf16_hi(w[k]);
+                            ss4[k] = fmaf(a, a, ss4[k]);
+                            ss4[k] = fmaf(bb, bb, ss4[k]);
                         }
                     }
                 }
+                const float ss = (ss4[0] + ss4[1]) + (ss4[2] + ss4[3]);
                 const float inv = 1.0f / sqrtf(ss * inv_d + 1e-6f);
                 __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.Xout) + (b * p.n + xr) * (int64_t)d;
 #pragma unroll
-                for (int c = 0; c < d; c += 32) {
-                    float v[32];
-                    tc::tmem_ld32(t_L + c, v);
-                    if (live) {
+                for (int c = 0; c < d; c += 16) {  // 16 values per 32-byte store
+                    float v[16];
+                    tc::tmem_ld16(t_L + c, v);
+                    uint32_t o[8];
 #pragma unroll
-                        for (int j = 0; j < 32; j += 16) {  // 16 values per 32-byte store
-                            uint32_t o[8];
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int e = c + 8 * hh;
+                        const uint4 r = *reinterpret_cast<const uint4*>(sX + (e / 64) * g.xpanel + swz<2>(xr, e & 63));
+                        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
-                            for (int hh = 0; hh < 2; ++hh) {
-                                const int jj = j + 8 * hh;
-                                const uint4 r = *reinterpret_cast<const uint4*>(sX + ((c + jj) / 64) * g.xpanel +
-                                                                                swz<2>(xr, (c + jj) & 63));
-                                const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-                                for (int k = 0; k < 4; ++k)
-                                    o[4 * hh + k] = pack_bf16x2((v[jj + 2 * k] + bf16_lo(w[k])) * inv,
-                                                                (v[jj + 2 * k + 1] + bf16_hi(w[k])) * inv);
-                            }
-                            st_global_256(dst + c + j, make_uint4(o[0], o[1], o[2], o[3]),
-                                          make_uint4(o[4], o[5], o[6], o[7]));
-                        }
+                        for (int k = 0; k < 4; ++k)
+                            o[4 * hh + k] = pack_bf16x2((v[8 * hh + 2 * k] + bf16_lo(w[k])) * inv,
+                                                        (v[8 * hh + 2 * k + 1] + bf16_hi(w[k])) * inv);
                     }
+                    st_global_256(dst + c, make_uint4(o[0], o[1], o[2], o[3]), make_uint4(o[4], o[5], o[6], o[7]));
                 }
+                tc::mbar_arrive(&x_empty[cx]);
             }
-            tc::mbar_arrive(x_empty);  // residual reads done
             tc::fence_before();
-            tc::mbar_arrive(tmem_empty);
+            tc::mbar_arrive(l_empty);
         }
-    } else {  // ---- FM group: Fin = rms_norm(flatten(X P)) over 4 M-tiles, two TMEM passes
+    } else {  // ---- FM group, warps 11..14: Fin = rms_norm(flatten(X P)) over 4 M-tiles, two TMEM passes
         const int q = warp & 3;
-        const int e = warp - 6;
+        const int e = warp - 11;
         const int row = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const float inv_nk = 1.0f / (float)(p.n * p.k);
@@ -689,8 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
             tc::mbar_wait(f_full, it & 1);
             tc::fence_after();
-            tc::mbar_arrive(x_empty);  // every MMA reading X has completed
-            float ss = 0.0f;
+            float ss4[4] = {0.f, 0.f, 0.f, 0.f};
             for (int mt = 0; mt < g.mf; ++mt) {
                 const int r = mt * 128 + row;
                 for (int c0 = 0; c0 < kpad; c0 += 16) {
@@ -699,11 +772,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (r < p.n) {
 #pragma unroll
                         for (int j = 0; j < 16; ++j)
-                            if (c0 + j < p.k) ss += v[j] * v[j];
+                            if (c0 + j < p.k) ss4[j & 3] = fmaf(v[j], v[j], ss4[j & 3]);
                     }
                 }
             }
-            ss = warp_sum(ss);
+            float ss = warp_sum((ss4[0] + ss4[1]) + (ss4[2] + ss4[3]));
             float* red = red_f + (it & 1) * 4;
             if (lane == 0) red[e] = ss;
             tc::named_bar(2, 128);
@@ -730,7 +803,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             tc::fence_before();
-            tc::mbar_arrive(tmem_empty);
+            tc::mbar_arrive(f_empty);
         }
     }
     tc::fence_before();
@@ -740,8 +813,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 size_t smem_bytes_large(const Params& p) {
     const GeoL g(p);
-    return 1024 + 2 * (size_t)g.xpanel + kWlStages * (size_t)g.wlpanel + (size_t)g.ytpanel * g.panels_n +
-           ((2 * (size_t)g.ppanel + 1023) & ~size_t(1023)) + 256;
+    return 1024 + 2 * (size_t)g.xpanel + (size_t)g.wl_stages * g.wlpanel + kYtStages * (size_t)g.ytpanel +
+           g.pbytes + 512;
 }
 
 bool is_large(const Params& p) { return p.n_pad > 256; }
@@ -772,7 +845,8 @@ lattice_status check(const Params& p) {
             return set_error(LATTICE_USAGE, "fm_lcb: nL must be <= 256 and nF + nL == n");
         if (64 + 256 + (p.n_pad / 128) * p.k_pad > 512)
             return set_error(LATTICE_USAGE, "fm_lcb: n = 512 needs k <= 48 (TMEM)");
-        if (smem_bytes(p) > 227 * 1024) return set_error(LATTICE_USAGE, "fm_lcb: shared memory budget exceeded");
+        if (GeoL(p).wl_stages < 3 || smem_bytes(p) > 227 * 1024)
+            return set_error(LATTICE_USAGE, "fm_lcb: shared memory budget exceeded");
         return LATTICE_OK;
     }
     if (p.n < 1 || p.n_pad % 16 || p.n_pad < p.n) return set_error(LATTICE_USAGE, "fm_lcb: bad n");
@@ -797,8 +871,8 @@ lattice_status make_maps(Plan* pl, const void* X, const void* WLpad, const void*
     }
     cuuint64_t dims[3] = {(cuuint64_t)p.d, (cuuint64_t)p.n, (cuuint64_t)p.B};
     cuuint64_t strides[2] = {(cuuint64_t)p.d * es, (cuuint64_t)p.n * p.d * es};
-    // TMA boxes hold at most 256 rows: the large variant loads X in two row halves
-    cuuint32_t box[3] = {(cuuint32_t)ep, (cuuint32_t)(p.n_pad > 256 ? 256 : p.n_pad), 1};
+    // the large variant loads X in 128-row chunks (one box per chunk and d-panel)
+    cuuint32_t box[3] = {(cuuint32_t)ep, (cuuint32_t)(p.n_pad > 256 ? 128 : p.n_pad), 1};
     cuuint32_t el[3] = {1, 1, 1};
     CUresult r = fn(&pl->tmX, p.f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                     const_cast<void*>(X), dims, strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -850,7 +924,7 @@ lattice_status launch(const Plan& pl, cudaStream_t st) {
         }
         const int grid = (int)(pl.p.B < num_sms() ? pl.p.B : num_sms());
         if (grid <= 0) return LATTICE_OK;
-        LAT_CUDA(launch_pdl(fm_lcb_large_kernel, grid, kThreads, smem_bytes(pl.p), st, pl));
+        LAT_CUDA(launch_pdl(fm_lcb_large_kernel, grid, kLargeThreads, smem_bytes(pl.p), st, pl));
         LAT_CUDA(cudaGetLastError());
         return LATTICE_OK;
     }
@@ -891,6 +965,7 @@ extern "C" lattice_status lattice_fm_lcb(const lattice_fm_lcb_args* a, lattice_s
     p.f32 = a->dtype == LATTICE_F32 ? 1 : 0;
     p.Fout = a->Fin;
     p.Xout = a->Xout;
+    p.Xin = a->X;
     lattice_status s = fm::check(p);
     if (s != LATTICE_OK) return s;
     const size_t es = p.f32 ? 4 : 2;
@@ -906,7 +981,25 @@ extern "C" lattice_status lattice_fm_lcb(const lattice_fm_lcb_args* a, lattice_s
                                        cudaMemcpyDeviceToDevice, st));
         lattice_status r = fm::make_maps(&pl, a->X, ws + yt_bytes, ws);
         if (r != LATTICE_OK) return r;
-        return fm::launch(pl, st);
+        const char* tr = std::getenv("LATTICE_FM_TRACE");
+        if (!(tr && std::atoi(tr) && fm::is_large(p))) return fm::launch(pl, st);
+        // wait-site profile of the large variant: cycles per site averaged over CTAs, to stderr
+        const int grid = (int)(p.B < num_sms() ? p.B : num_sms());
+        LAT_CUDA(cudaMalloc(&pl.p.trace, sizeof(unsigned long long) * 16 * grid));
+        LAT_CUDA(cudaMemset(pl.p.trace, 0, sizeof(unsigned long long) * 16 * grid));
+        r = fm::launch(pl, st);
+        std::vector<unsigned long long> h((size_t)16 * grid);
+        cudaMemcpy(h.data(), pl.p.trace, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost);
+        cudaFree(pl.p.trace);
+        const char* names[11] = {"mma:l_empty", "mma:x_full", "mma:yt_full", "mma:wl_full", "mma:pbuf_full",
+                                 "mma:f_empty", "mma:total", "samples", "xprod:x_empty", "wprod:yt_empty",
+                                 "wprod:wl_empty"};
+        for (int i = 0; i < 11; ++i) {
+            double sum = 0;
+            for (int b = 0; b < grid; ++b) sum += (double)h[(size_t)b * 16 + i];
+            std::fprintf(stderr, "[fm_trace] %-16s %14.0f\n", names[i], sum / grid);
+        }
+        return r;
     };
     s = body();
     cudaFreeAsync(ws, st);

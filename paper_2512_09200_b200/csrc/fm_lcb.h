@@ -15,8 +15,11 @@ struct Params {
     int n_pad, k_pad;       // multiples of 16
     int tmem_cols;          // informational (the kernel sizes its own allocation)
     int f32;                // 1: fp32 storage, kind::tf32 MMAs; 0: bf16, kind::f16
+    const void* Xin;        // [B][n][d], the X the tensor map reads (the large variant's LCB
+                            // residual rows come from here, L2-resident, instead of shared memory)
     void* Fout;             // [B][n*k]
     void* Xout;             // [B][n][d], rows nF .. n-1 written
+    unsigned long long* trace;  // optional [grid][16] cycles spent per wait site (LATTICE_FM_TRACE=1)
 };
 
 struct Plan {

@@ -250,6 +250,7 @@ lattice_status build_plans(lattice_net* net) {
         fp.p.f32 = net->f32 ? 1 : 0;
         fp.p.Fout = net->Fbuf;
         fp.p.Xout = Xn;
+        fp.p.Xin = Xc;
         lattice_status s = fm::check(fp.p);
         if (s != LATTICE_OK) return s;
         s = fm::make_maps(&fp, Xc, net->WL[blk], net->YT[blk]);
