@@ -401,6 +401,9 @@ typedef struct {
     int32_t group;      /* epilogue 3 group width (128 or 64) */
     int32_t in_dtype;   /* A/B dtype: LATTICE_BF16 (kind::f16) or LATTICE_F32 (kind::tf32);
                            resid has the output dtype */
+    int32_t a_major;    /* 0: A is [M][lda] (K-major); 1: A is stored [K][lda] with M contiguous
+                           (MN-major, bf16: a transposed operand read in place, e.g. dZ^T) */
+    int32_t b_major;    /* 0: B is [N][ldb]; 1: B is stored [K][ldb] with N contiguous */
 } lattice_gemm_args;
 
 lattice_status lattice_gemm(const lattice_gemm_args* args, lattice_stream stream);
@@ -525,6 +528,36 @@ void* lattice_net_buffer(lattice_net* net, int32_t which);
 /* logits: DEVICE fp32 [B][heads] in the caller's sample order. */
 lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch, float* logits,
                                    lattice_stream stream);
+/* ======================================================================================
+ * Backward. The reference defines no training step; it pins the activation
+ * derivative (swish_rn_jvp, numerics.hpp:113-136, test_numerics.cpp:151-178), whose adjoint these
+ * entries compute.
+ * lattice_rownorm_vjp: out = J(x)^T g per row of a [rows][width] matrix, J the Jacobian of
+ *   rms_norm (mode 0), swish_rn (1) or swish_rn_hard (2) (numerics.hpp:81-107); dtype F32 / F64.
+ * lattice_routed_bce: window-routed binary cross-entropy of the heads, each sample training only
+ *   its assigned window's head per task: loss = mean over (sample, task) of
+ *   bce(logits[b][t*W + window[b]], labels[b][t][window[b]]) (DEVICE fp64 scalar), and
+ *   dlogits [n][T*W] (zero for the other windows' heads). Deterministic.
+ * lattice_net_tower_backward: after a forward of `batch` samples, the gradients of the untied
+ *   towers from dlogits [batch][heads] (caller order): dW1 fp32 [G][tower_hidden][n*d], dW2 fp32
+ *   [G][heads][tower_hidden], optionally dX [batch][n*d] (the towers' input, domain-sorted rows:
+ *   lattice_net_buffer 1 maps samples to rows) in dx_dtype. tcgen05 GEMMs (operands read in place,
+ *   MN-major), fixed-order reductions: deterministic. Synchronises the stream once (segment sizes).
+ * ==================================================================================== */
+lattice_status lattice_rownorm_vjp(int32_t mode, int64_t rows, int64_t width, double eps, int32_t dtype,
+                                   const void* x, const void* g, void* out, lattice_stream stream);
+lattice_status lattice_routed_bce(int64_t n, int32_t tasks, int32_t windows, const float* logits,
+                                  const uint8_t* window, const uint8_t* labels, float* dlogits, double* loss,
+                                  lattice_stream stream);
+lattice_status lattice_net_tower_backward(lattice_net* net, int64_t batch, const float* dlogits, float* dW1,
+                                          float* dW2, void* dX, int32_t dx_dtype, lattice_stream stream);
+/* Plain SGD on the towers: master -= lr * grad for the caller's fp32 master copies of W1 [G][th][n*d]
+ * and W2 [G][heads][th] (start them from lattice_net_weight), and the network's own copies refreshed
+ * (W1 rounded to the network dtype) in the same pass. With data parallelism, all-reduce (average) the
+ * gradients first: every replica then applies the same update and stays bit-identical. */
+lattice_status lattice_net_tower_sgd(lattice_net* net, float lr, const float* dW1, const float* dW2, float* master_W1,
+                                     float* master_W2, lattice_stream stream);
+
 /* Per-stage CUDA-event times (ms) of the last forward when timing was enabled. */
 lattice_status lattice_net_set_timing(lattice_net* net, int32_t enable);
 lattice_status lattice_net_stage_times(lattice_net* net, float* ms, int32_t max_stages,

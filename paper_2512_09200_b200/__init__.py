@@ -102,7 +102,8 @@ class StudentArgs(ctypes.Structure):
 class GemmArgs(ctypes.Structure):
     _fields_ = [("M", _I64), ("N", _I64), ("K", _I64), ("A", _P), ("lda", _I64), ("B", _P),
                 ("ldb", _I64), ("C", _P), ("ldc", _I64), ("out_dtype", _I32), ("epilogue", _I32),
-                ("resid", _P), ("ldr", _I64), ("group", _I32), ("in_dtype", _I32)]
+                ("resid", _P), ("ldr", _I64), ("group", _I32), ("in_dtype", _I32), ("a_major", _I32),
+                ("b_major", _I32)]
 
 
 class FmLcbArgs(ctypes.Structure):
@@ -166,6 +167,10 @@ _sig("lattice_smooth_labels", ctypes.c_int, [_I64, _P, ctypes.c_double, _P, _I32
 _sig("lattice_swish_rn_jvp", ctypes.c_int, [_I64, _I64, ctypes.c_double, _P, _P, _P, _I32, _P])
 _sig("lattice_gemm", ctypes.c_int, [ctypes.POINTER(GemmArgs), _P])
 _sig("lattice_device_check", ctypes.c_int, [_P])
+_sig("lattice_rownorm_vjp", ctypes.c_int, [_I32, _I64, _I64, ctypes.c_double, _I32, _P, _P, _P, _P])
+_sig("lattice_routed_bce", ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _P, _P, _P])
+_sig("lattice_net_tower_backward", ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _I32, _P])
+_sig("lattice_net_tower_sgd", ctypes.c_int, [_P, ctypes.c_float, _P, _P, _P, _P, _P])
 _sig("lattice_net_create", ctypes.c_int, [ctypes.POINTER(NetConfig), ctypes.POINTER(_P)])
 _sig("lattice_net_destroy", None, [_P])
 _sig("lattice_net_weight", _P, [_P, _I32, _I32, _I32])
@@ -197,7 +202,8 @@ EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_versio
            "lattice_clip_features", "lattice_smooth_labels", "lattice_swish_rn_jvp",
            "lattice_jsonl_open", "lattice_jsonl_extract", "lattice_jsonl_task_columns",
            "lattice_jsonl_close", "lattice_net_set_weight", "lattice_fm_lcb",
-           "lattice_rownorm_f64", "lattice_device_check"]
+           "lattice_rownorm_f64", "lattice_device_check", "lattice_rownorm_vjp", "lattice_routed_bce",
+           "lattice_net_tower_backward", "lattice_net_tower_sgd"]
 
 lib = _lib
 
@@ -631,19 +637,22 @@ def domain_bucket(domain, G, stream=None):
 EPI_STORE, EPI_SWISH, EPI_SWISH_HARD, EPI_RESID_NORM = 0, 1, 2, 3
 
 
-def gemm(A, B, epilogue=EPI_STORE, out_dtype=None, resid=None, group=128, out=None, stream=None):
+def gemm(A, B, epilogue=EPI_STORE, out_dtype=None, resid=None, group=128, out=None, stream=None,
+         a_t=False, b_t=False):
     """C = A @ B^T with A [M,K], B [N,K] both bf16 (kind::f16) or both fp32 (kind::tf32) on
-    tcgen05; fused epilogue. resid (epilogue 3) has the output dtype."""
+    tcgen05; fused epilogue. resid (epilogue 3) has the output dtype. a_t / b_t: the operand is
+    given transposed (A as [K,M], B as [K,N], bf16) and read MN-major in place."""
     import torch
-    M, K = A.shape
-    N = B.shape[0]
+    M, K = (A.shape[1], A.shape[0]) if a_t else A.shape
+    N = B.shape[1] if b_t else B.shape[0]
     f32_in = A.dtype == torch.float32
     odt = out_dtype or (torch.float32 if f32_in else torch.bfloat16)
     if out is None:
         out = torch.empty((M, N), dtype=odt, device=A.device)
     a = GemmArgs(M, N, K, _p(A), A.stride(0), _p(B), B.stride(0), _p(out), out.stride(0),
                  F32 if odt == torch.float32 else BF16, epilogue, _p(resid),
-                 resid.stride(0) if resid is not None else 0, group, F32 if f32_in else BF16)
+                 resid.stride(0) if resid is not None else 0, group, F32 if f32_in else BF16,
+                 1 if a_t else 0, 1 if b_t else 0)
     check(_lib.lattice_gemm(ctypes.byref(a), _stream(stream)))
     return out
 
@@ -662,6 +671,31 @@ def fm_lcb(X, YT, WL, nF, Fin=None, Xout=None, stream=None):
                   _p(WL) if nL else None, _p(Fin), _p(Xout))
     check(_lib.lattice_fm_lcb(ctypes.byref(a), _stream(stream)))
     return Fin, Xout
+
+
+def rownorm_vjp(x, g, mode=1, eps=1e-6, stream=None):
+    """J(x)^T g per row (lattice_rownorm_vjp): mode 0 rms_norm, 1 swish_rn, 2 swish_rn_hard;
+    x, g fp32 or fp64 CUDA matrices [rows, width]."""
+    import torch
+    x, g = x.contiguous(), g.contiguous()
+    out = torch.empty_like(x)
+    rows = x.numel() // x.shape[-1] if x.numel() else 0
+    check(_lib.lattice_rownorm_vjp(mode, rows, x.shape[-1], eps, F64 if x.dtype == torch.float64 else F32, _p(x),
+                                   _p(g), _p(out), _stream(stream)))
+    return out
+
+
+def routed_bce(logits, window, labels, tasks, windows, dlogits=None, loss=None, stream=None):
+    """Window-routed BCE of the heads (lattice_routed_bce): (loss fp64 scalar tensor, dlogits)."""
+    import torch
+    n = logits.shape[0]
+    if dlogits is None:
+        dlogits = torch.empty_like(logits)
+    if loss is None:
+        loss = torch.empty((), dtype=torch.float64, device=logits.device)
+    check(_lib.lattice_routed_bce(n, tasks, windows, _p(logits), _p(window), _p(labels), _p(dlogits), _p(loss),
+                                  _stream(stream)))
+    return loss, dlogits
 
 
 def device_check(stream=None):
@@ -792,6 +826,41 @@ class Network:
         b.dense = _p(dense)
         check(_lib.lattice_net_forward(self._h, ctypes.byref(b), _p(logits), _stream(stream)))
         return logits
+
+    def tower_backward(self, dlogits, dW1=None, dW2=None, dX=None, dx_dtype=None, stream=None):
+        """Gradients of the untied towers after a forward of dlogits.shape[0] samples
+        (lattice_net_tower_backward): dW1 fp32 [G, th, n*d], dW2 fp32 [G, heads, th], and with
+        dx_dtype the towers' input gradient [B, n*d] in domain-sorted rows."""
+        import torch
+        c = self.cfg
+        B = dlogits.shape[0]
+        G, th, nd = c["domains"], c["tower_hidden"], c["n"] * c["d"]
+        dev = dlogits.device
+        if dW1 is None:
+            dW1 = torch.empty((G, th, nd), dtype=torch.float32, device=dev)
+        if dW2 is None:
+            dW2 = torch.empty((G, c["heads"], th), dtype=torch.float32, device=dev)
+        if dx_dtype is not None and dX is None:
+            dX = torch.empty((B, nd), dtype=dx_dtype, device=dev)
+        check(_lib.lattice_net_tower_backward(self._h, B, _p(dlogits.contiguous()), _p(dW1), _p(dW2), _p(dX),
+                                              BF16 if dX is not None and dX.dtype == torch.bfloat16 else F32,
+                                              _stream(stream)))
+        return dW1, dW2, dX
+
+    def tower_sgd(self, lr, dW1, dW2, master_W1, master_W2, stream=None):
+        """master -= lr * grad and the network's tower weights refreshed (lattice_net_tower_sgd)."""
+        check(_lib.lattice_net_tower_sgd(self._h, lr, _p(dW1), _p(dW2), _p(master_W1), _p(master_W2),
+                                         _stream(stream)))
+
+    def tower_masters(self):
+        """fp32 device copies of the towers' W1 [G, th, n*d] and W2 [G, heads, th] (SGD masters)."""
+        c = self.cfg
+        G, th, nd = c["domains"], c["tower_hidden"], c["n"] * c["d"]
+        import torch
+        wdt = torch.float32 if c["dtype"] in ("f32", "fp32", "float32") else torch.bfloat16
+        W1 = _view(_lib.lattice_net_weight(self._h, 0, 4, 0), (G, th, nd), wdt).float().clone()
+        W2 = _view(_lib.lattice_net_weight(self._h, 0, 5, 0), (G, c["heads"], th), torch.float32).clone()
+        return W1, W2
 
     def set_timing(self, on=True):
         check(_lib.lattice_net_set_timing(self._h, 1 if on else 0))

@@ -1,0 +1,32 @@
+// backward.h -- host interface of the towers' backward (backward.cu), used by network.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/lattice_b200.h"
+
+namespace lat {
+
+struct TowerBwd {
+    int64_t B;                 // batch rows (domain-sorted, as the forward left them)
+    int G, th, heads, hard;
+    int64_t nd;                // n * d: the towers' input width
+    const void* X;             // bf16 [B][nd] X_L, domain-sorted rows
+    const void* W1;            // bf16 [G*th][nd]
+    const float* W2;           // [G][heads][th]
+    const int32_t* order;      // sorted row -> caller sample
+    const int32_t* seg;        // DEVICE [G+1] domain segment starts
+    const float* dlogits;      // [B][heads], caller order
+    float* dW1;                // out [G][th][nd]
+    float* dW2;                // out [G][heads][th]
+    void* dX;                  // optional out [B][nd], domain-sorted rows
+    int dx_bf16;
+};
+
+lattice_status tower_backward(const TowerBwd& a, cudaStream_t st);
+// master -= lr * grad (n fp32 values); work (the network's copy) refreshed in bf16 or fp32
+lattice_status sgd_update(int64_t n, float lr, const float* grad, float* master, void* work, bool work_bf16,
+                          cudaStream_t st);
+
+}  // namespace lat

@@ -267,14 +267,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t ph = (g / STAGES) & 1;
                     tc::mbar_wait(&empty[st], ph ^ 1);
                     tc::mbar_expect_tx(&full[st], A_BYTES + B_BYTES);
-                    tc::tma_load_2d(sA + st * A_BYTES, &tmA, &full[st], kb * BKE, m0);
-                    tc::tma_load_2d(sB + st * B_BYTES, &tmB, &full[st], kb * BKE, b_row0);
+                    // K-major: one [rows][64 K] box; MN-major: [64 K rows][64 MN] panels, 8 KB apart
+                    if (p.a_mn) {
+                        for (int q = 0; q < BM / 64; ++q)
+                            tc::tma_load_2d(sA + st * A_BYTES + q * 8192, &tmA, &full[st], m0 + q * 64, kb * BKE);
+                    } else {
+                        tc::tma_load_2d(sA + st * A_BYTES, &tmA, &full[st], kb * BKE, m0);
+                    }
+                    if (p.b_mn) {
+                        for (int q = 0; q < BN / 64; ++q)
+                            tc::tma_load_2d(sB + st * B_BYTES + q * 8192, &tmB, &full[st], b_row0 + q * 64, kb * BKE);
+                    } else {
+                        tc::tma_load_2d(sB + st * B_BYTES, &tmB, &full[st], kb * BKE, b_row0);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---- MMA issuer
-            constexpr uint32_t idesc = tc::idesc_fmt(Op::kFormat, BM, BN, 0, 0);
+            const uint32_t idesc = tc::idesc_fmt(Op::kFormat, BM, BN, p.a_mn, p.b_mn);
             int g = 0, i = 0;
             for (int u = s.first; u < s.units; u += s.stride, ++i) {
                 const int acc = i & 1;
@@ -290,8 +301,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t b_base = tc::smem_u32(sB + st * B_BYTES);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {  // 4 x 32-byte K slices per k-block
-                        const uint64_t ad = tc::sdesc(a_base + k * 32, 16, 1024, 2);
-                        const uint64_t bd = tc::sdesc(b_base + k * 32, 16, 1024, 2);
+                        // K-major: the slice is 32 bytes into each 128-byte row; MN-major: 16 K rows
+                        // further into each 64-wide MN panel (panels 8 KB apart)
+                        const uint64_t ad = p.a_mn ? tc::sdesc(a_base + k * 2048, 8192, 1024, 2)
+                                                   : tc::sdesc(a_base + k * 32, 16, 1024, 2);
+                        const uint64_t bd = p.b_mn ? tc::sdesc(b_base + k * 2048, 8192, 1024, 2)
+                                                   : tc::sdesc(b_base + k * 32, 16, 1024, 2);
                         Op::mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
                     }
                     tc::mma_commit(&empty[st]);
@@ -791,7 +806,7 @@ bool use_2cta(const Params& p, bool f32) {
         const char* e = std::getenv("LATTICE_GEMM_2CTA");
         env = e ? std::atoi(e) : 1;
     }
-    if (env == 0 || f32 || p.tiles || p.M < 2 * BM) return false;
+    if (env == 0 || f32 || p.tiles || p.M < 2 * BM || p.a_mn || p.b_mn) return false;
     if (p.epi == kSwish || p.epi == kSwishHard) return p.rowpart && p.rowcnt && p.N == p.N_full;
     return p.cluster == 1 && (p.epi == kStore || p.epi == kResidNorm);
 }
@@ -829,13 +844,17 @@ lattice_status plan(GemmPlan* g, const void* A, int64_t lda, int64_t a_rows, con
                     int64_t ldb, int64_t b_rows, const Params& p, int grid_y, bool f32) {
     const uint64_t es = f32 ? 4 : 2;
     const uint32_t bke = f32 ? 32 : 64;
-    lattice_status s = make_map_2d(&g->ta, A, (uint64_t)p.K, (uint64_t)a_rows, (uint64_t)lda * es, bke, BM, f32);
+    if ((p.a_mn || p.b_mn) && f32) return set_error(LATTICE_USAGE, "gemm: MN-major operands need bf16");
+    // MN-major operands are stored [K][rows]: the map's inner dimension runs along M (or N)
+    lattice_status s = p.a_mn ? make_map_2d(&g->ta, A, (uint64_t)a_rows, (uint64_t)p.K, (uint64_t)lda * es, 64, 64)
+                              : make_map_2d(&g->ta, A, (uint64_t)p.K, (uint64_t)a_rows, (uint64_t)lda * es, bke, BM, f32);
     if (s != LATTICE_OK) return s;
     g->two_cta = use_2cta(p, f32);
     Params pp = p;
     if (g->two_cta) pp.cluster = 1;  // the pair kernel exchanges row statistics through global memory
-    s = make_map_2d(&g->tb, B, (uint64_t)p.K, (uint64_t)b_rows, (uint64_t)ldb * es, bke, g->two_cta ? BN / 2 : BN,
-                    f32);
+    s = p.b_mn ? make_map_2d(&g->tb, B, (uint64_t)b_rows, (uint64_t)p.K, (uint64_t)ldb * es, 64, 64)
+               : make_map_2d(&g->tb, B, (uint64_t)p.K, (uint64_t)b_rows, (uint64_t)ldb * es, bke,
+                             g->two_cta ? BN / 2 : BN, f32);
     if (s != LATTICE_OK) return s;
     g->p = pp;
     g->grid_y = grid_y;
@@ -865,8 +884,9 @@ extern "C" lattice_status lattice_gemm(const lattice_gemm_args* a, lattice_strea
     LAT_REQUIRE(a != nullptr, "lattice_gemm: null args");
     LAT_REQUIRE(a->M >= 0 && a->N > 0 && a->K > 0, "lattice_gemm: bad sizes");
     LAT_REQUIRE(a->M < (1ll << 31) && a->N < (1ll << 31) && a->K < (1ll << 31), "lattice_gemm: size overflow");
-    LAT_REQUIRE(a->K % 8 == 0 && a->lda % 8 == 0 && a->ldb % 8 == 0,
-                "lattice_gemm: K, lda, ldb must be multiples of 8 (16-byte TMA strides)");
+    // TMA row strides are 16-byte multiples; K is a row length only for a K-major operand
+    LAT_REQUIRE(a->lda % 8 == 0 && a->ldb % 8 == 0 && (a->K % 8 == 0 || (a->a_major == 1 && a->b_major == 1)),
+                "lattice_gemm: lda, ldb (and K, for a K-major operand) must be multiples of 8 (16-byte TMA strides)");
     LAT_REQUIRE(a->epilogue >= 0 && a->epilogue <= 3, "lattice_gemm: unknown epilogue");
     if (a->M == 0) return LATTICE_OK;
     Params p = {};
@@ -883,6 +903,13 @@ extern "C" lattice_status lattice_gemm(const lattice_gemm_args* a, lattice_strea
     p.N_full = p.N;
     p.cluster = 1;
     p.heads = 0;
+    p.a_mn = a->a_major == 1;
+    p.b_mn = a->b_major == 1;
+    LAT_REQUIRE(a->a_major >= 0 && a->a_major <= 1 && a->b_major >= 0 && a->b_major <= 1,
+                "lattice_gemm: a_major / b_major must be 0 (K-major) or 1 (MN-major)");
+    LAT_REQUIRE(!(p.a_mn || p.b_mn) || (a->in_dtype == LATTICE_BF16 && (!p.a_mn || a->lda >= a->M) &&
+                                        (!p.b_mn || a->ldb >= a->N)),
+                "lattice_gemm: MN-major operands need bf16 and a leading dimension >= M (A) / N (B)");
     if (p.epi == kSwish || p.epi == kSwishHard) {
         // the CTA-pair kernel (bf16, M >= 256) exchanges row statistics through global memory and
         // takes rows up to 16384 wide; the single-CTA kernel's DSMEM exchange stops at 2048
@@ -907,6 +934,8 @@ extern "C" lattice_status lattice_gemm(const lattice_gemm_args* a, lattice_strea
         p.rowpart = static_cast<float*>(ws);
         p.rowcnt = reinterpret_cast<int*>(static_cast<float*>(ws) + rows * p.cluster);
     }
+    if ((p.a_mn || p.b_mn) && (p.epi == kSwish || p.epi == kSwishHard) && p.cluster > kMaxCluster)
+        return set_error(LATTICE_USAGE, "lattice_gemm: MN-major operands run the single-CTA kernel: swish_rn rows up to 2048");
     lattice_status s = plan(&g, a->A, a->lda, a->M, a->B, a->ldb, a->N, p, (int)((a->M + BM - 1) / BM), f32);
     if (s == LATTICE_OK) s = launch(g, stream);
     if (ws) cudaFreeAsync(ws, stream);

@@ -61,6 +61,9 @@ struct Params {
     int heads;
     const int32_t* order;  // sorted row -> original sample
     float* logits;         // [B][heads]
+    // operand majorness (single-CTA kernel, bf16 only): 0 K-major (A [M][K], B [N][K]); 1 MN-major
+    // (A stored [K][M], B stored [K][N]: the transposed operands of a backward pass, read in place)
+    int a_mn, b_mn;
 };
 
 __host__ __device__ inline size_t smem_bytes(int BN, int stages, int cluster, int heads) {

@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "backward.h"
 #include "common.cuh"
 #include "fm_lcb.h"
 #include "gemm_host.h"
@@ -494,6 +495,48 @@ lattice_status lattice_net_set_weight(lattice_net* net, int32_t block, int32_t k
                                                           static_cast<__nv_bfloat16*>(dst), ld);
     LAT_CUDA(cudaGetLastError());
     return LATTICE_OK;
+}
+
+lattice_status lattice_net_tower_backward(lattice_net* net, int64_t batch, const float* dlogits, float* dW1,
+                                          float* dW2, void* dX, int32_t dx_dtype, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(net != nullptr && dlogits != nullptr && dW1 != nullptr && dW2 != nullptr,
+                "lattice_net_tower_backward: null argument");
+    const lattice_net_config& c = net->cfg;
+    LAT_REQUIRE(!net->f32, "lattice_net_tower_backward: needs a bf16 network");
+    LAT_REQUIRE(batch > 0 && batch <= c.max_batch, "lattice_net_tower_backward: bad batch");
+    LAT_REQUIRE(dX == nullptr || dx_dtype == LATTICE_F32 || dx_dtype == LATTICE_BF16,
+                "lattice_net_tower_backward: dX dtype must be f32 or bf16");
+    TowerBwd a = {};
+    a.B = batch;
+    a.G = c.domains;
+    a.th = c.tower_hidden;
+    a.heads = c.heads;
+    a.hard = c.hard;
+    a.nd = (int64_t)c.n * c.d;
+    a.X = net->X[c.blocks & 1];
+    a.W1 = net->T1;
+    a.W2 = net->T2;
+    a.order = net->order;
+    a.seg = net->seg;
+    a.dlogits = dlogits;
+    a.dW1 = dW1;
+    a.dW2 = dW2;
+    a.dX = dX;
+    a.dx_bf16 = dx_dtype == LATTICE_BF16;
+    return tower_backward(a, (cudaStream_t)stream);
+}
+
+lattice_status lattice_net_tower_sgd(lattice_net* net, float lr, const float* dW1, const float* dW2, float* master_W1,
+                                     float* master_W2, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(net && dW1 && dW2 && master_W1 && master_W2, "lattice_net_tower_sgd: null argument");
+    const lattice_net_config& c = net->cfg;
+    const int64_t n1 = (int64_t)c.domains * c.tower_hidden * c.n * c.d, n2 = (int64_t)c.domains * c.heads * c.tower_hidden;
+    const cudaStream_t st = (cudaStream_t)stream;
+    lattice_status s = sgd_update(n1, lr, dW1, master_W1, net->T1, !net->f32, st);
+    if (s != LATTICE_OK) return s;
+    return sgd_update(n2, lr, dW2, master_W2, net->T2, false, st);
 }
 
 lattice_status lattice_net_set_timing(lattice_net* net, int32_t enable) {

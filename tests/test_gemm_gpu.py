@@ -131,3 +131,20 @@ def test_two_networks_non_cooperative_never_hang():
     or lattice_device_check reports the timeout -- the process always finishes."""
     res = _run_concurrent("0")
     assert res["status"] == "ok" and res["bit_identical"] or res["status"].startswith("timeout reported"), res
+
+
+@pytest.mark.parametrize("M,N,K,a_t,b_t", [(256, 512, 1000, True, True), (304, 768, 4096, True, True),
+                                           (1000, 8192, 256, False, True), (512, 256, 776, True, False),
+                                           (136, 104, 1001, True, True)])
+def test_mn_major_operands(M, N, K, a_t, b_t):
+    """Operands read MN-major in place (the backward's transposed products, e.g. dW1 = dZ^T X with
+    the batch as K): A given as [K, M] and/or B as [K, N]; with both MN-major, K of any length
+    (it is the row count; TMA zero-fills the tail)."""
+    import torch
+    import paper_2512_09200_b200 as L
+    g = torch.Generator(device="cuda").manual_seed(M + K)
+    A = (torch.randn((K, M) if a_t else (M, K), generator=g, device="cuda") * 0.5).to(torch.bfloat16)
+    B = (torch.randn((K, N) if b_t else (N, K), generator=g, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    C = L.gemm(A, B, out_dtype=torch.float32, a_t=a_t, b_t=b_t)
+    ref = (A.float().t() if a_t else A.float()) @ (B.float() if b_t else B.float().t())
+    torch.testing.assert_close(C, ref, rtol=1e-4, atol=1e-4)

@@ -38,3 +38,15 @@ def test_cpp_sharded_network_bit_identical():
                        text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("bit-identical to") == n
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
+def test_data_parallel_tower_training():
+    """gradient all-reduce over NCCL keeps the replicas bit-identical."""
+    n = min(_gpus(), 8)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29518", os.path.join(ROOT, "tests", "dist_train_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "replicas bit-identical after every step: True" in r.stdout and "loss falls: True" in r.stdout, r.stdout
