@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cstdio>
 #include <cuda_bf16.h>
 #include <stdint.h>
 
@@ -45,11 +46,34 @@ __device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+#ifdef LATTICE_DEBUG_WAITS
+// Debug build (make debug -> liblattice_b200_debug.so): a pipeline wait that has not completed
+// after 10 s names its block, thread and barrier and traps, so a lost arrival or a phase slip in
+// the mbarrier/TMEM pipelines shows up as a reported fault instead of a hung GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint64_t t0 = 0;
+    for (uint32_t spin = 0; !mbar_try(a, parity); ++spin) {
+        if ((spin & 4095u) == 4095u) {
+            uint64_t now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if (t0 == 0) {
+                t0 = now;
+            } else if (now - t0 > 10ull * 1000 * 1000 * 1000) {
+                printf("lattice debug: mbarrier wait stuck: block %d thread %d smem bar 0x%x parity %u\n",
+                       (int)blockIdx.x, (int)threadIdx.x, a, parity);
+                __trap();
+            }
+        }
+    }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     while (!mbar_try(a, parity)) {
     }
 }
+#endif
 __device__ __forceinline__ bool mbar_try_cluster(uint32_t addr, uint32_t parity) {
     uint32_t ok;
     asm volatile(
