@@ -481,21 +481,35 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rank = (int)tc::cluster_rank();
-    const int mt2 = (p.M + 2 * BM - 1) / (2 * BM), nt = (p.N + BN - 1) / BN;
-    const int units = mt2 * nt, first = blockIdx.x / 2, stride = gridDim.x / 2;
+    const int nt = (p.N + BN - 1) / BN;
+    const int first = blockIdx.x / 2, stride = gridDim.x / 2;
     const int nk = (p.K + BKE - 1) / BKE;
     const bool swish = p.epi == kSwish || p.epi == kSwishHard;
-    auto decode2 = [&](int u, int& m0, int& n0) {
+    // grouped mode (swish only): M units come from a device table of 256-row tiles {group, row0,
+    // row_end} over the domain segments, B rows from the group's slice of a stacked weight
+    int mt2 = (p.M + 2 * BM - 1) / (2 * BM), units = 0;
+    auto decode2 = [&](int u, int& m0, int& n0, int& m_end, int& group, int& mu) {
+        m_end = p.M;
+        group = 0;
         if (swish) {  // row-major: a row block's N-tiles are consecutive units (see the exchange)
-            m0 = (u / nt) * 2 * BM;
+            mu = u / nt;
             n0 = (u % nt) * BN;
+            if (p.tiles) {
+                const int4 t = p.tiles[mu];
+                group = t.x;
+                m0 = t.y;
+                m_end = t.z;
+            } else {
+                m0 = mu * 2 * BM;
+            }
             return;
         }
         // banded raster over pair M-tiles
         const int per = kRasterGroup * nt;
         const int g = u / per, in = u % per;
         const int rows = min(kRasterGroup, mt2 - g * kRasterGroup);
-        m0 = (g * kRasterGroup + in % rows) * 2 * BM;
+        mu = g * kRasterGroup + in % rows;
+        m0 = mu * 2 * BM;
         n0 = (in / rows) * BN;
     };
 
@@ -518,16 +532,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::fence_after();
     tc::cluster_sync();
     const uint32_t tmem = *tmem_slot;
-    // PDL: set up while the preceding kernel drains; its outputs are read only after this
+    // PDL: set up while the preceding kernel drains; its outputs (and the tile count) are read
+    // only after this
     tc::griddep_wait();
     tc::griddep_launch_dependents();
+    if (p.tiles) mt2 = *p.n_tiles;
+    units = mt2 * nt;
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer (both CTAs), completions on the leader's barrier
             int g = 0;
             for (int u = first; u < units; u += stride) {
-                int m0, n0;
-                decode2(u, m0, n0);
+                int m0, n0, m_end, group, mu;
+                decode2(u, m0, n0, m_end, group, mu);
+                const int b_row0 = group * p.b_rows_per_group + n0;
                 for (int kb = 0; kb < nk; ++kb, ++g) {
                     const int st = g % STAGES;
                     const uint32_t ph = (g / STAGES) & 1;
@@ -535,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (rank == 0) tc::mbar_expect_tx(&full[st], 2 * (A_BYTES + B_BYTES));
                     const uint32_t bar = tc::mapa(tc::smem_u32(&full[st]), 0);
                     tc::tma_load_2d_cg2(sA + st * A_BYTES, &tmA, bar, kb * BKE, m0 + rank * BM);
-                    tc::tma_load_2d_cg2(sB + st * B_BYTES, &tmB, bar, kb * BKE, n0 + rank * (BN / 2));
+                    tc::tma_load_2d_cg2(sB + st * B_BYTES, &tmB, bar, kb * BKE, b_row0 + rank * (BN / 2));
                 }
             }
         }
@@ -571,12 +589,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = q * 32 + lane;
         int i = 0;
         for (int u = first; u < units; u += stride, ++i) {
-            int m0, n0;
-            decode2(u, m0, n0);
+            int m0, n0, m_end, group, mu;
+            decode2(u, m0, n0, m_end, group, mu);
             const int acc = i & 1;
             const uint32_t ph = (i >> 1) & 1;
             const int64_t m = (int64_t)m0 + rank * BM + row;
-            const bool valid = m < p.M;
+            const bool valid = m < m_end;
             const uint32_t taddr = tmem + acc * BN + ((uint32_t)(q * 32) << 16);
             tc::mbar_wait(&tfull[acc], ph);
             tc::fence_after();
@@ -605,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (valid) p.rowpart[m * nt + nn] = ss;
                 __threadfence();
                 __syncwarp();
-                int* cnt = p.rowcnt + (m0 / (2 * BM)) * 2 + rank;
+                int* cnt = p.rowcnt + mu * 2 + rank;
                 if (lane == 0) {
                     atomicAdd(cnt, 1);
                     const int want = 4 * nt;  // 4 epilogue warps per N-tile
@@ -726,7 +744,7 @@ lattice_status launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const Para
 
 constexpr int kStages2 = 6;
 
-lattice_status launch_2cta(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t st) {
+lattice_status launch_2cta(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid_m, cudaStream_t st) {
     const size_t smem = 1024 + (size_t)kStages2 * (BM * 128 + (BN / 2) * 128) + 256;
     static bool attr_done = false;
     if (!attr_done) {
@@ -765,9 +783,10 @@ lattice_status launch_2cta(const CUtensorMap& ta, const CUtensorMap& tb, const P
             mc = num_sms() / 2;
         mp = mc;
     }
-    const int units = ((p.M + 2 * BM - 1) / (2 * BM)) * ((p.N + BN - 1) / BN);
-    if (swish && !p.rowcnt_zeroed)
-        LAT_CUDA(cudaMemsetAsync(p.rowcnt, 0, sizeof(int) * 2 * ((p.M + 2 * BM - 1) / (2 * BM)), st));
+    // grouped: grid_m carries the tile table's capacity (the kernel reads the live count)
+    const int m_units = p.tiles ? grid_m : (p.M + 2 * BM - 1) / (2 * BM);
+    const int units = m_units * ((p.N + BN - 1) / BN);
+    if (swish && !p.rowcnt_zeroed) LAT_CUDA(cudaMemsetAsync(p.rowcnt, 0, sizeof(int) * 2 * m_units, st));
     int pairs = mp < units ? mp : units;
     if (pairs < 1) pairs = 1;
     // a row block's N-tiles are consecutive units handed round-robin to the pairs: each must land
@@ -806,8 +825,9 @@ bool use_2cta(const Params& p, bool f32) {
         const char* e = std::getenv("LATTICE_GEMM_2CTA");
         env = e ? std::atoi(e) : 1;
     }
-    if (env == 0 || f32 || p.tiles || p.M < 2 * BM || p.a_mn || p.b_mn) return false;
+    if (env == 0 || f32 || p.M < 2 * BM || p.a_mn || p.b_mn) return false;
     if (p.epi == kSwish || p.epi == kSwishHard) return p.rowpart && p.rowcnt && p.N == p.N_full;
+    if (p.tiles) return false;  // grouped tiles: swish epilogue only (the towers' pre-head layer)
     return p.cluster == 1 && (p.epi == kStore || p.epi == kResidNorm);
 }
 
@@ -832,7 +852,7 @@ lattice_status make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uin
 }
 
 lattice_status launch(const GemmPlan& g, cudaStream_t st) {
-    if (g.two_cta) return launch_2cta(g.ta, g.tb, g.p, st);
+    if (g.two_cta) return launch_2cta(g.ta, g.tb, g.p, g.grid_y, st);
     // grid_y carries the number of M units (dense M-tiles, or the tile-table capacity)
     const int nt = (g.p.N + BN - 1) / BN;
     const int units = g.p.cluster > 1 ? g.grid_y : g.grid_y * nt;

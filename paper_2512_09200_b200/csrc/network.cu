@@ -13,6 +13,7 @@
 // are exact in both dtypes).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -24,14 +25,15 @@
 namespace lat {
 namespace {
 
-__global__ void tiles_kernel(const int32_t* __restrict__ seg, int G, int4* __restrict__ tiles,
+// tower tile table: `rows`-row tiles (128: single-CTA grouped GEMM; 256: CTA-pair) per domain segment
+__global__ void tiles_kernel(const int32_t* __restrict__ seg, int G, int rows, int4* __restrict__ tiles,
                              int* __restrict__ n_tiles) {
     __shared__ int pre[65];
     if (threadIdx.x == 0) {
         int run = 0;
         for (int g = 0; g < G; ++g) {
             pre[g] = run;
-            run += (seg[g + 1] - seg[g] + 127) / 128;
+            run += (seg[g + 1] - seg[g] + rows - 1) / rows;
         }
         pre[G] = run;
         *n_tiles = run;
@@ -41,8 +43,46 @@ __global__ void tiles_kernel(const int32_t* __restrict__ seg, int G, int4* __res
     for (int t = threadIdx.x; t < total; t += blockDim.x) {
         int g = 0;
         while (pre[g + 1] <= t) ++g;
-        const int r0 = seg[g] + (t - pre[g]) * 128;
+        const int r0 = seg[g] + (t - pre[g]) * rows;
         tiles[t] = make_int4(g, r0, seg[g + 1], 0);
+    }
+}
+
+// towers on the CTA-pair GEMM: h = swish_rn(W1_g x) came out of the GEMM (fp32, domain-sorted
+// rows); one warp per row forms the heads W2_g . h and writes them in the caller's sample order
+__global__ void tower_heads_kernel(int64_t B, int th, int heads, int G, const float* __restrict__ h,
+                                   const int32_t* __restrict__ seg, const int32_t* __restrict__ order,
+                                   const float* __restrict__ W2, float* __restrict__ logits) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t m = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; m < B;
+         m += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int g = 0;
+        while (g + 1 < G && seg[g + 1] <= m) ++g;
+        const float* hr = h + m * th;
+        const float* w2 = W2 + (int64_t)g * heads * th;
+        float acc[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] = 0.0f;
+        for (int j = lane * 4; j < th; j += 128) {
+            const float4 hv = *reinterpret_cast<const float4*>(hr + j);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if (k < heads) {
+                    const float4 w = __ldg(reinterpret_cast<const float4*>(w2 + (int64_t)k * th + j));
+                    acc[k] += hv.x * w.x + hv.y * w.y + hv.z * w.z + hv.w * w.w;
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (k < heads) acc[k] = warp_sum(acc[k]);
+        if (lane < heads) {
+            float v = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (k == lane) v = acc[k];
+            logits[(int64_t)order[m] * heads + lane] = v;
+        }
     }
 }
 
@@ -136,6 +176,9 @@ struct lattice_net {
     unsigned long long* bad_domain = nullptr;  // checked forwards: first sample with a bad domain
     int4* tiles = nullptr;
     int* n_tiles = nullptr;
+    int tile_rows = 128;         // tower tile table granularity (256: CTA-pair tower)
+    bool tower_pair = false;     // towers = pair swish GEMM into Htower + tower_heads_kernel
+    float* Htower = nullptr;     // [max_batch][tower_hidden] fp32 (tower_pair)
     void* X[2] = {nullptr, nullptr};
     void* Fbuf = nullptr;
     void* H[2] = {nullptr, nullptr};
@@ -319,6 +362,30 @@ lattice_status build_plans(lattice_net* net) {
                        (int)((Bm + 127) / 128), net->f32);
         if (s != LATTICE_OK) return s;
     }
+    if (net->tower_pair) {  // towers: CTA-pair swish GEMM over 256-row domain tiles, heads after
+        gemm::Params p = {};
+        p.M = (int)Bm;
+        p.N = c.tower_hidden;
+        p.K = nd;
+        p.C = net->Htower;
+        p.ldc = c.tower_hidden;
+        p.out_bf16 = 0;
+        p.epi = c.hard ? gemm::kSwishHard : gemm::kSwish;
+        p.N_full = c.tower_hidden;
+        p.cluster = (c.tower_hidden + 255) / 256;
+        p.rowpart = net->rowpart;
+        p.rowcnt = net->rowcnt + (size_t)(c.blocks * (c.n_mlp - 1) + 1) * net->rowcnt_stride;
+        p.rowcnt_zeroed = 1;
+        p.tiles = net->tiles;
+        p.n_tiles = net->n_tiles;
+        p.b_rows_per_group = c.tower_hidden;
+        lattice_status s = gemm::plan(&net->tower_plan, net->X[c.blocks & 1], nd, Bm, net->T1, nd,
+                                      (int64_t)c.domains * c.tower_hidden, p, (int)((Bm + 255) / 256) + c.domains,
+                                      net->f32);
+        if (s == LATTICE_OK && !net->tower_plan.two_cta)
+            return set_error(LATTICE_CUDA, "network: CTA-pair tower plan unavailable");
+        return s;
+    }
     gemm::Params p = {};
     p.M = (int)Bm;
     p.N = c.tower_hidden;
@@ -406,13 +473,21 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
     }
     int max_hidden = 8;
     for (int i = 1; i < c.n_mlp; ++i) max_hidden = max_hidden > c.mlp[i] ? max_hidden : c.mlp[i];
+    {  // towers on the CTA-pair GEMM (bf16, >= 256 rows); LATTICE_TOWER_PAIR=0 keeps the fused
+       // single-CTA grouped tower (heads in its epilogue) for A/B runs
+        const char* e = std::getenv("LATTICE_TOWER_PAIR");
+        net->tower_pair = !net->f32 && Bm >= 256 && !(e && std::atoi(e) == 0);
+        net->tile_rows = net->tower_pair ? 256 : 128;
+        if (net->tower_pair) NET_TRY(dalloc(net, &net->Htower, (size_t)Bm * c.tower_hidden));
+    }
     {  // row-statistics exchange of the swish GEMMs: [rows][N-tiles of the widest] + counters
         const size_t rows = (size_t)((Bm + 255) / 256) * 256;
         int tiles = (max_hidden + 255) / 256;
         if (c.dense_features > 0 && (c.dense_hidden + 255) / 256 > tiles) tiles = (c.dense_hidden + 255) / 256;
         NET_TRY(dalloc(net, &net->rowpart, rows * (size_t)(tiles > 8 ? tiles : 8)));
-        net->rowcnt_stride = rows / 128 + 16;
-        net->rowcnt_total = net->rowcnt_stride * ((size_t)c.blocks * (c.n_mlp - 1) + 1);
+        net->rowcnt_stride = rows / 128 + 2 * (size_t)c.domains + 16;  // grouped tiles: + 2 per domain
+        // slots: every MLP swish GEMM, the dense processor's, the pair tower's
+        net->rowcnt_total = net->rowcnt_stride * ((size_t)c.blocks * (c.n_mlp - 1) + 2);
         NET_TRY(dalloc(net, &net->rowcnt, net->rowcnt_total));
     }
     NET_TRY(dalloc(net, &net->pos, (size_t)Bm));
@@ -420,7 +495,7 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
     NET_TRY(dalloc(net, &net->seg, (size_t)c.domains + 1));
     NET_TRY(dalloc(net, &net->bucket_ws, (size_t)lat::bucket_workspace(Bm, c.domains)));
     NET_TRY(dalloc(net, &net->bad_domain, 1));
-    NET_TRY(dalloc(net, &net->tiles, (size_t)((Bm + 127) / 128 + c.domains)));
+    NET_TRY(dalloc(net, &net->tiles, (size_t)((Bm + 127) / 128 + c.domains + 1)));
     NET_TRY(dalloc(net, &net->n_tiles, 1));
     NET_TRY(dalloc_bytes(net, &net->X[0], es * (size_t)Bm * nd));
     NET_TRY(dalloc_bytes(net, &net->X[1], es * (size_t)Bm * nd));
@@ -573,7 +648,7 @@ lattice_status lattice_net_bucket(lattice_net* net, int64_t batch, const int32_t
     lattice_status s = bucket_ws(batch, net->cfg.domains, domain, net->pos, net->order, net->seg, net->bucket_ws,
                                  (cudaStream_t)stream);
     if (s != LATTICE_OK) return s;
-    tiles_kernel<<<1, 256, 0, stream>>>(net->seg, net->cfg.domains, net->tiles, net->n_tiles);
+    tiles_kernel<<<1, 256, 0, stream>>>(net->seg, net->cfg.domains, net->tile_rows, net->tiles, net->n_tiles);
     LAT_CUDA(cudaGetLastError());
     return LATTICE_OK;
 }
@@ -617,7 +692,7 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
         LAT_CUDA(cudaMemsetAsync(net->bad_domain, 0xff, sizeof(*net->bad_domain), stream));
         FWD_TRY(bucket_ws(B, c.domains, batch->domain, net->pos, net->order, net->seg, net->bucket_ws,
                           (cudaStream_t)stream, net->bad_domain));
-        tiles_kernel<<<1, 256, 0, stream>>>(net->seg, c.domains, net->tiles, net->n_tiles);
+        tiles_kernel<<<1, 256, 0, stream>>>(net->seg, c.domains, net->tile_rows, net->tiles, net->n_tiles);
         LAT_CUDA(cudaGetLastError());
         unsigned long long bad = ~0ull;
         LAT_CUDA(cudaMemcpyAsync(&bad, net->bad_domain, sizeof(bad), cudaMemcpyDeviceToHost, stream));
@@ -725,8 +800,17 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
     gemm::GemmPlan t = net->tower_plan;
     t.p.M = (int)B;
     t.p.logits = logits;
-    t.grid_y = (int)((B + 127) / 128) + c.domains;
-    FWD_TRY(gemm::launch(t, stream));
+    if (net->tower_pair) {
+        t.grid_y = (int)((B + 255) / 256) + c.domains;
+        FWD_TRY(gemm::launch(t, stream));
+        const unsigned grid = (unsigned)((B * 32 + 255) / 256 < 148 * 16 ? (B * 32 + 255) / 256 : 148 * 16);
+        tower_heads_kernel<<<grid, 256, 0, stream>>>(B, c.tower_hidden, c.heads, c.domains, net->Htower, net->seg,
+                                                      net->order, net->T2, logits);
+        LAT_CUDA(cudaGetLastError());
+    } else {
+        t.grid_y = (int)((B + 127) / 128) + c.domains;
+        FWD_TRY(gemm::launch(t, stream));
+    }
     FWD_TRY(mark());
     if (batch->check) FWD_TRY(lattice_device_check(stream));  // checked forwards synchronise anyway
 #undef FWD_TRY
