@@ -469,11 +469,12 @@ __global__ void __launch_bounds__(kResThreads, 1)
 //     have read them, so the next sample's chunks load while this sample's F MMAs and epilogues
 //     run, and its P/L MMAs start on chunk 0 as it lands (the chunks holding LCB rows, read last,
 //     are needed last).
-//   * W_L in [128 x 64] panels (16 KB) through a deep TMA ring (4-5 stages; Y^T also streams, in
-//     [k_pad x 64] panels, so the ring gets its 32 KB), in K-outer order: for each 64-row K panel
-//     of X both L M-tiles and P advance, so P/L consume X chunk by chunk.
-// Warps: 0 X producer, 1 MMA issuer, 2 W_L / Y^T producer, 3..10 LCB group (8 warps: TMEM lane
-// quarter x L M-tile; the M-tile-0 warps also route P to the bf16 Pbuf), 11..14 FM group. TMEM:
+//   * W_L in [128 x 64] panels (16 KB) through a TMA ring (4 stages; Y^T also streams, in
+//     [k_pad x 64] panels through its own ring, so W_L gets its 32 KB), in K-outer order: for each
+//     64-row K panel of X, P and both L M-tiles advance, so P/L consume X chunk by chunk.
+// Warps: 0 X producer, 1 MMA issuer (the whole warp walks the schedule, one elected lane issues),
+// 2 W_L producer, 3..10 LCB group (8 warps: TMEM lane quarter x L M-tile; the M-tile-0 warps
+// also route P to the bf16 Pbuf), 11..14 FM group, 15 Y^T producer. TMEM:
 // P | L (2 M-tiles) | F (4 M-tiles) in one 512-column region, with separate "drained" barriers
 // for P+L (LCB group) and F (FM group), so this sample's FM epilogue overlaps the next sample's
 // P/L MMAs.
@@ -491,9 +492,9 @@ __global__ void __launch_bounds__(kResThreads, 1)
         }                                                                         \
     } while (0)
 
-constexpr int kLargeWarps = 15;
+constexpr int kLargeWarps = 16;
 constexpr int kLargeThreads = kLargeWarps * 32;
-constexpr int kYtStages = 2;
+constexpr int kYtStages = 4;
 
 struct GeoL {
     int panels_n, ml, mf, chunks, wl_stages;
@@ -508,7 +509,7 @@ struct GeoL {
         ppanel = (uint32_t)p.k_pad * 128u;
         wlpanel = 128u * 128u;
         pbytes = (2 * ppanel + 1023u) & ~1023u;
-        // as many W_L stages as fit next to X, the Y^T ring and Pbuf (227 KB per CTA)
+        // as many W_L stages (<= 5) as fit next to X, the Y^T ring and Pbuf (227 KB per CTA)
         const int64_t left = 227 * 1024 - 1024 - 512 - 2 * (int64_t)xpanel - kYtStages * (int64_t)ytpanel - pbytes;
         wl_stages = (int)(left / wlpanel);
         if (wl_stages > 5) wl_stages = 5;
@@ -533,15 +534,15 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
     uint64_t* x_empty = bars + 4;             // [4] chunk consumed (its F M-tile done)
     uint64_t* wl_full = bars + 8;             // [NW <= 5]
     uint64_t* wl_empty = bars + 13;           // [NW]
-    uint64_t* yt_full = bars + 18;            // [2]
-    uint64_t* yt_empty = bars + 20;           // [2]
-    uint64_t* pl_full = bars + 22;            // P and L accumulated
-    uint64_t* pbuf_full = bars + 23;          // P routed to Pbuf (bf16)
-    uint64_t* f_full = bars + 24;             // F accumulated
-    uint64_t* l_empty = bars + 25;            // P + L region drained (LCB group)
-    uint64_t* f_empty = bars + 26;            // F region drained (FM group)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 27);
-    float* red_f = reinterpret_cast<float*>(bars + 28);   // [2][4]
+    uint64_t* yt_full = bars + 18;            // [kYtStages = 4]
+    uint64_t* yt_empty = bars + 22;           // [4]
+    uint64_t* pl_full = bars + 26;            // P and L accumulated
+    uint64_t* pbuf_full = bars + 27;          // P routed to Pbuf (bf16)
+    uint64_t* f_full = bars + 28;             // F accumulated
+    uint64_t* l_empty = bars + 29;            // P + L region drained (LCB group)
+    uint64_t* f_empty = bars + 30;            // F region drained (FM group)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 31);
+    float* red_f = reinterpret_cast<float*>(bars + 32);   // [2][4]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0 && lane == 0) {
@@ -595,16 +596,11 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
             if (p.trace) p.trace[blockIdx.x * 16 + 8] = wt[8];
         }
     } else if (warp == 2) {
-        if (lane == 0) {  // ---- W_L / Y^T producer, in the MMA's K-outer order
+        if (lane == 0) {  // ---- W_L producer, in the MMA's K-outer order
             unsigned long long wt[16] = {0};
-            int gw = 0, gy = 0;
+            int gw = 0;
             for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
                 for (int kp = 0; kp < g.panels_n; ++kp) {
-                    const int sy = gy % kYtStages;
-                    FM_WAIT(9, &yt_empty[sy], ((gy / kYtStages) & 1) ^ 1);
-                    tc::mbar_expect_tx(&yt_full[sy], g.ytpanel);
-                    tc::tma_load_2d(sYT + sy * g.ytpanel, &tmYT, &yt_full[sy], kp * 64, 0);
-                    ++gy;
                     for (int mt = 0; mt < g.ml; ++mt, ++gw) {
                         const int s = gw % NW;
                         FM_WAIT(10, &wl_empty[s], ((gw / NW) & 1) ^ 1);
@@ -613,72 +609,83 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
                     }
                 }
             }
-            if (p.trace) p.trace[blockIdx.x * 16 + 9] = wt[9], p.trace[blockIdx.x * 16 + 10] = wt[10];
+            if (p.trace) p.trace[blockIdx.x * 16 + 10] = wt[10];
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---- MMA issuer
-            const uint32_t id_P = tc::idesc_bf16(128, kpad, 1, 0);
-            const uint32_t id_L = tc::idesc_bf16(128, d, 0, 1);
-            const uint32_t id_F = tc::idesc_bf16(128, kpad, 0, 0);
-            const uint32_t pb = tc::smem_u32(sP), xs = tc::smem_u32(sX);
-            const uint32_t wl0 = tc::smem_u32(sWL), yt0 = tc::smem_u32(sYT);
-            int it = 0, gw = 0, gy = 0;
+    } else if (warp == 15) {
+        if (lane == 0) {  // ---- Y^T producer: [k_pad x 64] panels, its own ring (4 deep)
             unsigned long long wt[16] = {0};
-            const long long t_start = clock64();
-            for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
-                const uint32_t ph = it & 1;
-                FM_WAIT(0, l_empty, ph ^ 1);  // the previous sample's P and L are drained
-                tc::fence_after();
-                for (int kp = 0; kp < g.panels_n; ++kp) {
-                    if ((kp & 1) == 0) FM_WAIT(1, &x_full[kp >> 1], ph);
+            int gy = 0;
+            for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
+                for (int kp = 0; kp < g.panels_n; ++kp, ++gy) {
                     const int sy = gy % kYtStages;
-                    FM_WAIT(2, &yt_full[sy], (gy / kYtStages) & 1);
-                    tc::fence_after();
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {  // P += X^T[:, k0:k0+16] . Y[k0:k0+16, :]
-                        const int k0 = kp * 64 + j * 16;
-                        const uint64_t a_xt = tc::sdesc(xs + k0 * 128, g.xpanel, 1024, 2);
-                        const uint64_t b_y = tc::sdesc(yt0 + sy * g.ytpanel + j * 32, 16, 1024, 2);
-                        tc::mma_f16(t_Pb, a_xt, b_y, id_P, (kp | j) != 0);
-                    }
-                    tc::mma_commit(&yt_empty[sy]);
-                    ++gy;
-                    for (int mt = 0; mt < g.ml; ++mt, ++gw) {  // L[mt] += W_L[mt, k0:k0+64] . X[k0:k0+64, :]
-                        const int s = gw % NW;
-                        FM_WAIT(3, &wl_full[s], (gw / NW) & 1);
-                        tc::fence_after();
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int k0 = kp * 64 + j * 16;
-                            const uint64_t a_wl = tc::sdesc(wl0 + s * g.wlpanel + j * 32, 16, 1024, 2);
-                            const uint64_t b_x = tc::sdesc(xs + k0 * 128, g.xpanel, 1024, 2);
-                            tc::mma_f16(t_Lb + mt * 128, a_wl, b_x, id_L, (kp | j) != 0);
-                        }
-                        tc::mma_commit(&wl_empty[s]);
-                    }
+                    FM_WAIT(9, &yt_empty[sy], ((gy / kYtStages) & 1) ^ 1);
+                    tc::mbar_expect_tx(&yt_full[sy], g.ytpanel);
+                    tc::tma_load_2d(sYT + sy * g.ytpanel, &tmYT, &yt_full[sy], kp * 64, 0);
                 }
-                tc::mma_commit(pl_full);
-                FM_WAIT(4, pbuf_full, ph);
-                FM_WAIT(5, f_empty, ph ^ 1);  // the previous sample's F is drained
+            }
+            if (p.trace) p.trace[blockIdx.x * 16 + 9] = wt[9];
+        }
+    } else if (warp == 1) {  // ---- MMA issuer: the whole warp walks the schedule, one lane issues
+        const uint32_t id_P = tc::idesc_bf16(128, kpad, 1, 0);
+        const uint32_t id_L = tc::idesc_bf16(128, d, 0, 1);
+        const uint32_t id_F = tc::idesc_bf16(128, kpad, 0, 0);
+        // descriptors built once; a step moves the 14-bit start address field (bytes >> 4) only
+        const uint64_t dx_mn = tc::sdesc(tc::smem_u32(sX), g.xpanel, 1024, 2);      // X^T (P: A) / X (L: B)
+        const uint64_t dx_k = tc::sdesc(tc::smem_u32(sX), 16, 1024, 2);             // X (F: A)
+        const uint64_t dy = tc::sdesc(tc::smem_u32(sYT), 16, 1024, 2);
+        const uint64_t dwl = tc::sdesc(tc::smem_u32(sWL), 16, 1024, 2);
+        const uint64_t dp = tc::sdesc(tc::smem_u32(sP), 16, 1024, 2);
+        int it = 0, sw = 0, sy = 0;
+        uint32_t pw = 0, py = 0;  // ring phases
+        unsigned long long wt[16] = {0};
+        const long long t_start = clock64();
+        for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
+            const uint32_t ph = it & 1;
+            FM_WAIT(0, l_empty, ph ^ 1);  // the previous sample's P and L are drained
+            tc::fence_after();
+            for (int kp = 0; kp < g.panels_n; ++kp) {
+                if ((kp & 1) == 0) FM_WAIT(1, &x_full[kp >> 1], ph);
+                FM_WAIT(2, &yt_full[sy], py);
                 tc::fence_after();
-                for (int mt = 0; mt < g.mf; ++mt) {  // F = X P, M-tile mt = X chunk mt
+                const uint64_t xk = dx_mn + (uint64_t)((kp * 64 * 128) >> 4);
+                const uint64_t yk = dy + (uint64_t)((sy * g.ytpanel) >> 4);
 #pragma unroll
-                    for (int kk = 0; kk < d / 16; ++kk) {
-                        const int k0 = kk * 16;
-                        const uint32_t pan = (uint32_t)(k0 / 64), kin = (uint32_t)(k0 % 64) * 2;
-                        const uint64_t a_x = tc::sdesc(xs + pan * g.xpanel + mt * 16384 + kin, 16, 1024, 2);
-                        const uint64_t b_p = tc::sdesc(pb + pan * g.ppanel + kin, 16, 1024, 2);
-                        tc::mma_f16(t_Fb + mt * kpad, a_x, b_p, id_F, kk != 0);
-                    }
-                    tc::mma_commit(&x_empty[mt]);  // every MMA reading chunk mt has completed
+                for (int j = 0; j < 4; ++j)  // P += X^T[:, k0:k0+16] . Y[k0:k0+16, :]
+                    tc::mma_f16_warp(t_Pb, xk + (uint64_t)((j * 16 * 128) >> 4), yk + (uint64_t)(j * 2), id_P,
+                                     (kp | j) != 0);
+                tc::mma_commit_warp(&yt_empty[sy]);
+                if (++sy == kYtStages) sy = 0, py ^= 1;
+                for (int mt = 0; mt < g.ml; ++mt) {  // L[mt] += W_L[mt, k0:k0+64] . X[k0:k0+64, :]
+                    FM_WAIT(3, &wl_full[sw], pw);
+                    tc::fence_after();
+                    const uint64_t wk = dwl + (uint64_t)((sw * g.wlpanel) >> 4);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        tc::mma_f16_warp(t_Lb + mt * 128, wk + (uint64_t)(j * 2), xk + (uint64_t)((j * 16 * 128) >> 4),
+                                         id_L, (kp | j) != 0);
+                    tc::mma_commit_warp(&wl_empty[sw]);
+                    if (++sw == NW) sw = 0, pw ^= 1;
                 }
-                tc::mma_commit(f_full);
             }
-            if (p.trace) {
-                for (int i = 0; i < 6; ++i) p.trace[blockIdx.x * 16 + i] = wt[i];
-                p.trace[blockIdx.x * 16 + 6] = (unsigned long long)(clock64() - t_start);
-                p.trace[blockIdx.x * 16 + 7] = (unsigned long long)it;
+            tc::mma_commit_warp(pl_full);
+            FM_WAIT(4, pbuf_full, ph);
+            FM_WAIT(5, f_empty, ph ^ 1);  // the previous sample's F is drained
+            tc::fence_after();
+            for (int mt = 0; mt < g.mf; ++mt) {  // F = X P, M-tile mt = X chunk mt
+#pragma unroll
+                for (int kk = 0; kk < d / 16; ++kk) {
+                    const uint32_t pan = (uint32_t)(kk / 4), kin = (uint32_t)(kk % 4) * 32;
+                    tc::mma_f16_warp(t_Fb + mt * kpad, dx_k + (uint64_t)((pan * g.xpanel + mt * 16384 + kin) >> 4),
+                                     dp + (uint64_t)((pan * g.ppanel + kin) >> 4), id_F, kk != 0);
+                }
+                tc::mma_commit_warp(&x_empty[mt]);  // every MMA reading chunk mt has completed
             }
+            tc::mma_commit_warp(f_full);
+        }
+        if (p.trace && lane == 0) {
+            for (int i = 0; i < 6; ++i) p.trace[blockIdx.x * 16 + i] = wt[i];
+            p.trace[blockIdx.x * 16 + 6] = (unsigned long long)(clock64() - t_start);
+            p.trace[blockIdx.x * 16 + 7] = (unsigned long long)it;
         }
     } else if (warp < 11) {  // ---- LCB group, warps 3..10: lane quarter q, L M-tile mt
         const int q = warp & 3;
@@ -901,17 +908,28 @@ lattice_status launch_t(const Plan& pl, cudaStream_t st) {
 
 // programmatic stream serialization unless LATTICE_PDL=0 (see tc::griddep_wait)
 template <typename K>
-cudaError_t launch_pdl(K kernel, int grid, int threads, size_t smem, cudaStream_t st, const Plan& pl) {
+cudaError_t launch_pdl(K kernel, int grid, int threads, size_t smem, cudaStream_t st, const Plan& pl, int cluster = 1) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid, 1, 1);
     cfg.blockDim = dim3(threads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (cluster > 1) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = cluster;
+        at[na].val.clusterDim.y = 1;
+        at[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (pdl_enabled()) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kernel, pl.tmX, pl.tmWL, pl.tmYT, pl.p);
 }
 
