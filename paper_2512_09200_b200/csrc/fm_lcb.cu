@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---- MMA issuer
+        {  // ---- MMA issuer: the whole warp walks the schedule, one elected lane issues (tc.cuh)
             // bf16: A = X^T and B = X read MN-major from the X image; fp32: K-major X^T copy
             constexpr int mn = ES == 2 ? 1 : 0;
             const uint32_t id_P = tc::idesc_fmt(Op::kFormat, 128, kpad, mn, 0);
@@ -241,12 +241,12 @@ __global__ void __launch_bounds__(kResThreads, 1)
                                                   : tc::sdesc(xt + kp * 16384 + kin, 16, 1024, 2);
                     // P += X^T[:, k0:k0+KK] . Y[k0:k0+KK, :]
                     const uint64_t b_y = tc::sdesc(yt + kp * g.ytpanel + kin, 16, 1024, 2);
-                    Op::mma(t_P, x_op, b_y, id_P, kk != 0);
+                    Op::mma_warp(t_P, x_op, b_y, id_P, kk != 0);
                     // L += W_L[:, k0:k0+KK] . X[k0:k0+KK, :]
                     const uint64_t a_wl = tc::sdesc(wl + kp * g.wlpanel + kin, 16, 1024, 2);
-                    Op::mma(t_L, a_wl, x_op, id_L, kk != 0);
+                    Op::mma_warp(t_L, a_wl, x_op, id_L, kk != 0);
                 }
-                tc::mma_commit(&pl_full[rg]);
+                tc::mma_commit_warp(&pl_full[rg]);
                 tc::mbar_wait(pbuf_full, it & 1);
                 tc::fence_after();
                 for (int mt = 0; mt < m_tiles; ++mt) {
@@ -255,10 +255,10 @@ __global__ void __launch_bounds__(kResThreads, 1)
                         const uint32_t pan = (uint32_t)(k0 / EP), kin = (uint32_t)(k0 % EP) * ES;
                         const uint64_t a_x = tc::sdesc(xs + pan * g.xpanel + mt * 16384 + kin, 16, 1024, 2);
                         const uint64_t b_p = tc::sdesc(pb + pan * g.ppanel + kin, 16, 1024, 2);
-                        Op::mma(t_F + mt * kpad, a_x, b_p, id_F, kk != 0);
+                        Op::mma_warp(t_F + mt * kpad, a_x, b_p, id_F, kk != 0);
                     }
                 }
-                tc::mma_commit(&f_full[rg]);
+                tc::mma_commit_warp(&f_full[rg]);
             }
         }
     } else if (warp < 2 + kLcbWarps) {  // ---- LCB group, warps 2..9: thread = TMEM lane

@@ -197,6 +197,16 @@ __device__ __forceinline__ void mma_f16_warp(uint32_t d_tmem, uint64_t adesc, ui
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+__device__ __forceinline__ void mma_tf32_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 __device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
@@ -256,12 +266,18 @@ struct Operand<__nv_bfloat16> {
     __device__ static void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
         mma_f16(d, a, b, id, acc);
     }
+    __device__ static void mma_warp(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+        mma_f16_warp(d, a, b, id, acc);
+    }
 };
 template <>
 struct Operand<float> {
     static constexpr int kBytes = 4, kRow = 32, kK = 8, kFormat = 2;  // TF32
     __device__ static void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
         mma_tf32(d, a, b, id, acc);
+    }
+    __device__ static void mma_warp(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+        mma_tf32_warp(d, a, b, id, acc);
     }
 };
 
