@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---- MMA issuer
+        {  // ---- MMA issuer: the whole warp walks the schedule, one elected lane issues
             const uint32_t idesc = tc::idesc_fmt(Op::kFormat, BM, BN, p.a_mn, p.b_mn);
             int g = 0, i = 0;
             for (int u = s.first; u < s.units; u += s.stride, ++i) {
@@ -307,11 +307,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                    : tc::sdesc(a_base + k * 32, 16, 1024, 2);
                         const uint64_t bd = p.b_mn ? tc::sdesc(b_base + k * 2048, 8192, 1024, 2)
                                                    : tc::sdesc(b_base + k * 32, 16, 1024, 2);
-                        Op::mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                        Op::mma_warp(d_tmem, ad, bd, idesc, (kb | k) != 0);
                     }
-                    tc::mma_commit(&empty[st]);
+                    tc::mma_commit_warp(&empty[st]);
                 }
-                tc::mma_commit(&tfull[acc]);
+                tc::mma_commit_warp(&tfull[acc]);
             }
         }
     } else {  // ---- epilogue warps 2..5
@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {  // ---- MMA issuer: the leader only
+        if (rank == 0) {  // ---- MMA issuer: the leader's warp walks the schedule, one lane issues
             constexpr uint32_t idesc = tc::idesc_fmt(Op::kFormat, 2 * BM, BN, 0, 0);
             int g = 0, i = 0;
             for (int u = first; u < units; u += stride, ++i) {
@@ -577,11 +577,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int k = 0; k < 4; ++k) {
                         const uint64_t ad = tc::sdesc(a_base + k * 32, 16, 1024, 2);
                         const uint64_t bd = tc::sdesc(b_base + k * 32, 16, 1024, 2);
-                        tc::mma_f16_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                        tc::mma_f16_cg2_warp(d_tmem, ad, bd, idesc, (kb | k) != 0);
                     }
-                    tc::mma_commit_cg2(&empty[st]);
+                    tc::mma_commit_cg2_warp(&empty[st]);
                 }
-                tc::mma_commit_cg2(&tfull[acc]);
+                tc::mma_commit_cg2_warp(&tfull[acc]);
             }
         }
     } else {  // ---- epilogue warps 2..5 (both CTAs): this CTA's 128 accumulator rows
