@@ -56,7 +56,9 @@ def net_config(**kw):
     (dict(n=600, nF=300, nL=300), "n must be in [1, 512]"),
     (dict(k=65), "k must be in [1, 64]"),
     (dict(mlp=[31, 64, 256]), "mlp[0] must equal n*k"),
-    (dict(mlp=[32, 4096, 256]), "hidden widths above 2048"),
+    (dict(mlp=[32, 20000, 256]), "hidden widths above 16384"),
+    (dict(mlp=[32, 4096, 256], max_batch=128), "hidden widths above 2048 need bf16 and max_batch >= 256"),
+    (dict(mlp=[32, 4096, 256], dtype=L.F32), "hidden widths above 2048 need bf16"),
     (dict(domains=33), "domains must be in [1, 32]"),
     (dict(heads=17), "heads must be in [1, 16]"),
     (dict(tower_hidden=12), "tower_hidden must be a multiple of 8"),
