@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
 
 constexpr int kLargeWarps = 16;
 constexpr int kLargeThreads = kLargeWarps * 32;
-constexpr int kYtStages = 4;
+constexpr int kYtStages = 2;
 
 struct GeoL {
     int panels_n, ml, mf, chunks, wl_stages;
@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
     uint64_t* x_empty = bars + 4;             // [4] chunk consumed (its F M-tile done)
     uint64_t* wl_full = bars + 8;             // [NW <= 5]
     uint64_t* wl_empty = bars + 13;           // [NW]
-    uint64_t* yt_full = bars + 18;            // [kYtStages = 4]
+    uint64_t* yt_full = bars + 18;            // [kYtStages <= 4]
     uint64_t* yt_empty = bars + 22;           // [4]
     uint64_t* pl_full = bars + 26;            // P and L accumulated
     uint64_t* pbuf_full = bars + 27;          // P routed to Pbuf (bf16)
@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
             if (p.trace) p.trace[blockIdx.x * 16 + 10] = wt[10];
         }
     } else if (warp == 15) {
-        if (lane == 0) {  // ---- Y^T producer: [k_pad x 64] panels, its own ring (4 deep)
+        if (lane == 0) {  // ---- Y^T producer: [k_pad x 64] panels through its own ring
             unsigned long long wt[16] = {0};
             int gy = 0;
             for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
