@@ -15,6 +15,7 @@
 // Every reduction runs in a fixed order (per-chunk partials, then a fixed-order sum): gradients are
 // deterministic, so data-parallel replicas that all-reduce them stay bit-identical.
 #include <cuda_bf16.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <string>
 #include <vector>
@@ -210,6 +211,10 @@ lattice_status sgd_update(int64_t n, float lr, const float* grad, float* master,
 
 // The towers' backward (see the file header); called by lattice_net_tower_backward (network.cu).
 lattice_status tower_backward(const TowerBwd& a, cudaStream_t st) {
+    nvtxRangePushA("lattice::tower_backward");
+    struct Pop {
+        ~Pop() { nvtxRangePop(); }
+    } pop;
     const int64_t B = a.B;
     const int G = a.G, th = a.th, heads = a.heads;
     const int64_t nd = a.nd;

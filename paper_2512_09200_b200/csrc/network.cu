@@ -12,6 +12,7 @@
 // weight_seed with the counter-based scheme shared with oracle/lattice_oracle.c (the values
 // are exact in both dtypes).
 #include <cuda_bf16.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdlib>
 #include <string>
@@ -685,9 +686,20 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
         lattice_status _s = (x);                  \
         if (_s != LATTICE_OK) return _s;          \
     } while (0)
+    // NVTX ranges name the stages for Nsight Systems / any NVTX tool (no-ops without one attached)
+    struct Range {
+        bool open = true;
+        explicit Range(const char* name) { nvtxRangePushA(name); }
+        void end() {
+            if (open) nvtxRangePop();
+            open = false;
+        }
+        ~Range() { end(); }
+    } range_forward("lattice::net_forward");
     const bool in_place = !batch->tables && batch->pooled_layout == 2;  // X0 written by peers
     const int nc = c.n - c.dense_features;  // sparse (table-pooled) embeddings come first
     FWD_TRY(mark());
+    Range range_embed("lattice::bucket+embedding");
     if (!in_place && batch->check) {  // checked: a domain outside [0, domains) is a DataError
         LAT_CUDA(cudaMemsetAsync(net->bad_domain, 0xff, sizeof(*net->bad_domain), stream));
         FWD_TRY(bucket_ws(B, c.domains, batch->domain, net->pos, net->order, net->seg, net->bucket_ws,
@@ -783,8 +795,10 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
                 static_cast<__nv_bfloat16*>(net->X[0]), c.n, nc);
         LAT_CUDA(cudaGetLastError());
     }
+    range_embed.end();
     FWD_TRY(mark());
     for (int blk = 0; blk < c.blocks; ++blk) {
+        Range range_block("lattice::dwfb_block");
         fm::Plan fp = net->fm_plans[blk];
         fp.p.B = B;
         FWD_TRY(fm::launch(fp, stream));
@@ -797,6 +811,7 @@ lattice_status lattice_net_forward(lattice_net* net, const lattice_batch* batch,
         }
         FWD_TRY(mark());
     }
+    Range range_towers("lattice::towers");
     gemm::GemmPlan t = net->tower_plan;
     t.p.M = (int)B;
     t.p.logits = logits;
