@@ -563,6 +563,8 @@ def run_mid(args, rank, world, local):
     # per step: domain bucketing (histogram, block scan, ranks) + tiles + bag, then per block the
     # FM/LCB kernel and one GEMM per MLP layer, then the grouped tower
     launches = 5 + c["blocks"] * (1 + len(c["mlp"]) - 1) + 1
+    if os.environ.get("LATTICE_TOWER_PAIR", "1") != "0":
+        launches += 1  # the towers run as the CTA-pair swish GEMM + tower_heads_kernel
     if peer:
         pb.check()
         launches += 2  # two barrier kernels (the bag slot above is the owner kernel)

@@ -54,11 +54,14 @@ __global__ void tiles_kernel(const int32_t* __restrict__ seg, int G, int rows, i
 __global__ void tower_heads_kernel(int64_t B, int th, int heads, int G, const float* __restrict__ h,
                                    const int32_t* __restrict__ seg, const int32_t* __restrict__ order,
                                    const float* __restrict__ W2, float* __restrict__ logits) {
+    __shared__ int32_t sseg[33];
+    for (int i = threadIdx.x; i <= G; i += blockDim.x) sseg[i] = seg[i];
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     for (int64_t m = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; m < B;
          m += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         int g = 0;
-        while (g + 1 < G && seg[g + 1] <= m) ++g;
+        while (g + 1 < G && sseg[g + 1] <= m) ++g;
         const float* hr = h + m * th;
         const float* w2 = W2 + (int64_t)g * heads * th;
         float acc[16];

@@ -359,3 +359,20 @@ def test_error_is_not_vacuous():
     bad = net.forward(dom, offsets, ids, ptrs, rws, torch.bfloat16).cpu().numpy()
     with pytest.raises(AssertionError):
         calibrated("sensitivity: one tower head negated", bad, ref64, ref32)
+
+
+def test_tower_paths_agree(tmp_path):
+    """The CTA-pair tower (default) and the round-1 single-CTA grouped tower (LATTICE_TOWER_PAIR=0)
+    compute the same fp32 heads from the same bf16 X_L: equal up to fp32 summation order."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = {}
+    for env in ("1", "0"):
+        f = tmp_path / f"logits_{env}.npy"
+        r = subprocess.run([sys.executable, os.path.join(here, "tower_path_check.py"), str(f)],
+                           env=dict(os.environ, LATTICE_TOWER_PAIR=env), capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stdout + r.stderr
+        out[env] = np.load(f)
+    np.testing.assert_allclose(out["1"], out["0"], rtol=1e-5, atol=1e-5)
