@@ -537,6 +537,15 @@ def run_mid(args, rank, world, local):
                     dst.copy_(src, non_blocking=True)
             copied[i % 2].record(cstream)
 
+    e2e_graphs = [None, None]  # the forward over each input buffer, replayed like the device-resident step
+
+    def e2e_forward(i):
+        if e2e_graphs[i % 2] is not None:
+            e2e_graphs[i % 2].replay()
+            return
+        o, ii, dm = bufs[i % 2]
+        forward(dm, o, ii, logits, d_imp[i % 2] if full else None, d_dv[i % 2] if full else None)
+
     def e2e_run(k):
         for e in consumed:
             e.record(stream)
@@ -545,13 +554,22 @@ def run_mid(args, rank, world, local):
             if i + 1 < k:
                 h2d(i + 1)
             stream.wait_event(copied[i % 2])
-            o, ii, dm = bufs[i % 2]
-            forward(dm, o, ii, logits, d_imp[i % 2] if full else None, d_dv[i % 2] if full else None)
+            e2e_forward(i)
             consumed[i % 2].record(stream)
             h_out.copy_(logits, non_blocking=True)
 
     e2e_run(2)
     torch.cuda.synchronize()
+    if args.graph:  # the same launch path as `value`: the forward step of each buffer from a graph
+        for i in range(2):
+            g = torch.cuda.CUDAGraph()
+            o, ii, dm = bufs[i]
+            with torch.cuda.graph(g):
+                forward(dm, o, ii, logits, d_imp[i] if full else None, d_dv[i] if full else None)
+            e2e_graphs[i] = g
+        stream = torch.cuda.current_stream()
+        e2e_run(2)
+        torch.cuda.synchronize()
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
