@@ -536,13 +536,15 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
     uint64_t* wl_empty = bars + 13;           // [NW]
     uint64_t* yt_full = bars + 18;            // [kYtStages <= 4]
     uint64_t* yt_empty = bars + 22;           // [4]
-    uint64_t* pl_full = bars + 26;            // P and L accumulated
+    uint64_t* pl_full = bars + 26;            // P and L M-tile 0 accumulated
     uint64_t* pbuf_full = bars + 27;          // P routed to Pbuf (bf16)
     uint64_t* f_full = bars + 28;             // F accumulated
-    uint64_t* l_empty = bars + 29;            // P + L region drained (LCB group)
+    uint64_t* l_empty = bars + 29;            // P + L M-tile 0 drained (LCB M-tile-0 warps)
     uint64_t* f_empty = bars + 30;            // F region drained (FM group)
+    uint64_t* l1_full = bars + 33;            // L M-tile 1 accumulated
+    uint64_t* l1_empty = bars + 34;           // L M-tile 1 drained (LCB M-tile-1 warps)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 31);
-    float* red_f = reinterpret_cast<float*>(bars + 32);   // [2][4]
+    float* red_f = reinterpret_cast<float*>(bars + 35);   // [2][4]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0 && lane == 0) {
@@ -567,7 +569,9 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
         tc::mbar_init(pl_full, 1);
         tc::mbar_init(pbuf_full, 128);
         tc::mbar_init(f_full, 1);
-        tc::mbar_init(l_empty, 8 * 32);
+        tc::mbar_init(l_empty, 4 * 32);
+        tc::mbar_init(l1_full, 1);
+        tc::mbar_init(l1_empty, 4 * 32);
         tc::mbar_init(f_empty, 4 * 32);
         tc::fence_mbar_init();
     }
@@ -600,8 +604,8 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
             unsigned long long wt[16] = {0};
             int gw = 0;
             for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
-                for (int kp = 0; kp < g.panels_n; ++kp) {
-                    for (int mt = 0; mt < g.ml; ++mt, ++gw) {
+                for (int mt = 0; mt < g.ml; ++mt) {  // the MMA's order: M-tile 0 over K, then M-tile 1
+                    for (int kp = 0; kp < g.panels_n; ++kp, ++gw) {
                         const int s = gw % NW;
                         FM_WAIT(10, &wl_empty[s], ((gw / NW) & 1) ^ 1);
                         tc::mbar_expect_tx(&wl_full[s], g.wlpanel);
@@ -641,8 +645,22 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
         const long long t_start = clock64();
         for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
             const uint32_t ph = it & 1;
-            FM_WAIT(0, l_empty, ph ^ 1);  // the previous sample's P and L are drained
+            // P and L M-tile 0 over every K panel, then L M-tile 1: the LCB warps of M-tile 0 drain
+            // their rows (and route P) while M-tile 1 accumulates, and vice versa across samples
+            FM_WAIT(0, l_empty, ph ^ 1);  // the previous sample's P and L M-tile 0 are drained
             tc::fence_after();
+            auto l_panel = [&](int mt, int kp) {  // L[mt] += W_L[mt, k0:k0+64] . X[k0:k0+64, :]
+                FM_WAIT(3, &wl_full[sw], pw);
+                tc::fence_after();
+                const uint64_t xk = dx_mn + (uint64_t)((kp * 64 * 128) >> 4);
+                const uint64_t wk = dwl + (uint64_t)((sw * g.wlpanel) >> 4);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    tc::mma_f16_warp(t_Lb + mt * 128, wk + (uint64_t)(j * 2), xk + (uint64_t)((j * 16 * 128) >> 4), id_L,
+                                     (kp | j) != 0);
+                tc::mma_commit_warp(&wl_empty[sw]);
+                if (++sw == NW) sw = 0, pw ^= 1;
+            };
             for (int kp = 0; kp < g.panels_n; ++kp) {
                 if ((kp & 1) == 0) FM_WAIT(1, &x_full[kp >> 1], ph);
                 FM_WAIT(2, &yt_full[sy], py);
@@ -655,19 +673,15 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
                                      (kp | j) != 0);
                 tc::mma_commit_warp(&yt_empty[sy]);
                 if (++sy == kYtStages) sy = 0, py ^= 1;
-                for (int mt = 0; mt < g.ml; ++mt) {  // L[mt] += W_L[mt, k0:k0+64] . X[k0:k0+64, :]
-                    FM_WAIT(3, &wl_full[sw], pw);
-                    tc::fence_after();
-                    const uint64_t wk = dwl + (uint64_t)((sw * g.wlpanel) >> 4);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        tc::mma_f16_warp(t_Lb + mt * 128, wk + (uint64_t)(j * 2), xk + (uint64_t)((j * 16 * 128) >> 4),
-                                         id_L, (kp | j) != 0);
-                    tc::mma_commit_warp(&wl_empty[sw]);
-                    if (++sw == NW) sw = 0, pw ^= 1;
-                }
+                if (g.ml > 0) l_panel(0, kp);
             }
             tc::mma_commit_warp(pl_full);
+            if (g.ml > 1) {
+                FM_WAIT(0, l1_empty, ph ^ 1);  // the previous sample's L M-tile 1 is drained
+                tc::fence_after();
+                for (int kp = 0; kp < g.panels_n; ++kp) l_panel(1, kp);
+                tc::mma_commit_warp(l1_full);
+            }
             FM_WAIT(4, pbuf_full, ph);
             FM_WAIT(5, f_empty, ph ^ 1);  // the previous sample's F is drained
             tc::fence_after();
@@ -700,7 +714,8 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
         const uint32_t t_L = t_Lb + lane_off + mt * 128;
         int it = 0;
         for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
-            tc::mbar_wait(pl_full, it & 1);
+            if (mt == 1 && g.ml < 2) continue;  // nL <= 128: no second L M-tile
+            tc::mbar_wait(mt == 0 ? pl_full : l1_full, it & 1);
             tc::fence_after();
             if (mt == 0) {  // P row `row` (a d index) -> bf16 -> Pbuf[j][row], F's K-major B operand
                 for (int c0 = 0; c0 < kpad; c0 += 16) {
@@ -758,7 +773,7 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
                 tc::mbar_arrive(&x_empty[cx]);
             }
             tc::fence_before();
-            tc::mbar_arrive(l_empty);
+            tc::mbar_arrive(mt == 0 ? l_empty : l1_empty);
         }
     } else {  // ---- FM group, warps 11..14: Fin = rms_norm(flatten(X P)) over 4 M-tiles, two TMEM passes
         const int q = warp & 3;
