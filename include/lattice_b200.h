@@ -521,7 +521,8 @@ lattice_status lattice_net_bucket(lattice_net* net, int64_t batch, const int32_t
  * export), 1 = sample_pos int32 [max_batch] (row of sample b in the domain-sorted activations),
  * 2 = the second activation buffer. Blocks ping-pong: block l reads buffer (l & 1 ? 2 : 0) and
  * writes the other, so after a forward buffer (blocks & 1 ? 2 : 0) holds the last block's output
- * X_L (the towers' input) and the other X_{L-1} (inspection / stage-wise tests). NULL for an
+ * X_L (the towers' input) and the other X_{L-1} (inspection / stage-wise tests); 3 = Fin
+ * [max_batch][n*k] (net dtype, domain-sorted rows): the last block's MLP input. NULL for an
  * unknown index. */
 void* lattice_net_buffer(lattice_net* net, int32_t which);
 
@@ -557,6 +558,21 @@ lattice_status lattice_net_tower_backward(lattice_net* net, int64_t batch, const
  * gradients first: every replica then applies the same update and stays bit-identical. */
 lattice_status lattice_net_tower_sgd(lattice_net* net, float lr, const float* dW1, const float* dW2, float* master_W1,
                                      float* master_W2, lattice_stream stream);
+/* Backward through the LAST DWFB block's FMB half (its MLP and the residual
+ * rms_norm_d), after a forward of `batch` samples: from dXout fp32 [batch][n*d] (d loss / d X_L,
+ * domain-sorted rows, e.g. lattice_net_tower_backward's dX; columns [0, nF*d) are used) ->
+ * dW[i] fp32 [mlp[i+1]][mlp[i]] for every MLP layer i < n_mlp; optionally dFin fp32
+ * [batch][n*k] (the MLP input; buffer 3 holds the forward's Fin) and dResid fp32 [batch][nF*d]
+ * (the residual branch's gradient to the block input rows [0, nF)). The MLP's hidden outputs are
+ * the forward's own (re-run bit-identically for n_mlp > 3); pre-activations are recomputed by
+ * fp32 GEMMs; gradients of z are rounded to bf16 as the tcgen05 GEMMs' operands. bf16 networks;
+ * deterministic. The FM / LCB interaction (P, W_L, Y) and earlier blocks are not differentiated. */
+lattice_status lattice_net_mlp_backward(lattice_net* net, int64_t batch, const float* dXout, float* const* dW,
+                                        float* dFin, float* dResid, lattice_stream stream);
+/* Plain SGD on one unpadded weight (kind 3..7, block / index as lattice_net_weight): fp32 master
+ * -= lr * grad, the network's copy refreshed in its dtype (kind 5: fp32). */
+lattice_status lattice_net_weight_sgd(lattice_net* net, int32_t block, int32_t kind, int32_t index, float lr,
+                                      const float* grad, float* master, lattice_stream stream);
 
 /* Per-stage CUDA-event times (ms) of the last forward when timing was enabled. */
 lattice_status lattice_net_set_timing(lattice_net* net, int32_t enable);

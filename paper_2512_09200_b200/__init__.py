@@ -171,6 +171,8 @@ _sig("lattice_rownorm_vjp", ctypes.c_int, [_I32, _I64, _I64, ctypes.c_double, _I
 _sig("lattice_routed_bce", ctypes.c_int, [_I64, _I32, _I32, _P, _P, _P, _P, _P, _P])
 _sig("lattice_net_tower_backward", ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _I32, _P])
 _sig("lattice_net_tower_sgd", ctypes.c_int, [_P, ctypes.c_float, _P, _P, _P, _P, _P])
+_sig("lattice_net_mlp_backward", ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _P])
+_sig("lattice_net_weight_sgd", ctypes.c_int, [_P, _I32, _I32, _I32, ctypes.c_float, _P, _P, _P])
 _sig("lattice_net_create", ctypes.c_int, [ctypes.POINTER(NetConfig), ctypes.POINTER(_P)])
 _sig("lattice_net_destroy", None, [_P])
 _sig("lattice_net_weight", _P, [_P, _I32, _I32, _I32])
@@ -203,7 +205,8 @@ EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_versio
            "lattice_jsonl_open", "lattice_jsonl_extract", "lattice_jsonl_task_columns",
            "lattice_jsonl_close", "lattice_net_set_weight", "lattice_fm_lcb",
            "lattice_rownorm_f64", "lattice_device_check", "lattice_rownorm_vjp", "lattice_routed_bce",
-           "lattice_net_tower_backward", "lattice_net_tower_sgd"]
+           "lattice_net_tower_backward", "lattice_net_tower_sgd", "lattice_net_mlp_backward",
+           "lattice_net_weight_sgd"]
 
 lib = _lib
 
@@ -794,7 +797,7 @@ class Network:
 
     def buffer(self, which):
         """Device pointer of a workspace buffer (lattice_net_buffer): 0 = X0 / even blocks'
-        input, 1 = sample_pos, 2 = odd blocks' input."""
+        input, 1 = sample_pos, 2 = odd blocks' input, 3 = the last block's MLP input Fin."""
         p = _lib.lattice_net_buffer(self._h, which)
         if not p:
             raise UsageError(f"lattice_net_buffer: unknown buffer {which}")
@@ -851,6 +854,39 @@ class Network:
         """master -= lr * grad and the network's tower weights refreshed (lattice_net_tower_sgd)."""
         check(_lib.lattice_net_tower_sgd(self._h, lr, _p(dW1), _p(dW2), _p(master_W1), _p(master_W2),
                                          _stream(stream)))
+
+    def mlp_backward(self, dXout, dW=None, dFin=False, dResid=False, stream=None):
+        """Gradients of the last block's FMB half (lattice_net_mlp_backward) from dXout fp32
+        [B, n*d] (d loss / d X_L, domain-sorted rows): returns (dW list of fp32 [out, in] per MLP
+        layer, dFin [B, n*k] or None, dResid [B, nF*d] or None)."""
+        import torch
+        c = self.cfg
+        B = dXout.shape[0]
+        widths = c["mlp"]
+        dev = dXout.device
+        if dW is None:
+            dW = [torch.empty((widths[i + 1], widths[i]), dtype=torch.float32, device=dev)
+                  for i in range(len(widths) - 1)]
+        fin = torch.empty((B, widths[0]), dtype=torch.float32, device=dev) if dFin else None
+        res = torch.empty((B, c["nF"] * c["d"]), dtype=torch.float32, device=dev) if dResid else None
+        ptrs = (ctypes.c_void_p * len(dW))(*[t.data_ptr() for t in dW])
+        check(_lib.lattice_net_mlp_backward(self._h, B, _p(dXout.contiguous()), ptrs, _p(fin), _p(res),
+                                            _stream(stream)))
+        return dW, fin, res
+
+    def weight_sgd(self, block, kind, index, lr, grad, master, stream=None):
+        """master -= lr * grad on one weight, the network's copy refreshed (lattice_net_weight_sgd)."""
+        check(_lib.lattice_net_weight_sgd(self._h, block, kind, index, lr, _p(grad), _p(master), _stream(stream)))
+
+    def mlp_masters(self, block=None):
+        """fp32 device copies of one block's MLP weights [out, in] (default: the last block)."""
+        c = self.cfg
+        import torch
+        blk = c["blocks"] - 1 if block is None else block
+        wdt = torch.float32 if c["dtype"] in ("f32", "fp32", "float32") else torch.bfloat16
+        w = c["mlp"]
+        return [_view(_lib.lattice_net_weight(self._h, blk, 3, i), (w[i + 1], w[i]), wdt).float().clone()
+                for i in range(len(w) - 1)]
 
     def tower_masters(self):
         """fp32 device copies of the towers' W1 [G, th, n*d] and W2 [G, heads, th] (SGD masters)."""

@@ -12,6 +12,12 @@
 //                                dz = J_swish(z)^T (W2_g^T dlogit)     (stored bf16, the GEMM operand)
 //                                dW1_g = dz_g^T X_g   (tcgen05 GEMM, both operands MN-major in place)
 //                                dX    = dz W1_g      (tcgen05 GEMM, W1_g MN-major in place)
+//   lattice_net_mlp_backward   gradients of the last DWFB block's FMB half: its
+//                              MLP weights, the MLP input Fin and the residual branch, from
+//                              d(loss)/d(X_L) (e.g. the towers' dX):
+//                                U = z_last + X[:nF];  dz_last = J_rmsnorm_d(U)^T dX_L[:nF]
+//                                per layer i (last to first): dW_i = dz_i^T a_i;  da_i = dz_i W_i
+//                                dz_{i-1} = J_swish(z_{i-1})^T da_i  (z recomputed by fp32 GEMMs)
 // Every reduction runs in a fixed order (per-chunk partials, then a fixed-order sum): gradients are
 // deterministic, so data-parallel replicas that all-reduce them stay bit-identical.
 #include <cuda_bf16.h>
@@ -53,9 +59,15 @@ __device__ __forceinline__ T act_grad(int mode, T r) {
 }
 
 // warp per row: J^T g = u/d - x (x . u) / (n d^3), u_i = act'(r_i) g_i, r = x/d, d = sqrt(mean(x^2)+eps)
-template <typename T>
+template <typename TO, typename T>
+__device__ __forceinline__ TO store_as(T v) {
+    if constexpr (sizeof(TO) == 2) return __float2bfloat16_rn((float)v);
+    else return (TO)v;
+}
+
+template <typename T, typename TO = T>
 __global__ void rownorm_vjp_kernel(int mode, int64_t rows, int64_t width, T eps, const T* __restrict__ x,
-                                   const T* __restrict__ g, T* __restrict__ out) {
+                                   const T* __restrict__ g, TO* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
          r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -71,7 +83,7 @@ __global__ void rownorm_vjp_kernel(int mode, int64_t rows, int64_t width, T eps,
         for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
         const T k = dot / (n * d * d * d);
         for (int64_t c = lane; c < width; c += 32)
-            out[r * width + c] = act_grad<T>(mode, xr[c] / d) * gr[c] / d - xr[c] * k;
+            out[r * width + c] = store_as<TO>(act_grad<T>(mode, xr[c] / d) * gr[c] / d - xr[c] * k);
     }
 }
 
@@ -148,6 +160,44 @@ __global__ void tower_dz_kernel(int64_t B, int th, int heads, int hard, const fl
     }
 }
 
+// Residual rms_norm_d of the FMB half: warp per (sample, row f < nF) of d <= 128 values,
+// U = z_last + X_in, g = dX_out (row stride nd); dU = g/s - U (U . g) / (d s^3), s = sqrt(mean(U^2)+eps)
+// -> bf16 (the MLP backward's GEMM operand) and optionally fp32 (the residual branch's gradient)
+__global__ void resid_vjp_kernel(int64_t B, int nF, int d, int64_t nd, const float* __restrict__ z,
+                                 const __nv_bfloat16* __restrict__ Xin, const float* __restrict__ dXout,
+                                 __nv_bfloat16* __restrict__ dz, float* __restrict__ dResid) {
+    const int lane = threadIdx.x & 31;
+    const int64_t rows = B * nF, w = (int64_t)nF * d;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t b = r / nF, f = r - b * nF;
+        const float* zr = z + b * w + f * d;
+        const __nv_bfloat16* xr = Xin + b * nd + f * d;
+        const float* gr = dXout + b * nd + f * d;
+        float u[4], gv[4], ss = 0.0f, dot = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = lane + 32 * i;
+            u[i] = c < d ? zr[c] + __bfloat162float(xr[c]) : 0.0f;
+            gv[i] = c < d ? gr[c] : 0.0f;
+            ss += u[i] * u[i];
+            dot += u[i] * gv[i];
+        }
+        ss = warp_sum(ss);
+        dot = warp_sum(dot);
+        const float s = sqrtf(ss / (float)d + 1e-6f);
+        const float k = dot / ((float)d * s * s * s);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = lane + 32 * i;
+            if (c >= d) continue;
+            const float o = gv[i] / s - u[i] * k;
+            dz[b * w + f * d + c] = __float2bfloat16_rn(o);
+            if (dResid) dResid[b * w + f * d + c] = o;
+        }
+    }
+}
+
 // dW2_g[k][j] = sum_{m in segment g} dlogit[order[m]][k] h[m][j]: thread per (g, j), rows in
 // chunks of `chunk` (partials [G][chunks][heads][th]), then a fixed-order sum over chunks
 __global__ void dw2_partial_kernel(int th, int heads, int G, int chunk, int chunks, const int32_t* __restrict__ seg,
@@ -195,6 +245,28 @@ unsigned grid_for_rows(int64_t rows) {
     return (unsigned)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
+// C [M][N] = op(A) op(B)^T over K (fp32 accumulate, plain store); a_mn / b_mn: the operand is
+// stored [K][M] / [K][N] (read in place as an MN-major tcgen05 operand)
+lattice_status gemm_store(const void* A, int64_t lda, int64_t M, int a_mn, const void* Bm, int64_t ldb, int64_t N,
+                          int b_mn, int64_t K, void* C, int64_t ldc, int out_bf16, cudaStream_t st) {
+    gemm::Params p = {};
+    p.M = (int)M;
+    p.N = (int)N;
+    p.K = (int)K;
+    p.C = C;
+    p.ldc = ldc;
+    p.out_bf16 = out_bf16;
+    p.epi = gemm::kStore;
+    p.N_full = (int)N;
+    p.cluster = 1;
+    p.a_mn = a_mn;
+    p.b_mn = b_mn;
+    gemm::GemmPlan gp;
+    lattice_status s = gemm::plan(&gp, A, lda, M, Bm, ldb, N, p, (int)((M + 127) / 128), false);
+    if (s != LATTICE_OK) return s;
+    return gemm::launch(gp, st);
+}
+
 }  // namespace
 
 lattice_status sgd_update(int64_t n, float lr, const float* grad, float* master, void* work, bool work_bf16,
@@ -238,30 +310,11 @@ lattice_status tower_backward(const TowerBwd& a, cudaStream_t st) {
     auto run = [&]() -> lattice_status {
         const __nv_bfloat16* X = static_cast<const __nv_bfloat16*>(a.X);
         const __nv_bfloat16* W1 = static_cast<const __nv_bfloat16*>(a.W1);
-        auto gemm_store = [&](const void* A, int64_t lda, int64_t M, int a_mn, const void* Bm, int64_t ldb, int64_t N,
-                              int b_mn, int64_t K, void* C, int64_t ldc, int out_bf16) -> lattice_status {
-            gemm::Params p = {};
-            p.M = (int)M;
-            p.N = (int)N;
-            p.K = (int)K;
-            p.C = C;
-            p.ldc = ldc;
-            p.out_bf16 = out_bf16;
-            p.epi = gemm::kStore;
-            p.N_full = (int)N;
-            p.cluster = 1;
-            p.a_mn = a_mn;
-            p.b_mn = b_mn;
-            gemm::GemmPlan gp;
-            lattice_status s = gemm::plan(&gp, A, lda, M, Bm, ldb, N, p, (int)((M + 127) / 128), false);
-            if (s != LATTICE_OK) return s;
-            return gemm::launch(gp, st);
-        };
         for (int g = 0; g < G; ++g) {  // z = X_g W1_g^T (fp32): the pre-activation the forward did not keep
             const int64_t rows = seg[g + 1] - seg[g];
             if (rows == 0) continue;
             lattice_status s = gemm_store(X + (int64_t)seg[g] * nd, nd, rows, 0, W1 + (int64_t)g * th * nd, nd, th, 0,
-                                          nd, z + (int64_t)seg[g] * th, th, 0);
+                                          nd, z + (int64_t)seg[g] * th, th, 0, st);
             if (s != LATTICE_OK) return s;
         }
         tower_dz_kernel<<<grid_for_rows(B), 256, 0, st>>>(B, th, heads, a.hard, z, a.order, a.seg, G, a.dlogits, a.W2,
@@ -281,15 +334,66 @@ lattice_status tower_backward(const TowerBwd& a, cudaStream_t st) {
             }
             // dW1_g [th][nd] = dz_g^T X_g: both operands stored with the batch rows as K (MN-major)
             lattice_status s = gemm_store(dz + (int64_t)seg[g] * th, th, th, 1, X + (int64_t)seg[g] * nd, nd, nd, 1,
-                                          rows, dW1g, nd, 0);
+                                          rows, dW1g, nd, 0, st);
             if (s != LATTICE_OK) return s;
             if (a.dX) {  // dX_g [rows][nd] = dz_g W1_g: W1_g stored [th][nd] is the MN-major B operand
                 void* C = a.dx_bf16 ? (void*)(static_cast<__nv_bfloat16*>(a.dX) + (int64_t)seg[g] * nd)
                                     : (void*)(static_cast<float*>(a.dX) + (int64_t)seg[g] * nd);
                 s = gemm_store(dz + (int64_t)seg[g] * th, th, rows, 0, W1 + (int64_t)g * th * nd, nd, nd, 1, th, C, nd,
-                               a.dx_bf16);
+                               a.dx_bf16, st);
                 if (s != LATTICE_OK) return s;
             }
+        }
+        return LATTICE_OK;
+    };
+    const lattice_status s = run();
+    cudaFreeAsync(ws, st);
+    return s;
+}
+
+// The FMB half's backward (see the file header); called by lattice_net_mlp_backward (network.cu).
+lattice_status mlp_backward(const MlpBwd& a, cudaStream_t st) {
+    nvtxRangePushA("lattice::mlp_backward");
+    struct Pop {
+        ~Pop() { nvtxRangePop(); }
+    } pop;
+    const int64_t B = a.B;
+    const int L = a.n_mlp;
+    int64_t wmax = 0;
+    for (int i = 1; i <= L; ++i) wmax = a.widths[i] > wmax ? a.widths[i] : wmax;
+    const size_t fb = sizeof(float) * (size_t)B * wmax, hb = sizeof(__nv_bfloat16) * (size_t)B * wmax;
+    uint8_t* ws = nullptr;
+    LAT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), 2 * fb + hb, st));
+    float* z = reinterpret_cast<float*>(ws);           // a pre-activation [B][w] (recomputed)
+    float* da = reinterpret_cast<float*>(ws + fb);     // d(loss)/d(a_i) [B][w_i]
+    __nv_bfloat16* dz = reinterpret_cast<__nv_bfloat16*>(ws + 2 * fb);  // d(loss)/d(z_i), bf16
+    auto run = [&]() -> lattice_status {
+        const int64_t wl = a.widths[L];  // nF * d
+        // z_last = a_{L-1} W_{L-1}^T; dz_last = J_rmsnorm_d(z_last + X[:nF])^T dX_L[:nF]
+        lattice_status s = gemm_store(a.act[L - 1], a.widths[L - 1], B, 0, a.W[L - 1], a.widths[L - 1], wl, 0,
+                                      a.widths[L - 1], z, wl, 0, st);
+        if (s != LATTICE_OK) return s;
+        resid_vjp_kernel<<<grid_for_rows(B * a.nF), 256, 0, st>>>(B, a.nF, a.d, a.nd, z,
+                                                                   static_cast<const __nv_bfloat16*>(a.Xin), a.dXout,
+                                                                   dz, a.dResid);
+        LAT_CUDA(cudaGetLastError());
+        for (int i = L - 1; i >= 0; --i) {
+            const int64_t in = a.widths[i], out = a.widths[i + 1];
+            // dW_i [out][in] = dz_i^T a_i: both stored with the batch rows as K (MN-major)
+            s = gemm_store(dz, out, out, 1, a.act[i], in, in, 1, B, a.dW[i], in, 0, st);
+            if (s != LATTICE_OK) return s;
+            if (i == 0 && !a.dFin) break;
+            // da_i [B][in] = dz_i W_i: W_i stored [out][in] is the MN-major B operand
+            s = gemm_store(dz, out, B, 0, a.W[i], in, in, 1, out, i == 0 ? a.dFin : da, in, 0, st);
+            if (s != LATTICE_OK) return s;
+            if (i == 0) break;
+            // z_{i-1} = a_{i-1} W_{i-1}^T (fp32), dz_{i-1} = J_act(z_{i-1})^T da_i -> bf16
+            const int64_t pin = a.widths[i - 1];
+            s = gemm_store(a.act[i - 1], pin, B, 0, a.W[i - 1], pin, in, 0, pin, z, in, 0, st);
+            if (s != LATTICE_OK) return s;
+            rownorm_vjp_kernel<float, __nv_bfloat16><<<grid_for_rows(B), 256, 0, st>>>(a.hard ? 2 : 1, B, in, 1e-6f,
+                                                                                       z, da, dz);
+            LAT_CUDA(cudaGetLastError());
         }
         return LATTICE_OK;
     };

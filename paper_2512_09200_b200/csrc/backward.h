@@ -25,6 +25,23 @@ struct TowerBwd {
 };
 
 lattice_status tower_backward(const TowerBwd& a, cudaStream_t st);
+
+struct MlpBwd {
+    int64_t B;                 // batch rows (domain-sorted)
+    int n_mlp;
+    int widths[6];             // mlp[0..n_mlp]: n*k, hidden..., nF*d
+    int nF, d, hard;
+    int64_t nd;                // n * d: row stride of X_in / dXout
+    const void* act[5];        // bf16 [B][widths[i]]: layer i's input (act[0] = Fin)
+    const void* W[5];          // bf16 [widths[i+1]][widths[i]]
+    const void* Xin;           // bf16 [B][nd]: the block's input (the residual)
+    const float* dXout;        // [B][nd]: d(loss)/d(block output), columns [0, nF*d) used
+    float* dW[5];              // out [widths[i+1]][widths[i]]
+    float* dFin;               // optional out [B][widths[0]]
+    float* dResid;             // optional out [B][nF*d]
+};
+
+lattice_status mlp_backward(const MlpBwd& a, cudaStream_t st);
 // master -= lr * grad (n fp32 values); work (the network's copy) refreshed in bf16 or fp32
 lattice_status sgd_update(int64_t n, float lr, const float* grad, float* master, void* work, bool work_bf16,
                           cudaStream_t st);

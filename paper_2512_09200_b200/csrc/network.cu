@@ -618,6 +618,86 @@ lattice_status lattice_net_tower_sgd(lattice_net* net, float lr, const float* dW
     return sgd_update(n2, lr, dW2, master_W2, net->T2, false, st);
 }
 
+lattice_status lattice_net_mlp_backward(lattice_net* net, int64_t batch, const float* dXout, float* const* dW,
+                                        float* dFin, float* dResid, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(net != nullptr && dXout != nullptr && dW != nullptr, "lattice_net_mlp_backward: null argument");
+    const lattice_net_config& c = net->cfg;
+    LAT_REQUIRE(!net->f32, "lattice_net_mlp_backward: needs a bf16 network");
+    LAT_REQUIRE(batch > 0 && batch <= c.max_batch, "lattice_net_mlp_backward: bad batch");
+    for (int i = 0; i < c.n_mlp; ++i) LAT_REQUIRE(dW[i] != nullptr, "lattice_net_mlp_backward: null dW");
+    const cudaStream_t st = (cudaStream_t)stream;
+    const int blk = c.blocks - 1;
+    MlpBwd a = {};
+    a.B = batch;
+    a.n_mlp = c.n_mlp;
+    for (int i = 0; i <= c.n_mlp; ++i) a.widths[i] = c.mlp[i];
+    a.nF = c.nF;
+    a.d = c.d;
+    a.hard = c.hard;
+    a.nd = (int64_t)c.n * c.d;
+    a.Xin = net->X[blk & 1];
+    a.dXout = dXout;
+    a.dFin = dFin;
+    a.dResid = dResid;
+    a.act[0] = net->Fbuf;
+    for (int i = 0; i < c.n_mlp; ++i) {
+        a.W[i] = net->mlp[(size_t)blk * c.n_mlp + i];
+        a.dW[i] = dW[i];
+    }
+    // hidden outputs: layer i writes H[i & 1], so after the forward the last two survive; deeper MLPs
+    // re-run the forward's own GEMMs (deterministic: bit-identical) and keep a copy of each output
+    std::vector<void*> copies;
+    if (c.n_mlp <= 3) {
+        for (int i = 1; i < c.n_mlp; ++i) a.act[i] = net->H[(i - 1) & 1];
+    } else {
+        LAT_CUDA(cudaMemsetAsync(net->rowcnt + (size_t)blk * (c.n_mlp - 1) * net->rowcnt_stride, 0,
+                                 sizeof(int) * (size_t)(c.n_mlp - 1) * net->rowcnt_stride, st));
+        for (int i = 0; i + 1 < c.n_mlp; ++i) {
+            gemm::GemmPlan g = net->mlp_plans[(size_t)blk * c.n_mlp + i];
+            g.p.M = (int)batch;
+            g.grid_y = (int)((batch + 127) / 128);
+            lattice_status s = gemm::launch(g, st);
+            void* h = nullptr;
+            const size_t bytes = sizeof(__nv_bfloat16) * (size_t)batch * c.mlp[i + 1];
+            if (s == LATTICE_OK) {
+                cudaError_t e = cudaMallocAsync(&h, bytes, st);
+                if (e == cudaSuccess) e = cudaMemcpyAsync(h, net->H[i & 1], bytes, cudaMemcpyDeviceToDevice, st);
+                if (h) copies.push_back(h);
+                if (e != cudaSuccess) s = check_cuda(e, "mlp_backward: hidden copy");
+            }
+            if (s != LATTICE_OK) {
+                for (void* q : copies) cudaFreeAsync(q, st);
+                return s;
+            }
+            a.act[i + 1] = h;
+        }
+    }
+    const lattice_status s = mlp_backward(a, st);
+    for (void* q : copies) cudaFreeAsync(q, st);
+    return s;
+}
+
+lattice_status lattice_net_weight_sgd(lattice_net* net, int32_t block, int32_t kind, int32_t index, float lr,
+                                      const float* grad, float* master, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(net && grad && master, "lattice_net_weight_sgd: null argument");
+    LAT_REQUIRE(kind >= 3 && kind <= 7, "lattice_net_weight_sgd: kind must be 3..7 (unpadded weights)");
+    void* w = const_cast<void*>(lattice_net_weight(net, block, kind, index));
+    LAT_REQUIRE(w != nullptr, "lattice_net_weight_sgd: no such weight (block / kind / index)");
+    const lattice_net_config& c = net->cfg;
+    int64_t n = 0;
+    switch (kind) {
+        case 3: n = (int64_t)c.mlp[index + 1] * c.mlp[index]; break;
+        case 4: n = (int64_t)c.domains * c.tower_hidden * c.n * c.d; break;
+        case 5: n = (int64_t)c.domains * c.heads * c.tower_hidden; break;
+        case 6: n = (int64_t)c.dense_hidden * c.dense_in; break;
+        default: n = (int64_t)c.dense_features * c.d * c.dense_hidden; break;
+    }
+    LAT_REQUIRE(n > 0, "lattice_net_weight_sgd: the network has no such weight");
+    return sgd_update(n, lr, grad, master, w, kind != 5 && !net->f32, (cudaStream_t)stream);
+}
+
 lattice_status lattice_net_set_timing(lattice_net* net, int32_t enable) {
     LAT_REQUIRE(net != nullptr, "lattice_net_set_timing: null net");
     net->timing = enable != 0;
@@ -663,6 +743,7 @@ void* lattice_net_buffer(lattice_net* net, int32_t which) {
         case 0: return net->X[0];
         case 1: return net->pos;
         case 2: return net->X[1];
+        case 3: return net->Fbuf;
         default: return nullptr;
     }
 }

@@ -1,7 +1,8 @@
-"""Data-parallel tower training on >= 2 GPUs (torchrun, NCCL): every rank forwards its own batch
-through an identically initialised network, TowerTrainer all-reduces the tower gradients (one NCCL
-collective on the flat bucket) and applies the same SGD update. Checks, printed by rank 0: the
-replicas' tower weights stay bit-identical after every step, and the mean routed loss falls."""
+"""Data-parallel training on >= 2 GPUs (torchrun, NCCL) of the towers and the last block's MLP:
+every rank forwards its own batch through an identically initialised network, TowerTrainer
+(train_mlp=True) all-reduces every gradient (one NCCL collective on the flat bucket) and applies
+the same SGD update. Checks, printed by rank 0: the replicas' tower and MLP weights stay
+bit-identical after every step, and the mean routed loss falls."""
 import os
 import sys
 
@@ -28,18 +29,20 @@ def main():
     dom = L.synth_domains(B, cfg["domains"], 0x1A78 + rank)
     imp = L.synth_impressions(B, 4, 7 + rank)
     win, lab, _ = L.zipper_assign_labels(*imp, [5400000, 86400000, 604800000], [1 / 3] * 3, 7)
-    tr = TowerTrainer(net, lr=2.0)
+    tr = TowerTrainer(net, lr=2.0, train_mlp=True)
     identical, losses = True, []
     for _ in range(4):
         logits = net.forward(dom, offsets, ids, ptrs, rws, torch.bfloat16)
         losses.append(float(tr.step(logits, win, lab, 4, 3)))
         W1, W2 = net.tower_masters()
-        cs = torch.stack([W1.double().sum(), W2.double().sum(), (W1.double() ** 2).sum()])
+        M = net.mlp_masters()
+        cs = torch.stack([W1.double().sum(), W2.double().sum(), (W1.double() ** 2).sum()] +
+                         [m.double().sum() for m in M] + [(m.double() ** 2).sum() for m in M])
         allcs = [torch.zeros_like(cs) for _ in range(world)]
         dist.all_gather(allcs, cs)
         identical = identical and all(torch.equal(c, allcs[0]) for c in allcs)
     if rank == 0:
-        print(f"dp tower training over {world} GPUs: losses {losses}")
+        print(f"dp tower + last-block MLP training over {world} GPUs: losses {losses}")
         print(f"replicas bit-identical after every step: {identical}")
         print(f"loss falls: {losses[-1] < 0.95 * losses[0]}")
     dist.destroy_process_group()

@@ -159,3 +159,83 @@ def test_tower_training_lowers_routed_loss():
         assert torch.equal(W1, tr.W1.bfloat16().float())  # the net runs the bf16 rounding of the master
     record("tower training: routed BCE per step", {"losses": losses})
     assert losses[-1] < losses[0] * 0.95, losses
+
+
+def mlp_backward_ref(cfg, w, Fin, Xin, dXout, acc, hard=False):
+    """Autograd of <rms_norm_d(z_last + X[:nF]), dX_L[:nF]> through the last block's MLP in `acc`
+    arithmetic, from the GPU's own Fin and X_{L-1} (domain-sorted rows): the hidden activations
+    q()-rounded as the forward stores them, every layer's d(loss)/dz rounded to bf16 by a hook
+    (the GPU's GEMM-operand rounding). Returns ([dW_i], dFin, dResid)."""
+    import torch
+    n, d, nF = cfg["n"], cfg["d"], cfg["nF"]
+    n_mlp = len(cfg["mlp"]) - 1
+    blk = cfg["blocks"] - 1
+    S = Fin.shape[0]
+    with torch_ref.accumulate(acc):
+        a = Fin.to(acc).detach().requires_grad_(True)
+        Ws = [torch_ref._t(w["mlp"][blk * n_mlp + i], Fin.device).requires_grad_(True) for i in range(n_mlp)]
+        h = a
+        for i in range(n_mlp):
+            z = h @ Ws[i].T
+            z.register_hook(lambda g: g.float().bfloat16().to(g.dtype))
+            if i + 1 < n_mlp:  # straight-through q(): autograd through .bfloat16() would round the
+                h = torch_ref.act(z, hard)  # gradient to bf16 too, which the GPU does not
+                h = h + (torch_ref.q(h, True) - h).detach()
+        Xr = Xin.to(acc).reshape(S, n, d)[:, :nF].detach().requires_grad_(True)
+        out = torch_ref.rms_norm(z.reshape(S, nF, d) + Xr)
+        loss = (out * dXout.to(acc).reshape(S, n, d)[:, :nF]).sum()
+        grads = torch.autograd.grad(loss, Ws + [a, Xr])
+    return list(grads[:n_mlp]), grads[n_mlp], grads[n_mlp + 1].reshape(S, nF * d)
+
+
+@pytest.mark.parametrize("mlp,hard", [([1024, 512, 4096], False), ([1024, 384, 256, 512, 4096], True)])
+def test_mlp_backward_matches_restatement(mlp, hard):
+    """lattice_net_mlp_backward against autograd of the torch restatement (fp64; calibrated by the
+    same in fp32). The 4-layer MLP takes the re-run path (its first hidden output is overwritten by
+    the forward's ping-pong)."""
+    import torch
+    import paper_2512_09200_b200 as L
+    cfg = dict(SMALL, mlp=mlp)
+    B, rows = 1000, 3000
+    net, tab, ptrs, rws, offsets, ids, dom = build(cfg, B, rows, hard=hard)
+    net.forward(dom, offsets, ids, ptrs, rws, torch.bfloat16)
+    n, d, k, nb = cfg["n"], cfg["d"], cfg["k"], cfg["blocks"]
+    Fin = L._view(net.buffer(3), (B, n * k), torch.bfloat16).clone()
+    Xin = L._view(net.buffer(2 if (nb - 1) & 1 else 0), (B, n * d), torch.bfloat16).clone()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    dXout = torch.randn((B, n * d), generator=g, device="cuda") / B
+    dW, dFin, dRes = net.mlp_backward(dXout, dFin=True, dResid=True)
+    # the forward's buffers are untouched by the backward (the re-run is bit-identical)
+    assert torch.equal(L._view(net.buffer(3), (B, n * k), torch.bfloat16), Fin)
+    w = net.weights()
+    r64 = mlp_backward_ref(cfg, w, Fin, Xin, dXout, torch.float64, hard)
+    r32 = mlp_backward_ref(cfg, w, Fin, Xin, dXout, torch.float32, hard)
+    pairs = [(f"dW{i}", dW[i], r64[0][i], r32[0][i]) for i in range(len(dW))]
+    pairs += [("dFin", dFin, r64[1], r32[1]), ("dResid", dRes, r64[2], r32[2])]
+    for name, got, a, b in pairs:
+        scale = float(a.abs().max())
+        calibrated(f"mlp backward ({len(mlp) - 1} layers, hard={hard}) {name}", got, a, b, atol=1e-3 * scale,
+                   rtol=1e-3, mean_floor=1e-5 * scale)
+    # deterministic
+    dW2, _, _ = net.mlp_backward(dXout)
+    assert all(torch.equal(x, y) for x, y in zip(dW, dW2))
+
+
+def test_tower_and_mlp_training_lowers_routed_loss():
+    import torch
+    import paper_2512_09200_b200 as L
+    from paper_2512_09200_b200.train import TowerTrainer
+    cfg = dict(SMALL, heads=12)
+    B, rows = 2048, 3000
+    net, tab, ptrs, rws, offsets, ids, dom = build(cfg, B, rows)
+    imp = L.synth_impressions(B, 4, 7)
+    win, lab, _ = L.zipper_assign_labels(*imp, [5400000, 86400000, 604800000], [1 / 3] * 3, 7)
+    tr = TowerTrainer(net, lr=2.0, train_mlp=True)
+    losses = []
+    for _ in range(6):
+        logits = net.forward(dom, offsets, ids, ptrs, rws, torch.bfloat16)
+        losses.append(float(tr.step(logits, win, lab, 4, 3)))
+        for i, m in enumerate(net.mlp_masters()):
+            assert torch.equal(m, tr.mlp[i].bfloat16().float())
+    record("tower + last-block MLP training: routed BCE per step", {"losses": losses})
+    assert losses[-1] < losses[0] * 0.95, losses
