@@ -84,3 +84,13 @@ def test_bucket_rownorm_jsonl_contracts():
           "< 2 GiB")
     usage(L.lib.lattice_jsonl_open(p, 10, b"x", None, ctypes.byref(info), None), "null argument")
     usage(L.lib.lattice_jsonl_task_columns(-1, p, p, p, p, 1, p, p, p, p, None), "bad sizes")
+
+
+def test_backward_contracts():
+    p = ctypes.c_void_p(16)
+    usage(L.lib.lattice_rownorm_vjp(3, 4, 8, 1e-6, L.F32, p, p, p, None), "mode must be 0, 1 or 2")
+    usage(L.lib.lattice_rownorm_vjp(1, 4, 8, 1e-6, L.BF16, p, p, p, None), "dtype must be f32 or f64")
+    usage(L.lib.lattice_routed_bce(4, 0, 3, p, p, p, p, p, None), "routed_bce: bad sizes")
+    usage(L.lib.lattice_net_tower_backward(None, 4, p, p, p, None, L.F32, None), "null argument")
+    usage(L.lib.lattice_net_mlp_backward(None, 4, p, p, None, None, None), "null argument")
+    usage(L.lib.lattice_net_weight_sgd(None, 0, 3, 0, 0.1, p, p, None), "null argument")
