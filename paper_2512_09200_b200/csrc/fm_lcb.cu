@@ -709,7 +709,10 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
         const float inv_d = 1.0f / (float)d;
         const int i = mt * 128 + row;
         const bool live = mt < g.ml && i < p.nL;
-        const int xr = p.nF + i;
+        // tcgen05.ld is warp-collective: a warp with any live lane runs the whole epilogue, its
+        // dead lanes on a valid residual row with their stores and arrivals masked
+        const bool warp_live = mt < g.ml && mt * 128 + q * 32 < p.nL;
+        const int xr = p.nF + (live ? i : 0);
         const int cx = xr >> 7;  // the X chunk holding the residual row
         const uint32_t t_L = t_Lb + lane_off + mt * 128;
         int it = 0;
@@ -729,7 +732,7 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
                 tc::fence_async_shared();
                 tc::mbar_arrive(pbuf_full);
             }
-            if (live) {  // X'[nF+i] = rms_norm_d(L[i] + X[nF+i]): sum of squares, then normalise + store;
+            if (warp_live) {  // X'[nF+i] = rms_norm_d(L[i] + X[nF+i]): sum of squares, then normalise + store;
                          // the residual row is read from the X chunk in shared memory, which this
                          // thread releases afterwards (the next sample's chunk loads behind it)
                 float ss4[4] = {0.f, 0.f, 0.f, 0.f};
@@ -768,9 +771,10 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
                             o[4 * hh + k] = pack_bf16x2((v[8 * hh + 2 * k] + bf16_lo(w[k])) * inv,
                                                         (v[8 * hh + 2 * k + 1] + bf16_hi(w[k])) * inv);
                     }
-                    st_global_256(dst + c, make_uint4(o[0], o[1], o[2], o[3]), make_uint4(o[4], o[5], o[6], o[7]));
+                    if (live)
+                        st_global_256(dst + c, make_uint4(o[0], o[1], o[2], o[3]), make_uint4(o[4], o[5], o[6], o[7]));
                 }
-                tc::mbar_arrive(&x_empty[cx]);
+                if (live) tc::mbar_arrive(&x_empty[cx]);
             }
             tc::fence_before();
             tc::mbar_arrive(mt == 0 ? l_empty : l1_empty);
@@ -841,6 +845,380 @@ size_t smem_bytes_large(const Params& p) {
 
 bool is_large(const Params& p) { return p.n_pad > 256; }
 
+// ---------------------------------------------------------------------------------------------
+// CTA-pair variant of the large kernel (n_pad = 512, bf16, d = 128, k_pad 16 or 32, nF and nL
+// multiples of 32): a cluster of two CTAs on one TPC takes two samples per pass, CTA r holding
+// sample 2s + r in its shared memory, and every MMA is a cta_group::2 MMA issued by the leader:
+//   P  (M = 256: each CTA's X^T rows) x Y      -> each CTA's TMEM holds its own sample's P;
+//                                                 CTA r keeps Y^T rows [r k/2, +k/2) resident
+//   L  (M = 256: CTA r's W_L rows [128r, +128)) x [X_a | X_b] (N = 256: each CTA's X)
+//                                              -> CTA r holds L rows [128r, +128) of both samples
+//   F  (M = 256: each CTA's X rows) x [P_a | P_b] (N = 2k) -> CTA r reads its own sample's columns
+// so W_L streams once per PAIR of samples and each SM stages half of it: shared-memory operand
+// traffic per sample drops by about a third against the single-CTA kernel, which is bound by it.
+// The LCB epilogue reads its own sample's residual rows from shared memory and the partner's
+// from global memory (L2-resident: the partner's TMA load just brought them in).
+// Measured (scripts/fm_bench.py, B = 65536): 4.49 ms against the single-CTA kernel's 3.48 ms, so
+// it is opt-in (LATTICE_FM_PAIR=1): L (256 columns) and F (256, P aliased) fill TMEM, so L cannot
+// be double-buffered and each pass's LCB epilogue (the partner half waiting on L2) sits between
+// this pass's and the next pass's L MMAs; the single-CTA kernel overlaps them across its two
+// L M-tiles.
+// ---------------------------------------------------------------------------------------------
+struct GeoP {
+    int kh, wl_stages;
+    uint32_t xpanel, ytpanel, ybytes, ppanel, pbytes, wlpanel;
+    __host__ __device__ GeoP(const Params& p) {
+        kh = p.k_pad / 2;
+        xpanel = (uint32_t)p.n_pad * 128u;
+        ytpanel = (uint32_t)kh * 128u;                       // one 64-wide K panel of this CTA's Y^T rows
+        ybytes = (((uint32_t)p.n_pad / 64u) * ytpanel + 1023u) & ~1023u;
+        ppanel = (uint32_t)p.k_pad * 128u;
+        pbytes = (2 * ppanel + 1023u) & ~1023u;
+        wlpanel = 128u * 128u;
+        const int64_t left = 227 * 1024 - 1024 - 512 - 2 * (int64_t)xpanel - ybytes - pbytes;
+        wl_stages = (int)(left / wlpanel);
+        if (wl_stages > 8) wl_stages = 8;
+    }
+};
+
+__global__ void __launch_bounds__(kLargeThreads, 1)
+    fm_lcb_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWL,
+                       const __grid_constant__ CUtensorMap tmYT, const Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int kpad = p.k_pad;
+    constexpr int d = 128;
+    const GeoP g(p);
+    const int NW = g.wl_stages;
+    const int panels_n = p.n_pad / 64;
+    uint8_t* sX = smem;                       // [2 d-panels][n_pad rows][128 B]: this CTA's sample
+    uint8_t* sWL = sX + 2 * g.xpanel;         // ring [NW][128 rows][128 B]: this CTA's W_L rows
+    uint8_t* sYT = sWL + NW * g.wlpanel;      // [panels_n][k/2 rows][128 B]: this CTA's Y^T rows, resident
+    uint8_t* sP = sYT + g.ybytes;             // [2 d-panels][k_pad][128 B]: this sample's P^T (F's B half)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + g.pbytes);
+    uint64_t* x_full = bars;          // [4] leader: both CTAs' chunk c landed
+    uint64_t* x_empty = bars + 4;     // [4] local: chunk c consumed (F M-tile c + own-sample LCB reads)
+    uint64_t* wl_full = bars + 8;     // [NW <= 8] leader
+    uint64_t* wl_empty = bars + 16;   // [NW] local
+    uint64_t* y_full = bars + 24;     // leader: both CTAs' Y^T halves resident
+    uint64_t* pl_full = bars + 25;    // local: P and L accumulated
+    uint64_t* pbuf_full = bars + 26;  // leader: both CTAs' P routed (8 warps)
+    uint64_t* f_full = bars + 27;     // local: F accumulated
+    uint64_t* l_empty = bars + 28;    // leader: L drained (16 LCB warps of both CTAs)
+    uint64_t* f_empty = bars + 29;    // leader: F drained (8 FM warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
+    float* red_f = reinterpret_cast<float*>(bars + 31);  // [2][4]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = (int)tc::cluster_rank();
+    const int64_t npairs = (p.B + 1) / 2;
+    const int64_t first = blockIdx.x >> 1, stride = gridDim.x >> 1;
+    if (warp == 0 && lane == 0) {
+        tc::tma_prefetch(&tmX);
+        tc::tma_prefetch(&tmWL);
+        tc::tma_prefetch(&tmYT);
+        for (int c = 0; c < 4; ++c) {
+            // the MMA commit + this CTA's LCB warps whose residual rows (own sample) lie in chunk c
+            int readers = 0;
+            for (int q = 0; q < 4; ++q) {
+                const int i = 128 * rank + 32 * q;
+                if (i < p.nL && ((p.nF + i) >> 7) == c) ++readers;
+            }
+            tc::mbar_init(&x_full[c], 1);
+            tc::mbar_init(&x_empty[c], 1 + readers);
+        }
+        for (int i = 0; i < NW; ++i) {
+            tc::mbar_init(&wl_full[i], 1);
+            tc::mbar_init(&wl_empty[i], 1);
+        }
+        tc::mbar_init(y_full, 1);
+        tc::mbar_init(pl_full, 1);
+        tc::mbar_init(pbuf_full, 8);
+        tc::mbar_init(f_full, 1);
+        tc::mbar_init(l_empty, 16);
+        tc::mbar_init(f_empty, 8);
+        tc::fence_mbar_init();
+    }
+    if (warp == 1) tc::tmem_alloc_cg2(tmem_slot, 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    tc::cluster_sync();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t t_L = tmem, t_F = tmem + 256, t_P = t_F;  // P is routed out before F overwrites it
+    tc::griddep_wait();
+    tc::griddep_launch_dependents();
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- X producer: this CTA's sample, four 128-row chunks, completions on the leader
+            int it = 0;
+            for (int64_t sp = first; sp < npairs; sp += stride, ++it) {
+                const int b = (int)(2 * sp + rank);  // b == B (odd batch): zero-filled or unused rows, no output
+                for (int c = 0; c < 4; ++c) {
+                    tc::mbar_wait(&x_empty[c], (it & 1) ^ 1);
+                    if (rank == 0) tc::mbar_expect_tx(&x_full[c], 2u * 2u * 128u * 128u);
+                    const uint32_t bar = tc::mapa(tc::smem_u32(&x_full[c]), 0);
+                    for (int pd = 0; pd < 2; ++pd)
+                        tc::tma_load_3d_cg2(sX + pd * g.xpanel + c * 16384, &tmX, bar, pd * 64, c * 128, b);
+                }
+            }
+        }
+    } else if (warp == 2) {
+        if (lane == 0) {  // ---- W_L producer: this CTA's 128 rows, K panel by K panel
+            int gw = 0;
+            for (int64_t sp = first; sp < npairs; sp += stride) {
+                for (int kp = 0; kp < panels_n; ++kp, ++gw) {
+                    const int s = gw % NW;
+                    tc::mbar_wait(&wl_empty[s], ((gw / NW) & 1) ^ 1);
+                    if (rank == 0) tc::mbar_expect_tx(&wl_full[s], 2u * g.wlpanel);
+                    tc::tma_load_2d_cg2(sWL + s * g.wlpanel, &tmWL, tc::mapa(tc::smem_u32(&wl_full[s]), 0), kp * 64,
+                                        rank * 128);
+                }
+            }
+        }
+    } else if (warp == 3) {
+        if (lane == 0) {  // ---- Y^T rows [r k/2, +k/2), once
+            if (rank == 0) tc::mbar_expect_tx(y_full, 2u * (uint32_t)panels_n * g.ytpanel);
+            const uint32_t bar = tc::mapa(tc::smem_u32(y_full), 0);
+            for (int kp = 0; kp < panels_n; ++kp)
+                tc::tma_load_2d_cg2(sYT + kp * g.ytpanel, &tmYT, bar, kp * 64, rank * g.kh);
+        }
+    } else if (warp == 1) {
+        if (rank == 0) {  // ---- MMA issuer (leader): the whole warp walks the schedule, one lane issues
+            const uint32_t id_P = tc::idesc_bf16(256, kpad, 1, 0);
+            const uint32_t id_L = tc::idesc_bf16(256, 256, 0, 1);
+            const uint32_t id_F = tc::idesc_bf16(256, 2 * kpad, 0, 0);
+            const uint64_t dx_mn = tc::sdesc(tc::smem_u32(sX), g.xpanel, 1024, 2);  // X^T (P: A) / X (L: B)
+            const uint64_t dx_k = tc::sdesc(tc::smem_u32(sX), 16, 1024, 2);         // X (F: A)
+            const uint64_t dy = tc::sdesc(tc::smem_u32(sYT), 16, 1024, 2);
+            const uint64_t dwl = tc::sdesc(tc::smem_u32(sWL), 16, 1024, 2);
+            const uint64_t dp = tc::sdesc(tc::smem_u32(sP), 16, 1024, 2);
+            int it = 0, sw = 0;
+            uint32_t pw = 0;
+            unsigned long long wt[16] = {0};
+            const long long t_start = clock64();
+            tc::mbar_wait(y_full, 0);
+            for (int64_t sp = first; sp < npairs; sp += stride, ++it) {
+                const uint32_t ph = it & 1;
+                FM_WAIT(0, l_empty, ph ^ 1);  // the previous pass's L is drained
+                FM_WAIT(5, f_empty, ph ^ 1);  // ... and its F (P shares F's columns)
+                tc::fence_after();
+                for (int kp = 0; kp < panels_n; ++kp) {
+                    if ((kp & 1) == 0) FM_WAIT(1, &x_full[kp >> 1], ph);
+                    tc::fence_after();
+                    const uint64_t xk = dx_mn + (uint64_t)((kp * 64 * 128) >> 4);
+                    const uint64_t yk = dy + (uint64_t)((kp * g.ytpanel) >> 4);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)  // P += X^T[:, k0:k0+16] . Y[k0:k0+16, :]
+                        tc::mma_f16_cg2_warp(t_P, xk + (uint64_t)((j * 16 * 128) >> 4), yk + (uint64_t)(j * 2), id_P,
+                                             (kp | j) != 0);
+                    FM_WAIT(3, &wl_full[sw], pw);
+                    tc::fence_after();
+                    const uint64_t wk = dwl + (uint64_t)((sw * g.wlpanel) >> 4);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)  // L += W_L[:, k0:k0+16] . [X_a | X_b][k0:k0+16, :]
+                        tc::mma_f16_cg2_warp(t_L, wk + (uint64_t)(j * 2), xk + (uint64_t)((j * 16 * 128) >> 4), id_L,
+                                             (kp | j) != 0);
+                    tc::mma_commit_cg2_warp(&wl_empty[sw]);
+                    if (++sw == NW) sw = 0, pw ^= 1;
+                }
+                tc::mma_commit_cg2_warp(pl_full);
+                FM_WAIT(4, pbuf_full, ph);
+                tc::fence_after();
+                for (int mt = 0; mt < 4; ++mt) {  // F = X [P_a | P_b], M-tile mt = X chunk mt
+#pragma unroll
+                    for (int kk = 0; kk < d / 16; ++kk) {
+                        const uint32_t pan = (uint32_t)(kk / 4), kin = (uint32_t)(kk % 4) * 32;
+                        tc::mma_f16_cg2_warp(t_F + mt * 2 * kpad,
+                                             dx_k + (uint64_t)((pan * g.xpanel + mt * 16384 + kin) >> 4),
+                                             dp + (uint64_t)((pan * g.ppanel + kin) >> 4), id_F, kk != 0);
+                    }
+                    tc::mma_commit_cg2_warp(&x_empty[mt]);  // every MMA reading chunk mt (both CTAs) is done
+                }
+                tc::mma_commit_cg2_warp(f_full);
+            }
+            if (p.trace && lane == 0) {
+                for (int i = 0; i < 6; ++i) p.trace[blockIdx.x * 16 + i] = wt[i];
+                p.trace[blockIdx.x * 16 + 6] = (unsigned long long)(clock64() - t_start);
+                p.trace[blockIdx.x * 16 + 7] = (unsigned long long)it;
+            }
+        }
+    } else if (warp < 12) {  // ---- LCB, warps 4..11: lane quarter q, sample half h (L columns [128h, +128))
+        const int q = warp & 3;
+        const int h = (warp - 4) >> 2;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const float inv_d = 1.0f / (float)d;
+        const int i = 128 * rank + 32 * q + lane;  // W_L row
+        const bool live = 128 * rank + 32 * q < p.nL;  // warp-uniform (nL % 32 == 0)
+        const bool local = h == rank;                  // the residual rows sit in this CTA's smem
+        const int xr = p.nF + i;
+        const uint32_t t = t_L + lane_off + h * 128;
+        int it = 0;
+        unsigned long long t_epi = 0;
+        for (int64_t sp = first; sp < npairs; sp += stride, ++it) {
+            const int64_t bh = 2 * sp + h;
+            const bool act = live && bh < p.B;
+            // the residual row X[bh][nF+i] in registers: the partner's sample from global memory,
+            // issued before the wait so its latency hides behind the MMAs; this CTA's own from smem
+            uint4 res[16];
+            if (act && !local) {
+                const uint4* grow = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.Xin) +
+                                                                   (bh * p.n + xr) * (int64_t)d);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) res[j] = __ldg(grow + j);
+            }
+            tc::mbar_wait(pl_full, it & 1);
+            tc::fence_after();
+            const long long t0 = clock64();
+            if (act) {  // X'[nF+i] = rms_norm_d(L[i] + X[nF+i]): sum of squares, then normalise + store
+                if (local) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        res[j] = *reinterpret_cast<const uint4*>(sX + (j / 8) * g.xpanel + swz<2>(xr, (j * 8) & 63));
+                }
+                float ss4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int c = 0; c < d; c += 16) {
+                    float v[16];
+                    tc::tmem_ld16(t + c, v);
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const uint4 r = res[c / 8 + hh];
+                        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float a = v[8 * hh + 2 * k] + bf16_lo(w[k]), bb = v[8 * hh + 2 * k + 1] + bf16_hi(w[k]);
+                            ss4[k] = fmaf(a, a, ss4[k]);
+                            ss4[k] = fmaf(bb, bb, ss4[k]);
+                        }
+                    }
+                }
+                const float ss = (ss4[0] + ss4[1]) + (ss4[2] + ss4[3]);
+                const float inv = 1.0f / sqrtf(ss * inv_d + 1e-6f);
+                __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.Xout) + (bh * p.n + xr) * (int64_t)d;
+#pragma unroll
+                for (int c = 0; c < d; c += 16) {
+                    float v[16];
+                    tc::tmem_ld16(t + c, v);
+                    uint32_t o[8];
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {  // the residual again (smem, or L1/L2 for the partner's)
+                        const int e = c + 8 * hh;
+                        const uint4 r = local ? *reinterpret_cast<const uint4*>(sX + (e / 64) * g.xpanel + swz<2>(xr, e & 63))
+                                              : __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.Xin) +
+                                                                                     (bh * p.n + xr) * (int64_t)d + e));
+                        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            o[4 * hh + k] = pack_bf16x2((v[8 * hh + 2 * k] + bf16_lo(w[k])) * inv,
+                                                        (v[8 * hh + 2 * k + 1] + bf16_hi(w[k])) * inv);
+                    }
+                    st_global_256(dst + c, make_uint4(o[0], o[1], o[2], o[3]), make_uint4(o[4], o[5], o[6], o[7]));
+                }
+            }
+            __syncwarp();
+            if (live && local && lane == 0) tc::mbar_arrive(&x_empty[xr >> 7]);
+            tc::fence_before();
+            if (lane == 0) tc::mbar_arrive_remote_relaxed(tc::mapa(tc::smem_u32(l_empty), 0));
+            t_epi += (unsigned long long)(clock64() - t0);
+        }
+        // trace: slot 9 = the local-residual LCB warp's epilogue cycles, slot 10 = the partner-residual one
+        if (p.trace && lane == 0 && q == 0) p.trace[blockIdx.x * 16 + (local ? 9 : 10)] = t_epi;
+    } else {  // ---- FM, warps 12..15: route P to Pbuf, then Fin = rms_norm(flatten(X P)) of this CTA's sample
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const float inv_nk = 1.0f / (float)(p.n * p.k);
+        int it = 0;
+        for (int64_t sp = first; sp < npairs; sp += stride, ++it) {
+            const int64_t bo = 2 * sp + rank;
+            tc::mbar_wait(pl_full, it & 1);
+            tc::fence_after();
+            for (int c0 = 0; c0 < kpad; c0 += 16) {  // P row `row` (a d index) -> bf16 -> Pbuf[j][row]
+                float pv[16];
+                tc::tmem_ld16(t_P + lane_off + c0, pv);
+                uint8_t* pan = sP + (row / 64) * g.ppanel;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    *reinterpret_cast<__nv_bfloat16*>(pan + swz<2>(c0 + j, row & 63)) = __float2bfloat16_rn(pv[j]);
+            }
+            tc::fence_async_shared();
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive_remote(tc::mapa(tc::smem_u32(pbuf_full), 0));
+            tc::mbar_wait(f_full, it & 1);
+            tc::fence_after();
+            const uint32_t tf = t_F + lane_off + rank * kpad;  // this sample's columns of each M-tile
+            float ss4[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int mt = 0; mt < 4; ++mt) {
+                const int r = mt * 128 + row;
+                for (int c0 = 0; c0 < kpad; c0 += 16) {
+                    float v[16];
+                    tc::tmem_ld16(tf + mt * 2 * kpad + c0, v);
+                    if (r < p.n) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (c0 + j < p.k) ss4[j & 3] = fmaf(v[j], v[j], ss4[j & 3]);
+                    }
+                }
+            }
+            const float ssw = warp_sum((ss4[0] + ss4[1]) + (ss4[2] + ss4[3]));
+            float* red = red_f + (it & 1) * 4;
+            if (lane == 0) red[q] = ssw;
+            tc::named_bar(2, 128);
+            const float inv = 1.0f / sqrtf((red[0] + red[1] + red[2] + red[3]) * inv_nk + 1e-6f);
+            if (bo < p.B) {
+                for (int mt = 0; mt < 4; ++mt) {
+                    const int r = mt * 128 + row;
+                    for (int c0 = 0; c0 < kpad; c0 += 16) {
+                        float v[16];
+                        tc::tmem_ld16(tf + mt * 2 * kpad + c0, v);
+                        if (r < p.n) {
+                            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.Fout) + bo * (int64_t)p.n * p.k +
+                                                 (int64_t)r * p.k + c0;
+                            if ((p.k & 15) == 0) {
+                                float o[16];
+#pragma unroll
+                                for (int k = 0; k < 16; ++k) o[k] = v[k] * inv;
+                                Store<__nv_bfloat16>::row16(dst, o);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 16; ++j)
+                                    if (c0 + j < p.k) dst[j] = __float2bfloat16_rn(v[j] * inv);
+                            }
+                        }
+                    }
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive_remote_relaxed(tc::mapa(tc::smem_u32(f_empty), 0));
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::cluster_sync();  // the leader's MMAs read the partner's smem and write its TMEM until the end
+    if (warp == 1) tc::tmem_dealloc_cg2(tmem, 512);
+}
+
+size_t smem_bytes_pair(const Params& p) {
+    const GeoP g(p);
+    return 1024 + 2 * (size_t)g.xpanel + (size_t)g.wl_stages * g.wlpanel + g.ybytes + g.pbytes + 512;
+}
+
+// opt-in (LATTICE_FM_PAIR=1) for the large shapes it was written for: measured slower than the
+// single-CTA kernel (4.49 vs 3.48 ms at B = 65536) -- its L accumulator fills
+// half of TMEM with no second buffer, so each pass's LCB epilogue sits on the MMA critical path
+bool is_pair(const Params& p) {
+    static const int env = [] {
+        const char* e = std::getenv("LATTICE_FM_PAIR");
+        return e ? std::atoi(e) : 0;
+    }();
+    return env != 0 && p.n_pad == 512 && !p.f32 && p.d == 128 && (p.k_pad == 16 || p.k_pad == 32) &&
+           p.nF % 32 == 0 && p.nL % 32 == 0 && GeoP(p).wl_stages >= 3 && smem_bytes_pair(p) <= 227 * 1024;
+}
+
+
 size_t smem_bytes(const Params& p) {
     if (is_large(p)) return smem_bytes_large(p);
     const Geo g(p, p.f32 ? 4 : 2);
@@ -903,8 +1281,9 @@ lattice_status make_maps(Plan* pl, const void* X, const void* WLpad, const void*
     lattice_status s = gemm::make_map_2d(&pl->tmWL, WLpad, (uint64_t)p.n_pad, (uint64_t)wl_rows(p),
                                          (uint64_t)p.n_pad * es, ep, 128, p.f32);
     if (s != LATTICE_OK) return s;
+    // the pair variant: each CTA loads its half of Y^T's rows
     return gemm::make_map_2d(&pl->tmYT, YTpad, (uint64_t)p.n_pad, (uint64_t)p.k_pad, (uint64_t)p.n_pad * es, ep,
-                             (uint32_t)p.k_pad, p.f32);
+                             (uint32_t)(is_large(p) && is_pair(p) ? p.k_pad / 2 : p.k_pad), p.f32);
 }
 
 template <typename T>
@@ -949,6 +1328,42 @@ cudaError_t launch_pdl(K kernel, int grid, int threads, size_t smem, cudaStream_
 }
 
 lattice_status launch(const Plan& pl, cudaStream_t st) {
+    if (is_large(pl.p) && is_pair(pl.p)) {
+        static bool attr = false;
+        if (!attr) {
+            LAT_CUDA(cudaFuncSetAttribute(fm_lcb_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            attr = true;
+        }
+        // persistent grid: as many pairs as the device keeps resident at once (a TPC's two SMs
+        // per pair; not every SM finds a partner), so no pair waits for a second wave
+        static int max_pairs[64] = {0};
+        int dev = 0;
+        LAT_CUDA(cudaGetDevice(&dev));
+        int& mp = max_pairs[dev & 63];
+        if (!mp) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(2 * (num_sms() / 2), 1, 1);
+            cfg.blockDim = dim3(kLargeThreads, 1, 1);
+            cfg.dynamicSmemBytes = smem_bytes_pair(pl.p);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 2;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int mc = 0;
+            if (cudaOccupancyMaxActiveClusters(&mc, fm_lcb_pair_kernel, &cfg) != cudaSuccess || mc < 1)
+                mc = num_sms() / 2;
+            mp = mc;
+        }
+        const int64_t pairs = (pl.p.B + 1) / 2;
+        const int grid = 2 * (int)(pairs < mp ? pairs : mp);
+        if (grid <= 0) return LATTICE_OK;
+        LAT_CUDA(launch_pdl(fm_lcb_pair_kernel, grid, kLargeThreads, smem_bytes_pair(pl.p), st, pl, 2));
+        LAT_CUDA(cudaGetLastError());
+        return LATTICE_OK;
+    }
     if (is_large(pl.p)) {
         static bool attr = false;
         if (!attr) {
@@ -1024,9 +1439,10 @@ extern "C" lattice_status lattice_fm_lcb(const lattice_fm_lcb_args* a, lattice_s
         std::vector<unsigned long long> h((size_t)16 * grid);
         cudaMemcpy(h.data(), pl.p.trace, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost);
         cudaFree(pl.p.trace);
+        const bool pair = fm::is_pair(p);
         const char* names[11] = {"mma:l_empty", "mma:x_full", "mma:yt_full", "mma:wl_full", "mma:pbuf_full",
-                                 "mma:f_empty", "mma:total", "samples", "xprod:x_empty", "wprod:yt_empty",
-                                 "wprod:wl_empty"};
+                                 "mma:f_empty", "mma:total", pair ? "passes" : "samples", "xprod:x_empty",
+                                 pair ? "lcb:own_epi" : "wprod:yt_empty", pair ? "lcb:partner_epi" : "wprod:wl_empty"};
         for (int i = 0; i < 11; ++i) {
             double sum = 0;
             for (int b = 0; b < grid; ++b) sum += (double)h[(size_t)b * 16 + i];

@@ -57,8 +57,14 @@ CASES = [
     (24, 64, 16, 12, 600, "bf16"),       # d = 64, n not a multiple of 16
     (8, 64, 4, 4, 512, "f32"),           # tiny config, fp32 storage on kind::tf32
     (512, 128, 32, 256, 640, "bf16"),    # large block (fm_lcb_large_kernel)
-    (384, 128, 16, 256, 512, "bf16"),    # large variant, zero-padded n
+    (512, 128, 32, 256, 641, "bf16"),    # odd batch (the pair variant's last pair has one sample)
+    (512, 128, 32, 288, 512, "bf16"),    # nL = 224
+    (384, 128, 16, 256, 512, "bf16"),    # zero-padded n, nL = 128, k = 16
+    (400, 128, 32, 200, 512, "bf16"),    # nF, nL not multiples of 32: warps with live and dead lanes
+    (512, 128, 48, 256, 512, "bf16"),    # k = 48
 ]
+PAIR_CASES = ["512-128-32-256-640-bf16", "512-128-32-256-641-bf16", "512-128-32-288-512-bf16",
+              "384-128-16-256-512-bf16"]
 
 
 @pytest.mark.parametrize("n,d,k,nF,B,dtype", CASES)
@@ -93,6 +99,22 @@ def test_fm_lcb_realistic_inputs_calibrated(n, d, k, nF, B, dtype):
     calibrated(tag + " Fin", Fin, refs[torch.float64][0], refs[torch.float32][0], atol=floor, rtol=ulp)
     calibrated(tag + " LCB rows", Xout[:, nF:], refs[torch.float64][1], refs[torch.float32][1], atol=floor,
                rtol=ulp)
+
+
+def test_fm_lcb_pair_kernel():
+    """The opt-in CTA-pair variant (LATTICE_FM_PAIR=1, read once per process) on its shapes, both
+    input families, in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, LATTICE_FM_PAIR="1")
+    f = os.path.join(here, "test_fm_lcb_gpu.py")
+    ids = [f"{f}::{t}[{c}]" for c in PAIR_CASES
+           for t in ("test_fm_lcb_exact_inputs_one_rounding", "test_fm_lcb_realistic_inputs_calibrated")]
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", *ids], env=env,
+                       capture_output=True, text=True, timeout=600, cwd=os.path.dirname(here))
+    assert r.returncode == 0 and f"{len(ids)} passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
 
 
 def test_fm_lcb_contract():
