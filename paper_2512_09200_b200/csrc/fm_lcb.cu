@@ -732,9 +732,10 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
                 tc::fence_async_shared();
                 tc::mbar_arrive(pbuf_full);
             }
-            if (warp_live) {  // X'[nF+i] = rms_norm_d(L[i] + X[nF+i]): sum of squares, then normalise + store;
-                         // the residual row is read from the X chunk in shared memory, which this
-                         // thread releases afterwards (the next sample's chunk loads behind it)
+            if (warp_live) {  // X'[nF+i] = rms_norm_d(L[i] + X[nF+i]): pass 1 forms L + X (the residual
+                              // row from the X chunk in shared memory, read once), keeps it in TMEM in
+                              // place of L and sums its squares; pass 2 normalises and stores. The
+                              // chunk is released after pass 1 (the next sample's chunk loads behind it).
                 float ss4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int c = 0; c < d; c += 16) {
@@ -747,12 +748,16 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
                         const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
-                            const float a = v[8 * hh + 2 * k] + bf16_lo(w[k]), bb = v[8 * hh + 2 * k + 1] + bf16_hi(w[k]);
-                            ss4[k] = fmaf(a, a, ss4[k]);
-                            ss4[k] = fmaf(bb, bb, ss4[k]);
+                            v[8 * hh + 2 * k] += bf16_lo(w[k]);
+                            v[8 * hh + 2 * k + 1] += bf16_hi(w[k]);
+                            ss4[k] = fmaf(v[8 * hh + 2 * k], v[8 * hh + 2 * k], ss4[k]);
+                            ss4[k] = fmaf(v[8 * hh + 2 * k + 1], v[8 * hh + 2 * k + 1], ss4[k]);
                         }
                     }
+                    tc::tmem_st16(t_L + c, v);
                 }
+                tc::tmem_wait_st();
+                if (live) tc::mbar_arrive(&x_empty[cx]);
                 const float ss = (ss4[0] + ss4[1]) + (ss4[2] + ss4[3]);
                 const float inv = 1.0f / sqrtf(ss * inv_d + 1e-6f);
                 __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.Xout) + (b * p.n + xr) * (int64_t)d;
@@ -762,19 +767,10 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
                     tc::tmem_ld16(t_L + c, v);
                     uint32_t o[8];
 #pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        const int e = c + 8 * hh;
-                        const uint4 r = *reinterpret_cast<const uint4*>(sX + (e / 64) * g.xpanel + swz<2>(xr, e & 63));
-                        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            o[4 * hh + k] = pack_bf16x2((v[8 * hh + 2 * k] + bf16_lo(w[k])) * inv,
-                                                        (v[8 * hh + 2 * k + 1] + bf16_hi(w[k])) * inv);
-                    }
+                    for (int k = 0; k < 8; ++k) o[k] = pack_bf16x2(v[2 * k] * inv, v[2 * k + 1] * inv);
                     if (live)
                         st_global_256(dst + c, make_uint4(o[0], o[1], o[2], o[3]), make_uint4(o[4], o[5], o[6], o[7]));
                 }
-                if (live) tc::mbar_arrive(&x_empty[cx]);
             }
             tc::fence_before();
             tc::mbar_arrive(mt == 0 ? l_empty : l1_empty);
