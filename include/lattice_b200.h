@@ -161,6 +161,24 @@ lattice_status lattice_ipc_close(void* dptr);
 lattice_status lattice_peer_barrier(uint32_t* const* flags, int32_t rank, int32_t world,
                                     double timeout_s, int32_t* status, lattice_stream stream);
 
+/* Data-parallel gradient reduction fused with the optimizer over peer memory (replaces an NCCL
+ * all-reduce + a separate SGD pass): rank r owns elements [r*S, (r+1)*S) of the flat gradient
+' * buffer (S = ceil(n / world) rounded up to a multiple of 4); for each it sums every rank's gradient in rank order (grads:
+ * DEVICE [world] peer-mapped pointers), divides by world and, per segment, either applies SGD to
+ * this rank's flat fp32 master (ZeRO-1: only the owned shard [r*S, (r+1)*S) of `master` is kept
+ * current) and writes the new weight (dst dtype) into EVERY rank's copy, or (mode 1) writes the
+ * mean itself (e.g. a loss). Deterministic: replicas' weights stay bit-identical.
+ * Bracket it with lattice_peer_barrier (gradients published before; copies written after). */
+typedef struct {
+    int64_t offset, count;   /* elements [offset, offset + count) of the flat buffers */
+    int32_t mode;            /* 0: sgd; 1: mean */
+    int32_t dst_dtype;       /* LATTICE_F32, or LATTICE_BF16 for sgd segments */
+    void* const* dst;        /* DEVICE [world]: every rank's destination (element j = offset + j) */
+} lattice_peer_seg;
+lattice_status lattice_peer_reduce_sgd(const float* const* grads, float* master,
+                                       const lattice_peer_seg* segs, int32_t nseg, int64_t n,
+                                       int32_t rank, int32_t world, float lr, lattice_stream stream);
+
 /* Sender side of the static ids exchange: out[o][j] = ids[bounds[o] + j] for
  * j < bounds[o+1] - bounds[o] (o < slices); slices longer than cap set *overflow = 1.
  * All sizes are read on the device: no host synchronisation. */

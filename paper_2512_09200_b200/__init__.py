@@ -66,6 +66,10 @@ class BagArgs(ctypes.Structure):
                 ("slice_cap", _I64)]
 
 
+class PeerSeg(ctypes.Structure):
+    _fields_ = [("offset", _I64), ("count", _I64), ("mode", _I32), ("dst_dtype", _I32), ("dst", _P)]
+
+
 class PeerBagArgs(ctypes.Structure):
     _fields_ = [("rank", _I32), ("world", _I32), ("features_local", _I32), ("feature_base", _I32),
                 ("batch", _I64), ("dim", _I32), ("table_dtype", _I32), ("tables", _P), ("rows", _P),
@@ -155,6 +159,7 @@ _sig("lattice_ipc_handle", ctypes.c_int, [_P, _P, ctypes.POINTER(_I64)])
 _sig("lattice_ipc_open", ctypes.c_int, [_P, _I64, ctypes.POINTER(_P)])
 _sig("lattice_ipc_close", ctypes.c_int, [_P])
 _sig("lattice_peer_barrier", ctypes.c_int, [_P, _I32, _I32, ctypes.c_double, _P, _P])
+_sig("lattice_peer_reduce_sgd", ctypes.c_int, [_P, _P, _P, _I32, _I64, _I32, _I32, ctypes.c_float, _P])
 _sig("lattice_net_bucket", ctypes.c_int, [_P, _I64, _P, _P])
 _sig("lattice_net_buffer", _P, [_P, _I32])
 _sig("lattice_correlation_loss", ctypes.c_int, [_I64, _I32, _P, _I64, _P, _I64, ctypes.c_double, _P, _I32, _P])
@@ -206,7 +211,7 @@ EXPORTS = ["lattice_last_error", "lattice_last_error_index", "lattice_abi_versio
            "lattice_jsonl_close", "lattice_net_set_weight", "lattice_fm_lcb",
            "lattice_rownorm_f64", "lattice_device_check", "lattice_rownorm_vjp", "lattice_routed_bce",
            "lattice_net_tower_backward", "lattice_net_tower_sgd", "lattice_net_mlp_backward",
-           "lattice_net_weight_sgd"]
+           "lattice_net_weight_sgd", "lattice_peer_reduce_sgd"]
 
 lib = _lib
 
@@ -412,6 +417,17 @@ def ipc_close(ptr):
 def peer_barrier(flag_ptrs, rank, world, status, timeout_s=30.0, stream=None):
     """Stream-ordered cross-GPU barrier over peer-mapped flag arrays (lattice_peer_barrier)."""
     check(_lib.lattice_peer_barrier(_p(flag_ptrs), rank, world, timeout_s, _p(status), _stream(stream)))
+
+
+def peer_reduce_sgd(grad_ptrs, master, segs, n, rank, world, lr, stream=None):
+    """lattice_peer_reduce_sgd: grad_ptrs int64 device tensor [world] of peer-mapped pointers;
+    master: this rank's flat fp32 masters (its shard is updated); segs: list of
+    (offset, count, mode, dst_dtype, dst_ptrs tensor [world])."""
+    arr = (PeerSeg * len(segs))()
+    for i, (off, cnt, mode, dt, dst) in enumerate(segs):
+        arr[i] = PeerSeg(off, cnt, mode, dt, ctypes.c_void_p(dst.data_ptr()))
+    check(_lib.lattice_peer_reduce_sgd(_p(grad_ptrs), _p(master), arr, len(segs), n, rank, world, lr,
+                                       _stream(stream)))
 
 
 def merge_dense(domain, values, src_col, out_width, out_dtype=None, check_errors=True, stream=None):
@@ -887,6 +903,13 @@ class Network:
         w = c["mlp"]
         return [_view(_lib.lattice_net_weight(self._h, blk, 3, i), (w[i + 1], w[i]), wdt).float().clone()
                 for i in range(len(w) - 1)]
+
+    def weight_ptr(self, block, kind, index=0):
+        """Device pointer of one weight buffer (lattice_net_weight; kinds as set_weight)."""
+        p = _lib.lattice_net_weight(self._h, block, kind, index)
+        if not p:
+            raise UsageError(f"lattice_net_weight: no weight (block {block}, kind {kind}, index {index})")
+        return p
 
     def tower_masters(self):
         """fp32 device copies of the towers' W1 [G, th, n*d] and W2 [G, heads, th] (SGD masters)."""

@@ -161,3 +161,122 @@ lattice_status lattice_peer_barrier(uint32_t* const* flags, int32_t rank, int32_
 }
 
 }  // extern "C"
+
+// ---- data-parallel gradient reduction fused with the optimizer, over peer memory ---------------
+namespace lat {
+namespace {
+constexpr int kMaxSegs = 16;
+struct SegK {
+    int64_t off, cnt;
+    int32_t mode, bf16;
+    void* const* dst;
+};
+struct ReduceParams {
+    const float* const* grads;
+    float* master;
+    SegK seg[kMaxSegs];
+    int32_t nseg, world, rank;
+    int64_t lo, hi;
+    float lr;
+};
+
+// Owner of elements [lo, hi): mean of every rank's gradient in rank order (read over NVLink,
+// uncached), SGD on this rank's fp32 master shard (ZeRO-1: each master element lives on its
+// owner only), and the new weight written into EVERY rank's copy (NVLink stores) --
+// reduce-scatter + optimizer + all-gather in one pass, deterministic, so all replicas hold
+// identical weights.
+__device__ __forceinline__ void reduce_sgd_one(const ReduceParams& p, const SegK& sg, int64_t i) {
+    float g = 0.0f;
+    for (int r = 0; r < p.world; ++r) g += __ldcv(p.grads[r] + i);
+    g = g / (float)p.world;
+    const int64_t j = i - sg.off;
+    if (sg.mode == 1) {  // mean only (e.g. the loss)
+        for (int r = 0; r < p.world; ++r) static_cast<float*>(sg.dst[r])[j] = g;
+        return;
+    }
+    const float w = p.master[i] - p.lr * g;
+    p.master[i] = w;
+    for (int r = 0; r < p.world; ++r) {
+        if (sg.bf16)
+            static_cast<__nv_bfloat16*>(sg.dst[r])[j] = __float2bfloat16_rn(w);
+        else
+            static_cast<float*>(sg.dst[r])[j] = w;
+    }
+}
+
+// groups of 4 elements: 16-byte gradient loads from every rank and 8 / 16-byte weight stores
+// when the group sits inside one segment at a 4-aligned position, element by element otherwise
+__global__ void reduce_sgd_kernel(const ReduceParams p) {
+    int s = 0;
+    for (int64_t i0 = p.lo + 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); i0 < p.hi;
+         i0 += 4 * (int64_t)gridDim.x * blockDim.x) {
+        while (s + 1 < p.nseg && i0 >= p.seg[s + 1].off) ++s;
+        const SegK& sg = p.seg[s];
+        const int64_t j0 = i0 - sg.off;
+        if (j0 >= 0 && ((j0 | i0) & 3) == 0 && i0 + 4 <= sg.off + sg.cnt && i0 + 4 <= p.hi && sg.mode == 0) {
+            float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int r = 0; r < p.world; ++r) {
+                const float4 v = __ldcv(reinterpret_cast<const float4*>(p.grads[r] + i0));
+                g.x += v.x, g.y += v.y, g.z += v.z, g.w += v.w;
+            }
+            const float W = (float)p.world;
+            float4 m = *reinterpret_cast<const float4*>(p.master + i0);
+            m.x = m.x - p.lr * (g.x / W), m.y = m.y - p.lr * (g.y / W);
+            m.z = m.z - p.lr * (g.z / W), m.w = m.w - p.lr * (g.w / W);
+            *reinterpret_cast<float4*>(p.master + i0) = m;
+            if (sg.bf16) {
+                const uint2 o = make_uint2(pack_bf16x2(m.x, m.y), pack_bf16x2(m.z, m.w));
+                for (int r = 0; r < p.world; ++r)
+                    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(sg.dst[r]) + j0) = o;
+            } else {
+                for (int r = 0; r < p.world; ++r) *reinterpret_cast<float4*>(static_cast<float*>(sg.dst[r]) + j0) = m;
+            }
+            continue;
+        }
+        for (int64_t i = i0; i < i0 + 4 && i < p.hi; ++i) {  // segment edges, gaps, the loss
+            int t = 0;
+            while (t + 1 < p.nseg && i >= p.seg[t + 1].off) ++t;
+            if (i >= p.seg[t].off && i < p.seg[t].off + p.seg[t].cnt) reduce_sgd_one(p, p.seg[t], i);
+        }
+    }
+}
+}  // namespace
+}  // namespace lat
+
+extern "C" lattice_status lattice_peer_reduce_sgd(const float* const* grads, float* master,
+                                                   const lattice_peer_seg* segs, int32_t nseg, int64_t n, int32_t rank,
+                                                   int32_t world, float lr, lattice_stream stream) {
+    using namespace lat;
+    LAT_REQUIRE(grads && master && segs, "peer_reduce_sgd: null argument");
+    LAT_REQUIRE(world >= 1 && world <= 1024 && rank >= 0 && rank < world, "peer_reduce_sgd: bad rank/world");
+    LAT_REQUIRE(nseg >= 1 && nseg <= kMaxSegs, "peer_reduce_sgd: need 1..16 segments");
+    LAT_REQUIRE(n >= 0, "peer_reduce_sgd: bad size");
+    ReduceParams p = {};
+    p.grads = grads;
+    p.master = master;
+    p.nseg = nseg;
+    p.world = world;
+    p.rank = rank;
+    p.lr = lr;
+    int64_t prev_end = 0;
+    for (int i = 0; i < nseg; ++i) {
+        const lattice_peer_seg& q = segs[i];
+        LAT_REQUIRE(q.offset >= prev_end && q.count >= 0 && q.offset + q.count <= n,
+                    "peer_reduce_sgd: segments must be sorted, disjoint and inside [0, n)");
+        LAT_REQUIRE(q.mode == 0 || q.mode == 1, "peer_reduce_sgd: mode must be 0 (sgd) or 1 (mean)");
+        LAT_REQUIRE(q.dst != nullptr, "peer_reduce_sgd: null dst");
+        LAT_REQUIRE(q.dst_dtype == LATTICE_F32 || (q.dst_dtype == LATTICE_BF16 && q.mode == 0),
+                    "peer_reduce_sgd: dst dtype must be f32 (or bf16 for sgd segments)");
+        p.seg[i] = {q.offset, q.count, q.mode, q.dst_dtype == LATTICE_BF16 ? 1 : 0, q.dst};
+        prev_end = q.offset + q.count;
+    }
+    const int64_t shard = ((n + world - 1) / world + 3) / 4 * 4;  // 4-aligned shards
+    p.lo = (int64_t)rank * shard < n ? (int64_t)rank * shard : n;
+    p.hi = p.lo + shard < n ? p.lo + shard : n;
+    if (p.hi <= p.lo) return LATTICE_OK;
+    const int64_t blocks = (p.hi - p.lo + 1023) / 1024;
+    const unsigned grid = (unsigned)(blocks < (int64_t)num_sms() * 8 ? blocks : num_sms() * 8);
+    reduce_sgd_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(p);
+    LAT_CUDA(cudaGetLastError());
+    return LATTICE_OK;
+}

@@ -49,4 +49,7 @@ def test_data_parallel_tower_training():
            "--master-addr", "127.0.0.1", "--master-port", "29518", os.path.join(ROOT, "tests", "dist_train_check.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert "replicas bit-identical after every step: True" in r.stdout and "loss falls: True" in r.stdout, r.stdout
+    for red in ("nccl", "peer"):  # NCCL all-reduce + SGD, and the fused peer-memory reduce + SGD kernel
+        assert f"[{red}] replicas bit-identical after every step: True" in r.stdout, r.stdout
+        assert f"[{red}] loss falls: True" in r.stdout, r.stdout
+    assert "peer-memory step matches the NCCL step: True" in r.stdout, r.stdout

@@ -111,3 +111,86 @@ def test_single_process_skips_collective():
                       loss_fn=lambda *a: (torch.tensor(0.25, dtype=torch.float64), torch.zeros((2, 2))))
     loss = tr.step(torch.zeros((2, 2)), None, None, 1, 2)
     assert not calls and float(loss) == 0.25 and torch.allclose(tr.W1, W1_0 - 1.0)
+
+
+MAPPED = 1 << 40
+
+
+class FakePeerOps:
+    """IPC / barrier / reduce kernel stand-ins recording the calls (the real ones run in
+    tests/dist_train_check.py on >= 2 GPUs)."""
+    BF16, F32 = 1, 0
+
+    def __init__(self, rank):
+        self.rank, self.log = rank, []
+
+    def ipc_handle(self, ptr):
+        return (int(ptr).to_bytes(8, "little") + bytes([self.rank]) * 56, 0)
+
+    def ipc_open(self, h, off):
+        assert h[8] != self.rank
+        return int.from_bytes(h[:8], "little") + off + MAPPED
+
+    def ipc_close(self, p):
+        pass
+
+    def peer_barrier(self, flags, rank, world, status, timeout_s, stream=None):
+        self.log.append(("barrier",))
+
+    def peer_reduce_sgd(self, grads, masters, segs, n, rank, world, lr, stream=None):
+        self.log.append(("reduce", grads.tolist(), masters.data_ptr(),
+                         [(o, c, m, dt, d.tolist()) for o, c, m, dt, d in segs], n, rank, world, lr))
+
+
+class FakeWeightNet(FakeNet):
+    def __init__(self, rank):
+        super().__init__()
+        self.cfg["dtype"] = "bf16"
+        self.rank = rank
+
+    def weight_ptr(self, block, kind, index=0):
+        return 10_000 * (self.rank + 1) + 100 * kind + 10 * block + index
+
+
+def _peer_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ops = FakePeerOps(rank)
+    net = FakeWeightNet(rank)
+    tr = TowerTrainer(net, lr=0.25, backward=lambda *a: None, loss_fn=lambda *a: (torch.tensor(0.5), torch.zeros(2)),
+                      train_mlp=True, reducer="peer", peer_ops=ops)
+    tr.step(torch.zeros((2, 2)), None, None, 1, 2)
+    kinds = [e[0] for e in ops.log]
+    _, grads, masters, segs, n, r, w, lr = ops.log[1]
+    sizes = [tr.W1.numel(), tr.W2.numel()] + [m.numel() for m in tr.mlp]
+
+    def own_at_rank(ptrs, base):  # own pointer unmapped, peers' mapped
+        return ptrs[rank] == base and all(p >= MAPPED for i, p in enumerate(ptrs) if i != rank)
+
+    ok = (kinds == ["barrier", "reduce", "barrier"] and n == tr.bucket.numel() and (r, w, lr) == (rank, world, 0.25)
+          and own_at_rank(grads, tr.bucket.data_ptr()) and masters == tr.master.data_ptr()
+          and [s[1] for s in segs] == sizes + [1]
+          and [s[0] for s in segs] == tr.offsets + [n - 1]
+          and [s[2] for s in segs] == [0] * len(sizes) + [1]                 # sgd ..., loss: mean
+          and [s[3] for s in segs] == [1, 0, 1, 1, 0]                        # bf16 W1, fp32 W2, bf16 MLP, fp32 loss
+          and own_at_rank(segs[0][4], net.weight_ptr(0, 4)) and own_at_rank(segs[2][4], net.weight_ptr(1, 3, 0))
+          and torch.equal(tr.W1, net.tower_masters()[0]) and torch.equal(tr.mlp[1], net.mlp_masters()[1]))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_reducer_host_logic(world):
+    """TowerTrainer(reducer="peer"): exports bucket / every trained weight / loss (masters stay local), one
+    barrier -> lattice_peer_reduce_sgd -> barrier per step, segments in bucket order (sgd for the
+    weights in their storage dtype, mean for the loss)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world)), res
