@@ -94,3 +94,14 @@ def test_backward_contracts():
     usage(L.lib.lattice_net_tower_backward(None, 4, p, p, p, None, L.F32, None), "null argument")
     usage(L.lib.lattice_net_mlp_backward(None, 4, p, p, None, None, None), "null argument")
     usage(L.lib.lattice_net_weight_sgd(None, 0, 3, 0, 0.1, p, p, None), "null argument")
+
+
+def test_peer_reduce_sgd_contracts():
+    p = ctypes.c_void_p(16)
+    segs = (L.PeerSeg * 2)(L.PeerSeg(0, 8, 0, L.BF16, p), L.PeerSeg(4, 8, 0, L.F32, p))  # overlapping
+    usage(L.lib.lattice_peer_reduce_sgd(None, p, segs, 2, 16, 0, 2, 0.1, None), "null argument")
+    usage(L.lib.lattice_peer_reduce_sgd(p, p, segs, 0, 16, 0, 2, 0.1, None), "1..16 segments")
+    usage(L.lib.lattice_peer_reduce_sgd(p, p, segs, 2, 16, 2, 2, 0.1, None), "bad rank/world")
+    usage(L.lib.lattice_peer_reduce_sgd(p, p, segs, 2, 16, 0, 2, 0.1, None), "sorted, disjoint")
+    bad = (L.PeerSeg * 1)(L.PeerSeg(0, 1, 1, L.BF16, p))  # a mean segment must be fp32
+    usage(L.lib.lattice_peer_reduce_sgd(p, p, bad, 1, 16, 0, 2, 0.1, None), "dst dtype")
