@@ -28,7 +28,6 @@ overlaps the local HBM gathers inside one kernel.
 `ops` is injectable so the handle-exchange logic runs under gloo on CPU
 (tests/test_peer_cpu.py); on GPUs it is this package's ctypes binding.
 """
-import os
 
 import torch
 import torch.distributed as dist
@@ -91,13 +90,6 @@ class PeerBags:
     def pool(self, key, tables, table_ptrs, rows, stream=None):
         off_ptrs, ids_ptrs, _, _ = self.batches[key]
         pos_ptrs, out_ptrs = self.pos_ptrs, self.out_ptrs
-        dbg = os.environ.get("LATTICE_PEER_DEBUG", "")
-        if dbg:  # timing experiments only (wrong results): replace peer pointers by local ones
-            loc = lambda t: torch.full_like(t, int(t[self.r].item()))
-            if "reads" in dbg:
-                off_ptrs, ids_ptrs, pos_ptrs = loc(off_ptrs), loc(ids_ptrs), loc(pos_ptrs)
-            if "stores" in dbg:
-                out_ptrs = loc(out_ptrs)
         self.ops.peer_embedding_bag(self.r, self.W, tables, table_ptrs, rows, self.r * self.Fl, self.B,
                                     off_ptrs, ids_ptrs, pos_ptrs, out_ptrs, self.row_stride,
                                     normalize=True, stream=stream)
