@@ -497,7 +497,7 @@ constexpr int kLargeThreads = kLargeWarps * 32;
 constexpr int kYtStages = 2;
 
 struct GeoL {
-    int panels_n, ml, mf, chunks, wl_stages;
+    int panels_n, ml, mf, chunks, wl_stages, ys;
     uint32_t xpanel, ytpanel, ppanel, wlpanel, pbytes;
     __host__ __device__ GeoL(const Params& p) {
         panels_n = p.n_pad / 64;
@@ -509,8 +509,9 @@ struct GeoL {
         ppanel = (uint32_t)p.k_pad * 128u;
         wlpanel = 128u * 128u;
         pbytes = (2 * ppanel + 1023u) & ~1023u;
-        // as many W_L stages (<= 5) as fit next to X, the Y^T ring and Pbuf (227 KB per CTA)
-        const int64_t left = 227 * 1024 - 1024 - 512 - 2 * (int64_t)xpanel - kYtStages * (int64_t)ytpanel - pbytes;
+        ys = p.y_res ? panels_n : kYtStages;  // Y^T panels held: all (resident) or a 2-deep ring
+        // as many W_L stages (<= 5) as fit next to X, Y^T and Pbuf (227 KB per CTA)
+        const int64_t left = 227 * 1024 - 1024 - 512 - 2 * (int64_t)xpanel - ys * (int64_t)ytpanel - pbytes;
         wl_stages = (int)(left / wlpanel);
         if (wl_stages > 5) wl_stages = 5;
     }
@@ -527,8 +528,8 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
     const int NW = g.wl_stages;
     uint8_t* sX = smem;                                   // [2 d-panels][n_pad rows][128 B]
     uint8_t* sWL = sX + 2 * g.xpanel;                     // ring [NW][128 rows][128 B]
-    uint8_t* sYT = sWL + NW * g.wlpanel;                  // ring [kYtStages][k_pad rows][128 B]
-    uint8_t* sP = sYT + kYtStages * g.ytpanel;            // [2 d-panels][k_pad][128 B]
+    uint8_t* sYT = sWL + NW * g.wlpanel;                  // [ys][k_pad rows][128 B]: ring or resident
+    uint8_t* sP = sYT + g.ys * g.ytpanel;                 // [2 d-panels][k_pad][128 B]
     uint64_t* bars = reinterpret_cast<uint64_t*>(sP + g.pbytes);
     uint64_t* x_full = bars;                  // [4] chunk landed
     uint64_t* x_empty = bars + 4;             // [4] chunk consumed (its F M-tile done)
@@ -616,7 +617,10 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
             if (p.trace) p.trace[blockIdx.x * 16 + 10] = wt[10];
         }
     } else if (warp == 15) {
-        if (lane == 0) {  // ---- Y^T producer: [k_pad x 64] panels through its own ring
+        if (lane == 0 && p.y_res) {  // ---- Y^T resident: every panel once, on yt_full[0]
+            tc::mbar_expect_tx(&yt_full[0], (uint32_t)g.panels_n * g.ytpanel);
+            for (int kp = 0; kp < g.panels_n; ++kp) tc::tma_load_2d(sYT + kp * g.ytpanel, &tmYT, &yt_full[0], kp * 64, 0);
+        } else if (lane == 0) {  // ---- Y^T producer: [k_pad x 64] panels through its own ring
             unsigned long long wt[16] = {0};
             int gy = 0;
             for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
@@ -643,6 +647,7 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
         uint32_t pw = 0, py = 0;  // ring phases
         unsigned long long wt[16] = {0};
         const long long t_start = clock64();
+        if (p.y_res) FM_WAIT(2, &yt_full[0], 0);
         for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x, ++it) {
             const uint32_t ph = it & 1;
             // P and L M-tile 0 over every K panel, then L M-tile 1: the LCB warps of M-tile 0 drain
@@ -663,16 +668,18 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
             };
             for (int kp = 0; kp < g.panels_n; ++kp) {
                 if ((kp & 1) == 0) FM_WAIT(1, &x_full[kp >> 1], ph);
-                FM_WAIT(2, &yt_full[sy], py);
+                if (!p.y_res) FM_WAIT(2, &yt_full[sy], py);
                 tc::fence_after();
                 const uint64_t xk = dx_mn + (uint64_t)((kp * 64 * 128) >> 4);
-                const uint64_t yk = dy + (uint64_t)((sy * g.ytpanel) >> 4);
+                const uint64_t yk = dy + (uint64_t)(((p.y_res ? kp : sy) * g.ytpanel) >> 4);
 #pragma unroll
                 for (int j = 0; j < 4; ++j)  // P += X^T[:, k0:k0+16] . Y[k0:k0+16, :]
                     tc::mma_f16_warp(t_Pb, xk + (uint64_t)((j * 16 * 128) >> 4), yk + (uint64_t)(j * 2), id_P,
                                      (kp | j) != 0);
-                tc::mma_commit_warp(&yt_empty[sy]);
-                if (++sy == kYtStages) sy = 0, py ^= 1;
+                if (!p.y_res) {
+                    tc::mma_commit_warp(&yt_empty[sy]);
+                    if (++sy == kYtStages) sy = 0, py ^= 1;
+                }
                 if (g.ml > 0) l_panel(0, kp);
             }
             tc::mma_commit_warp(pl_full);
@@ -835,7 +842,7 @@ __global__ void __launch_bounds__(kLargeThreads, 1)
 
 size_t smem_bytes_large(const Params& p) {
     const GeoL g(p);
-    return 1024 + 2 * (size_t)g.xpanel + (size_t)g.wl_stages * g.wlpanel + kYtStages * (size_t)g.ytpanel +
+    return 1024 + 2 * (size_t)g.xpanel + (size_t)g.wl_stages * g.wlpanel + g.ys * (size_t)g.ytpanel +
            g.pbytes + 512;
 }
 
@@ -1368,7 +1375,22 @@ lattice_status launch(const Plan& pl, cudaStream_t st) {
         }
         const int grid = (int)(pl.p.B < num_sms() ? pl.p.B : num_sms());
         if (grid <= 0) return LATTICE_OK;
-        LAT_CUDA(launch_pdl(fm_lcb_large_kernel, grid, kLargeThreads, smem_bytes(pl.p), st, pl));
+        // Y^T resident (loaded once per CTA instead of streamed per sample: 32 KB less TMA traffic
+        // into shared memory per sample, the kernel's bound) whenever >= 3 W_L stages still fit:
+        // 3.48 -> 3.32 ms at B = 65536 (profiles/r02/ab/fm_large_yres_*.log); LATTICE_FM_YRES=0
+        // keeps the 2-deep Y^T ring with 5 W_L stages
+        static const int yres_env = [] {
+            const char* e = std::getenv("LATTICE_FM_YRES");
+            return e ? std::atoi(e) : 1;
+        }();
+        Plan pr = pl;
+        pr.p.y_res = 0;
+        if (yres_env) {
+            Params q = pl.p;
+            q.y_res = 1;
+            if (GeoL(q).wl_stages >= 3) pr.p.y_res = 1;
+        }
+        LAT_CUDA(launch_pdl(fm_lcb_large_kernel, grid, kLargeThreads, smem_bytes(pr.p), st, pr));
         LAT_CUDA(cudaGetLastError());
         return LATTICE_OK;
     }

@@ -20,6 +20,7 @@ struct Params {
     void* Fout;             // [B][n*k]
     void* Xout;             // [B][n][d], rows nF .. n-1 written
     unsigned long long* trace;  // optional [grid][16] cycles spent per wait site (LATTICE_FM_TRACE=1)
+    int y_res;              // large variant: Y^T resident in smem (set at launch when it fits)
 };
 
 struct Plan {
