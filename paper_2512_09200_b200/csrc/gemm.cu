@@ -630,8 +630,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     int seen;
                     uint64_t t0 = 0;
                     for (uint32_t spin = 0;; ++spin) {
-                        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
-                        if (seen >= want) break;
+                        // relaxed polling (an acquire load per iteration invalidates L1 every time:
+                        // CCTL.IVALL was the top stall of the 2048-wide swish GEMM); one acquire
+                        // load once the count is reached orders the partial reads after it
+                        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
+                        if (seen >= want) {
+                            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
+                            break;
+                        }
                         // bounded: a partner that never runs (co-residency lost to another workload)
                         // is reported through lattice_device_check instead of hanging the GPU
                         if ((spin & 1023u) == 1023u) {
@@ -670,7 +676,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tc::fence_before();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive_remote(tc::mapa(tc::smem_u32(&tempty[acc]), 0));
+            // relaxed: the TMEM reads are complete (wait::ld + fence::before_thread_sync); a release
+            // would first wait for this warp's output stores to complete (MEMBAR.GPU + ERRBAR)
+            if (lane == 0) tc::mbar_arrive_remote_relaxed(tc::mapa(tc::smem_u32(&tempty[acc]), 0));
         }
     }
     tc::fence_before();
