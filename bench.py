@@ -687,6 +687,50 @@ def emb_stage(workload, t_ms, alg_bytes, hbm):
     return d
 
 
+def train_timing(steps=8, warmup=2):
+    """The data-parallel training step of SURVEY 8f rank 4 at the mid config on one GPU: forward +
+    window-routed BCE (2 objectives x 3 Zipper windows = the 6 heads) + backward of the towers and
+    the last block's MLP + SGD (TowerTrainer(train_mlp=True)), eager launches, device time per
+    step. Not the headline: the reference defines no training step."""
+    import torch
+    import paper_2512_09200_b200 as L
+    from paper_2512_09200_b200.train import TowerTrainer
+    c, B = MID, MID_B
+    n, d = c["n"], c["d"]
+    net = L.Network(**c, max_batch=B, weight_seed=SEED_W)
+    tab = torch.empty((n, MID_ROWS, d), dtype=torch.bfloat16, device="cuda")
+    L.fill_tables(tab, SEED_T)
+    ptrs = torch.tensor([t.data_ptr() for t in tab.unbind(0)], dtype=torch.int64, device="cuda")
+    rows = torch.full((n,), MID_ROWS, dtype=torch.int64, device="cuda")
+    offsets, ids = L.synth_bags(n, B, MID_MAXLEN, MID_ROWS, SEED_D)
+    dom = L.synth_domains(B, c["domains"], SEED_D)
+    imp = L.synth_impressions(B, 2, 7)
+    win, lab, _ = L.zipper_assign_labels(*imp, [5400000, 86400000, 604800000], [1 / 3] * 3, 7)
+    tr = TowerTrainer(net, lr=0.05, train_mlp=True)
+    logits = torch.empty((B, c["heads"]), dtype=torch.float32, device="cuda")
+    losses = []
+
+    def step():
+        net.forward(dom, offsets, ids, ptrs, rows, torch.bfloat16, logits=logits)
+        return tr.step(logits, win, lab, 2, 3)
+
+    for _ in range(warmup):
+        losses.append(float(step()))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        loss = step()
+    e1.record()
+    torch.cuda.synchronize()
+    losses.append(float(loss))
+    ms = e0.elapsed_time(e1) / steps
+    return {"metric": "training samples/s (forward + routed BCE + backward of towers and last-block MLP + SGD)",
+            "value": B / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms, "steps": steps,
+            "trained_parameters": int(tr.bucket.numel() - 1), "loss_first_last": [losses[0], losses[-1]],
+            "launch": "eager (the tower backward reads its domain segment sizes once per step)"}
+
+
 def zipper_timing(steps=20):
     """K5 Zipper (window assignment + labels, full-portfolio shape: 4 tasks x 3 windows) on
     65,536 impressions per step on the GPU, beside the reference's own zip_dataset
@@ -893,6 +937,12 @@ def main():
                                                   "e2e", "clocks")}
             torch.cuda.empty_cache()
         res["zipper"] = zipper_timing()
+        torch.cuda.empty_cache()
+        try:
+            res["train"] = train_timing()
+        except Exception as e:  # informational sub-object: never fail the headline line
+            res["train"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+        torch.cuda.empty_cache()
     if rank == 0:
         if world == 1 and args.workload != "large":
             res["cpu_baseline"] = base(args.cpu_seconds)

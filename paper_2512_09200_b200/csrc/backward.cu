@@ -302,7 +302,13 @@ lattice_status tower_backward(const TowerBwd& a, cudaStream_t st) {
     const size_t zb = sizeof(float) * (size_t)B * th, db = sizeof(__nv_bfloat16) * (size_t)B * th;
     const size_t pb = sizeof(float) * (size_t)G * chunks * heads * th;
     uint8_t* ws = nullptr;
-    LAT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), 2 * zb + db + pb, st));
+    const bool own = !a.scratch;
+    if (own) {
+        LAT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), 2 * zb + db + pb, st));
+    } else {
+        ws = static_cast<uint8_t*>(a.scratch(2 * zb + db + pb));
+        LAT_REQUIRE(ws != nullptr, "tower_backward: workspace allocation failed");
+    }
     float* z = reinterpret_cast<float*>(ws);
     float* h = reinterpret_cast<float*>(ws + zb);
     __nv_bfloat16* dz = reinterpret_cast<__nv_bfloat16*>(ws + 2 * zb);
@@ -347,7 +353,7 @@ lattice_status tower_backward(const TowerBwd& a, cudaStream_t st) {
         return LATTICE_OK;
     };
     const lattice_status s = run();
-    cudaFreeAsync(ws, st);
+    if (own) cudaFreeAsync(ws, st);
     return s;
 }
 
@@ -363,7 +369,13 @@ lattice_status mlp_backward(const MlpBwd& a, cudaStream_t st) {
     for (int i = 1; i <= L; ++i) wmax = a.widths[i] > wmax ? a.widths[i] : wmax;
     const size_t fb = sizeof(float) * (size_t)B * wmax, hb = sizeof(__nv_bfloat16) * (size_t)B * wmax;
     uint8_t* ws = nullptr;
-    LAT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), 2 * fb + hb, st));
+    const bool own = !a.scratch;
+    if (own) {
+        LAT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), 2 * fb + hb, st));
+    } else {
+        ws = static_cast<uint8_t*>(a.scratch(2 * fb + hb));
+        LAT_REQUIRE(ws != nullptr, "mlp_backward: workspace allocation failed");
+    }
     float* z = reinterpret_cast<float*>(ws);           // a pre-activation [B][w] (recomputed)
     float* da = reinterpret_cast<float*>(ws + fb);     // d(loss)/d(a_i) [B][w_i]
     __nv_bfloat16* dz = reinterpret_cast<__nv_bfloat16*>(ws + 2 * fb);  // d(loss)/d(z_i), bf16
@@ -398,7 +410,7 @@ lattice_status mlp_backward(const MlpBwd& a, cudaStream_t st) {
         return LATTICE_OK;
     };
     const lattice_status s = run();
-    cudaFreeAsync(ws, st);
+    if (own) cudaFreeAsync(ws, st);
     return s;
 }
 

@@ -1,6 +1,8 @@
 // backward.h -- host interface of the towers' backward (backward.cu), used by network.cu.
 #pragma once
 
+#include <functional>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -22,6 +24,9 @@ struct TowerBwd {
     float* dW2;                // out [G][heads][th]
     void* dX;                  // optional out [B][nd], domain-sorted rows
     int dx_bf16;
+    // scratch provider (the network's persistent workspace, grown on demand); null: stream-ordered
+    // cudaMallocAsync per call
+    std::function<void*(size_t)> scratch;
 };
 
 lattice_status tower_backward(const TowerBwd& a, cudaStream_t st);
@@ -39,6 +44,7 @@ struct MlpBwd {
     float* dW[5];              // out [widths[i+1]][widths[i]]
     float* dFin;               // optional out [B][widths[0]]
     float* dResid;             // optional out [B][nF*d]
+    std::function<void*(size_t)> scratch;  // as TowerBwd::scratch
 };
 
 lattice_status mlp_backward(const MlpBwd& a, cudaStream_t st);

@@ -15,6 +15,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <cstdlib>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -195,6 +196,10 @@ struct lattice_net {
     bool timing = false;
     std::vector<cudaEvent_t> ev;
     std::vector<void*> allocs;
+    // backward scratch, kept between calls and grown on demand: a stream-ordered allocation per
+    // call returned GBs to the driver at every synchronisation and re-mapped them next time
+    void* bwd_ws = nullptr;
+    size_t bwd_ws_bytes = 0;
 };
 
 namespace {
@@ -515,6 +520,7 @@ lattice_status lattice_net_create(const lattice_net_config* cfg, lattice_net** o
 
 void lattice_net_destroy(lattice_net* net) {
     if (!net) return;
+    if (net->bwd_ws) cudaFree(net->bwd_ws);
     for (void* p : net->allocs) cudaFree(p);
     for (cudaEvent_t e : net->ev) cudaEventDestroy(e);
     delete net;
@@ -576,6 +582,26 @@ lattice_status lattice_net_set_weight(lattice_net* net, int32_t block, int32_t k
     return LATTICE_OK;
 }
 
+namespace {
+// the network's backward scratch (grown with cudaMalloc, which synchronises the device, only when a
+// larger batch or layer needs more)
+std::function<void*(size_t)> net_scratch(lattice_net* net) {
+    return [net](size_t bytes) -> void* {
+        if (net->bwd_ws_bytes < bytes) {
+            if (net->bwd_ws) cudaFree(net->bwd_ws);
+            net->bwd_ws = nullptr;
+            net->bwd_ws_bytes = 0;
+            if (cudaMalloc(&net->bwd_ws, bytes) != cudaSuccess) {
+                net->bwd_ws = nullptr;
+                return nullptr;
+            }
+            net->bwd_ws_bytes = bytes;
+        }
+        return net->bwd_ws;
+    };
+}
+}  // namespace
+
 lattice_status lattice_net_tower_backward(lattice_net* net, int64_t batch, const float* dlogits, float* dW1,
                                           float* dW2, void* dX, int32_t dx_dtype, lattice_stream stream) {
     using namespace lat;
@@ -603,6 +629,7 @@ lattice_status lattice_net_tower_backward(lattice_net* net, int64_t batch, const
     a.dW2 = dW2;
     a.dX = dX;
     a.dx_bf16 = dx_dtype == LATTICE_BF16;
+    a.scratch = net_scratch(net);
     return tower_backward(a, (cudaStream_t)stream);
 }
 
@@ -673,6 +700,7 @@ lattice_status lattice_net_mlp_backward(lattice_net* net, int64_t batch, const f
             a.act[i + 1] = h;
         }
     }
+    a.scratch = net_scratch(net);
     const lattice_status s = mlp_backward(a, st);
     for (void* q : copies) cudaFreeAsync(q, st);
     return s;
